@@ -1,0 +1,526 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native inflight-refactor KV transition.
+
+One "step" = one complete inflight refactor of the BASELINE config-3 workload
+(Llama-2-13B shape, 8->4 stage merge, ~17 GB live paged KV), driven by the
+reference engine's OWN wave plan for it (tests/golden/llama13b_8to4.jsonl,
+extracted from the unmodified reference): wave 0 over every live token, the
+barrier / drain decision, the final post-barrier wave, commit (Eq. 10 check +
+block-table compaction).  All through the kvx C-ABI (include/kvx.h).
+
+  value     KV-refactor GB/s = reference-accounted KV bytes of the step
+            (kv_synced_bytes, engine.cpp:644-684) / device time per step,
+            KV resident in HBM (CUDA events on the transition stream).
+  e2e       same metric through the public API with the control inputs in
+            host memory: kvx_begin (grant + source block table H2D), the wave
+            descriptors H2D, the commit result (violations + compacted block
+            table + free list) D2H, host wall clock.
+  stall_ms  barrier -> commit done (final wave + commit), engine.cpp:676-686.
+  roofline  dominant kernel = kvx_move_kernel of wave 0: algorithmic
+            read+write bytes / its CUDA-event duration vs MEASURED_PEAKS hbm_gbs.
+
+`--impl reference` times the reference's CPU path for the same metric: the
+oracle restatement (oracle/kvx_oracle.c, all host threads) on a bounded
+sample, since the reference itself moves no bytes.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; N>1 via
+torch.distributed.run (one rank per GPU, NVLink P2P through CUDA IPC pools).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2510_11938_b200 import workload as W  # noqa: E402
+
+CONFIGS = {
+    # name: (golden, shape, description)
+    "c3": ("llama13b_8to4", "llama2-13b",
+           "Llama-2-13B shape (40 layers, 40 KV heads, d=128, fp16), 8->4 stage merge, "
+           "256 live requests, ~17 GB paged KV (16-token blocks)"),
+    "c1": ("llama7b_4to2", "llama2-7b",
+           "Llama-2-7B shape (32 layers, 32 KV heads), 4->2 merge, 16 requests, ~4k tokens"),
+    "c2": ("llama7b_2to8", "llama2-7b",
+           "Llama-2-7B shape, 2->8 split, 1024 live requests"),
+    "c4": ("llama70b_8to2to8", "llama2-70b",
+           "Llama-2-70B GQA shape (80 layers, 8 KV heads), 8->2 and 2->8"),
+}
+SEED = 0xB200
+METRIC = "KV-refactor GB/s (% of HBM/NVLink roofline); refactor stall ms at 1/2/4/8 B200"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- placement
+def stage_of(bounds, layer):
+    s = 0
+    for b in bounds:
+        if layer < b:
+            break
+        s += 1
+    return s
+
+
+def placement(L, ob, nb, n_gpus, mode="affinity"):
+    """Logical stages -> physical GPUs.  Old stage k on GPU floor(k*N/K_old);
+    new stage j on the GPU that already holds most of its layers (the
+    reference's warm-start affinity, cluster.cpp:525-536), ties to the lowest
+    id; 'disjoint' shifts every new stage by N/2 GPUs so all its KV crosses
+    NVLink (the reference's disjoint-GPU grant, engine.cpp:584-591)."""
+    k_old, k_new = len(ob) + 1, len(nb) + 1
+    old_dev = [k * n_gpus // k_old for k in range(k_old)]
+    new_dev = []
+    for j, (b, e) in enumerate(W.stage_ranges(L, nb)):
+        share = {}
+        for l in range(b, e):
+            d = old_dev[stage_of(ob, l)]
+            share[d] = share.get(d, 0) + 1
+        best = sorted(share.items(), key=lambda kv: (-kv[1], kv[0]))[0][0]
+        if mode == "disjoint" and n_gpus > 1:
+            best = (best + n_gpus // 2) % n_gpus
+        new_dev.append(best)
+    return old_dev, new_dev
+
+
+def link_bytes(L, ob, nb, old_dev, new_dev, layer_bytes, n_gpus):
+    """Per-GPU (HBM read+write, NVLink out, NVLink in) bytes of one transition
+    given the bytes moved per layer."""
+    hbm = [0] * n_gpus
+    out = [0] * n_gpus
+    inn = [0] * n_gpus
+    for l in range(L):
+        s, d = old_dev[stage_of(ob, l)], new_dev[stage_of(nb, l)]
+        hbm[s] += layer_bytes
+        hbm[d] += layer_bytes
+        if s != d:
+            out[s] += layer_bytes
+            inn[d] += layer_bytes
+    return hbm, out, inn
+
+
+# ------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.err = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception as e:  # nvidia-smi absent
+            self.err = str(e)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0: float, t1: float):
+        if self.err or not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "note": self.err or "no nvidia-smi samples"}
+        sel = [r for (t, r) in self.rows if t0 - 0.06 <= t <= t1 + 0.06] or [r for _, r in self.rows[-3:]]
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in sel:
+            parts = [p.strip() for p in r.split(",")]
+            try:
+                sm.append(float(parts[2]))
+                smax.append(float(parts[3]))
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+class Plan:
+    """The golden transition and everything derived from it."""
+
+    def __init__(self, cfg: str):
+        golden, shape, self.desc = CONFIGS[cfg]
+        self.golden = golden
+        self.scn = W.load_golden(golden)
+        self.t = [t for t in self.scn.transitions if t.outcome == "commit"][-1] if cfg == "c4" \
+            else self.scn.transitions[0]
+        self.L, self.H, self.D = W.SHAPES[shape]
+        self.N = self.scn.num_requests
+        self.tokens = self.t.max_tokens(self.N)
+        self.max_blocks = int(max(1, (self.tokens.max() + 15) // 16))
+        self.src_bt, self.old_blocks = W.fragmented_block_table(self.tokens, self.max_blocks, 16, seed=7)
+        self.dst_blocks = int(((self.tokens + 15) // 16).sum())
+        self.live = np.nonzero(self.tokens)[0].astype(np.int32)
+        self.token_bytes = self.H * self.D * 2
+        self.kv_bytes_per_token = self.scn.kv_bytes_per_token
+        self.step_tokens = sum(int((w.hi - w.lo).clip(min=0).sum()) for w in self.t.waves)
+        self.step_bytes = self.step_tokens * self.kv_bytes_per_token  # reference-accounted
+        w0 = self.t.waves[0]
+        self.wave0_tokens = int((w0.hi - w0.lo).clip(min=0).sum())
+
+
+def run_step(tr, t, stall_ev=None):
+    """One transition through the reference-shaped handlers, in the order the
+    reference engine issued them (engine.cpp:637-713).  stall_ev = (start,
+    end, stream): start is recorded right before the call that issues the
+    final post-barrier wave, end after commit -- the B200 refactor stall."""
+    from paper_2510_11938_b200 import kvx
+    ev = list(t.events)
+    w0 = ev.pop(0)
+    tr.begin_refactor((w0.req, w0.hi))
+    while ev:
+        e = ev.pop(0)
+        if isinstance(e, W.Barrier):
+            if e.inflight_batches > 0:
+                act, _ = tr.on_kv_sync_complete((e.req, e.kv), e.inflight_batches)
+                assert act == kvx.ACT_BARRIER_WAIT, act
+                continue
+            if stall_ev is not None:
+                stall_ev[0].record(stall_ev[2])
+            act, _ = tr.on_kv_sync_complete((e.req, e.kv), 0)
+            assert act == kvx.ACT_FINAL, act
+            ev.pop(0)  # the final wave this handler just issued
+        elif e.final:
+            if stall_ev is not None:
+                stall_ev[0].record(stall_ev[2])
+            act, _ = tr.on_kv_sync_complete((e.req, e.hi), 0)
+            assert act == kvx.ACT_FINAL, act
+        else:
+            act, _ = tr.on_kv_sync_complete((e.req, e.hi), 1)
+            assert act == kvx.ACT_DELTA, act
+    res = tr.on_refactor_commit((t.live_req, t.live_kv))
+    if stall_ev is not None:
+        stall_ev[1].record(stall_ev[2])
+    return res
+
+
+# -------------------------------------------------------------- CPU baseline
+def cpu_sample_run(plan: Plan, steps: int, warmup: int, threads: int, target_bytes: float = 1.0e9):
+    """The oracle executor (oracle/kvx_oracle.c, pthreads) on a bounded sample
+    of the same transition: the first requests whose KV totals ~target_bytes.
+    Returns (GB/s, sample description, bytes per step)."""
+    from oracle import pyoracle as O
+    per_req = plan.tokens * plan.kv_bytes_per_token
+    order = plan.live
+    csum = np.cumsum(per_req[order])
+    nsel = int(np.searchsorted(csum, target_bytes) + 1)
+    sel = np.sort(order[:max(1, nsel)])
+    tokens = np.zeros_like(plan.tokens)
+    tokens[sel] = plan.tokens[sel]
+    src_bt, old_blocks = W.fragmented_block_table(tokens, plan.max_blocks, 16, seed=7)
+    dst_blocks = int(((tokens + 15) // 16).sum())
+    g = O.geo(plan.L, plan.H, plan.D)
+    t = plan.t
+    waves = []
+    for w in t.waves:
+        m = np.isin(w.req, sel)
+        waves.append((w.req[m], w.lo[m], w.hi[m]))
+    step_bytes = sum(int((hi - lo).clip(min=0).sum()) for _, lo, hi in waves) * plan.kv_bytes_per_token
+    dp = O.DataPlane(g, t.old_boundaries, t.new_boundaries, old_blocks, dst_blocks, plan.N,
+                     plan.max_blocks, src_bt)
+    for p in dp.old_pools:  # touch every page (a real KV cache is resident)
+        p[:] = np.arange(p.size, dtype=np.uint64).astype(np.uint8)
+    for p in dp.new_pools:
+        p[:] = 0
+    times = []
+    for s in range(warmup + steps):
+        dp.bt[:] = -1
+        dp.synced_hi[:] = 0
+        dp.d.next_block = 0
+        t0 = time.perf_counter()
+        for req, lo, hi in waves:
+            assert dp.wave(req, lo, hi, threads=threads) == 0
+        live_m = np.isin(t.live_req, sel)
+        dp.commit(t.live_req[live_m], t.live_kv[live_m])
+        if s >= warmup:
+            times.append(time.perf_counter() - t0)
+    gbs = step_bytes * len(times) / sum(times) / 1e9
+    desc = (f"{len(sel)} of {len(plan.live)} live requests of {plan.golden} "
+            f"({step_bytes / 1e9:.2f} GB of KV per step, real geometry), same wave plan, "
+            f"oracle run-granular memcpy on {threads} threads, {len(times)} steps")
+    return gbs, desc, step_bytes
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    plan = Plan(args.config)
+    threads = os.cpu_count() or 1
+    steps = args.steps
+    gbs, desc, step_bytes = cpu_sample_run(plan, steps, max(1, args.warmup), threads)
+    ms = step_bytes / (gbs * 1e9) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16 (u16 words)",
+        "data": "synthetic", "config": {"workload": plan.desc, "golden_wave_plan": plan.golden},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (pipesim) is a simulator that moves no bytes; its CPU path for this "
+                "metric is the oracle restatement executing the identical byte plan",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="kvx", choices=["kvx", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--placement", default="affinity", choices=["affinity", "disjoint"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.warmup < 3:
+        args.warmup = 3
+
+    import torch
+    import torch.distributed as dist
+    from paper_2510_11938_b200 import kvx
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = world
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = local if world > 1 else 0
+
+    plan = Plan(args.config)
+    t = plan.t
+    L = plan.L
+    g = kvx.geometry(L, plan.H, plan.D)
+    old_dev, new_dev = placement(L, t.old_boundaries, t.new_boundaries, n_gpus, args.placement)
+
+    # ---- pools on this GPU; new-stage pools exchanged through CUDA IPC
+    old_pools = [None] * (len(t.old_boundaries) + 1)
+    for k, (b, e) in enumerate(W.stage_ranges(L, t.old_boundaries)):
+        if old_dev[k] == rank:
+            p = kvx.Pool(dev, g, e - b, plan.old_blocks)
+            p.fill_pattern(SEED, b, plan.live, plan.tokens[plan.live], plan.src_bt)
+            old_pools[k] = p
+    new_pools = [None] * (len(t.new_boundaries) + 1)
+    handles = {}
+    for j, (b, e) in enumerate(W.stage_ranges(L, t.new_boundaries)):
+        if new_dev[j] == rank:
+            p = kvx.Pool(dev, g, e - b, plan.dst_blocks)
+            p.zero()
+            new_pools[j] = p
+            if world > 1:
+                handles[j] = p.export_ipc()
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, handles)
+        for r, hs in enumerate(gathered):
+            for j, h in hs.items():
+                if r != rank:
+                    b, e = W.stage_ranges(L, t.new_boundaries)[int(j)]
+                    new_pools[int(j)] = kvx.Pool.import_ipc(dev, h, g, e - b, plan.dst_blocks)
+        dist.barrier()
+
+    stream = torch.cuda.Stream(device=dev)
+    sp = stream.cuda_stream
+
+    def make():
+        return kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, dev,
+                              plan.N, plan.max_blocks, plan.dst_blocks, plan.src_bt, epoch=t.epoch,
+                              max_sync_rounds=plan.scn.max_sync_rounds,
+                              kv_bytes_per_token=plan.kv_bytes_per_token, stream=sp)
+
+    K, Wm = args.steps, args.warmup
+    trs = [make() for _ in range(Wm + K)]
+
+    # ---- warm-up
+    for s in range(Wm):
+        run_step(trs[s], t)
+    torch.cuda.synchronize(dev)
+
+    # ---- correctness gate on the warm-up output (device-side payload check)
+    bad = 0
+    if not args.no_verify:
+        bad = trs[Wm - 1].verify_pattern(SEED, t.live_req, t.live_kv)
+    if world > 1:
+        tb = torch.tensor([bad], dtype=torch.int64, device=dev)
+        dist.all_reduce(tb)
+        bad = int(tb.item())
+    if bad:
+        raise SystemExit(f"bench: destination KV differs from the source payload ({bad} words)")
+
+    # ---- timed region (device-resident KV): K steps
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.3)
+    stall_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), stream)
+                   for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = kvx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
+    ev0.record(stream)
+    for s in range(K):
+        run_step(trs[Wm + s], t, stall_pairs[s])
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    w1 = time.time()
+    launches = kvx.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    sampler.stop()
+    dev_ms = ev0.elapsed_time(ev1)
+    stalls = sorted(a.elapsed_time(b) for a, b, _ in stall_pairs)
+    stall_med = statistics.median(stalls)
+    # dominant kernel: wave-0 move of each timed step
+    mv = [trs[Wm + s].move_timings() for s in range(K)]
+    w0_ms = [m[0][0] for m in mv if m]
+    w0_bytes = mv[0][0][1] if mv and mv[0] else 0
+    w0_avg = sum(w0_ms) / len(w0_ms) if w0_ms else float("nan")
+    all_move_ms = sum(x[0] for m in mv for x in m)
+
+    tm = torch.tensor([dev_ms, stall_med, float(launches), w0_avg, float(w0_bytes)], dtype=torch.float64,
+                      device=dev)
+    if world > 1:
+        mx = tm.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tm.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_ms, stall_med, w0_avg = float(mx[0]), float(mx[1]), float(mx[3])
+        launches = int(sm[2])
+        w0_bytes_total = int(sm[4])
+    else:
+        w0_bytes_total = w0_bytes
+    for tr in trs:
+        tr.close()
+
+    # ---- e2e through the public API (host inputs, results back to host)
+    e2e_steps = args.e2e_steps or K
+    h2d = d2h = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = time.perf_counter()
+    for s in range(e2e_steps):
+        tr = make()  # grant: device state + source block table H2D
+        res = run_step(tr, t)
+        tr.close()
+        if s == 0:
+            n_entries = sum(len(w.req) for w in t.waves)
+            h2d = plan.src_bt.nbytes + n_entries * (4 + 8 + 8) + len(t.live_req) * (4 + 8)
+            d2h = 3 * 8 + res.row_ptr.nbytes + res.blocks.nbytes + res.free_list.nbytes
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - e0
+    if world > 1:
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = peaks()
+    layer_bytes = plan.wave0_tokens * 2 * plan.token_bytes  # K+V bytes per layer in wave 0
+    hbm, out, inn = link_bytes(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev, layer_bytes,
+                               n_gpus)
+    nvl_peak = 770.0  # measured peer copy GB/s per direction (B200_PROFILING.md)
+    t_roof = max(max(h / (peak * 1e9) for h in hbm), max(o / (nvl_peak * 1e9) for o in out),
+                 max(i / (nvl_peak * 1e9) for i in inn))
+    if n_gpus == 1:
+        achieved = w0_bytes / (w0_avg * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "kvx_move_kernel (wave 0)", "bytes_per_launch": w0_bytes,
+                "launch_ms": round(w0_avg, 4), "peak_source": peak_kind}
+    else:
+        frac = t_roof * 1e3 / w0_avg
+        bound = "nvlink" if max(out + inn) / nvl_peak > max(hbm) / peak else "hbm"
+        roof = {"bound": bound, "achieved": round(frac * (peak if bound == "hbm" else nvl_peak), 1),
+                "peak": peak if bound == "hbm" else nvl_peak, "unit": "GB/s", "frac": round(frac, 4),
+                "traffic": None, "kernel": "kvx_move_kernel (wave 0, slowest rank)",
+                "t_roof_ms": round(t_roof * 1e3, 4), "launch_ms": round(w0_avg, 4),
+                "peak_source": f"hbm {peak_kind}; nvlink 770 GB/s measured peer copy"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    value = plan.step_bytes * K / (dev_ms * 1e-3) / 1e9
+    e2e_value = plan.step_bytes * e2e_steps / e2e_s / 1e9
+    clocks = sampler.summary(w0, w1)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": n_gpus, "steps": K,
+        "warmup": Wm, "ms_per_step": round(dev_ms / K, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp16 (u16 words)", "data": "synthetic",
+        "config": {"workload": plan.desc, "golden_wave_plan": plan.golden,
+                   "bytes_per_step": plan.step_bytes, "tokens_per_step": plan.step_tokens,
+                   "placement": {"mode": args.placement, "old_stage_gpu": old_dev, "new_stage_gpu": new_dev},
+                   "l2": "inputs (17 GB) larger than L2 (126 MB); no flush needed"},
+        "stall_ms": round(stall_med, 4), "stall_ms_all": [round(x, 4) for x in (stalls[0], stalls[-1])],
+        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+                "ms_per_step": round(e2e_s * 1e3 / e2e_steps, 4)},
+        "roofline": roof, "gpu_launches": int(launches), "clocks": clocks,
+        "move_kernel_ms_per_step": round(all_move_ms / K, 4),
+    }
+    if n_gpus == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        gbs, desc, _ = cpu_sample_run(plan, 3, 1, threads)
+        line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                                "sample": desc}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

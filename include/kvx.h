@@ -1,0 +1,219 @@
+/*
+ * kvx.h -- C-ABI of the B200-native inflight-refactor KV transition.
+ *
+ * Drop-in data plane for FlexPipe's pipeline-refactoring cache transition
+ * (reference: /root/reference/proj, "pipesim").  The reference engine keeps
+ * its control plane -- which tokens move in which snapshot / delta / final
+ * wave, the barrier, commit and abort -- and calls this library at exactly
+ * the points where it charges simulated KV movement today:
+ *
+ *   kvx_begin / kvx_wave   engine.cpp:633-647  begin_refactor, wave 0
+ *   kvx_wave               engine.cpp:665-674  delta waves
+ *   kvx_wave               engine.cpp:680-687  final post-barrier wave
+ *   kvx_wait               engine.cpp:651-662  KvSyncComplete (wave done)
+ *   kvx_commit             engine.cpp:697-713  final apply + Eq. 10 check
+ *   kvx_abort              engine.cpp:759-772  abort_refactor (revocation)
+ *   kvx_destroy            engine.cpp:747-750  ctx reset after commit
+ *
+ * The kvx_ctl_* entry points additionally restate the reference's
+ * RefactorCtx state machine (engine.hpp:149-158) on the library side, so a
+ * caller that does not keep its own synced/target maps can drive a whole
+ * transition with live (request, kv_tokens) snapshots only.
+ *
+ * Conventions:
+ *   - every function returns an int status (KVX_OK == 0) and never throws;
+ *     kvx_last_error() returns a thread-local message for the last failure;
+ *   - caller arrays are copied before return; the handle owns device memory
+ *     and one CUDA stream; kvx_wait / kvx_commit are the only host syncs;
+ *   - calls on one handle are single-threaded (the engine is);
+ *   - results are deterministic: destination block ids are a pure function
+ *     of the wave inputs;
+ *   - a destination overflow returns KVX_ENOSPC, which the engine maps to a
+ *     refactor hold (engine.cpp:563,592-593), not to an error;
+ *   - an epoch mismatch returns KVX_ESTALE, the analogue of the reference's
+ *     stale-event drop (engine.cpp:654,693).
+ *
+ * HBM layout of one stage pool (per physical GPU):
+ *     pool[layer_local][block][kv][token_in_block][kv_head][head_dim]
+ * so one (layer, block) slab of K and V is 2 * block_tokens * token_bytes
+ * contiguous bytes (320 KiB for Llama-2-13B, 64 KiB for 70B GQA).
+ */
+#ifndef KVX_H
+#define KVX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVX_ABI_VERSION 1
+
+#define KVX_OK 0
+#define KVX_EINVAL (-1)  /* bad argument (null, out of range, unsorted wave) */
+#define KVX_ESTALE (-2)  /* epoch mismatch: event of an aborted/older transition */
+#define KVX_ENOSPC (-3)  /* destination pool or block table full -> refactor hold */
+#define KVX_ECUDA (-4)   /* CUDA runtime / driver failure */
+#define KVX_ESTATE (-5)  /* call out of order (wave after commit, double commit) */
+
+#define KVX_IPC_HANDLE_BYTES 64
+
+const char* kvx_last_error(void);
+int kvx_abi_version(void);
+/* Kernels this library launched in this process (evidence for bench.py). */
+uint64_t kvx_launch_count(void);
+int kvx_device_count(int32_t* out);
+
+/* Model geometry.  token_bytes = num_kv_heads * head_dim * elem_bytes must
+ * be a multiple of 16 (vectorised 16-byte moves).  Replaces the scalar
+ * ExecModelParams::kv_bytes_per_token (modelgraph.hpp:115), which equals
+ * 2 * num_layers * token_bytes. */
+typedef struct kvx_geometry {
+    int32_t num_layers;   /* ops of the chain, one op per decoder layer */
+    int32_t num_kv_heads;
+    int32_t head_dim;
+    int32_t elem_bytes;   /* 2: fp16 / bf16 */
+    int32_t block_tokens; /* paged-KV block size, 16 */
+} kvx_geometry;
+
+/* ------------------------------------------------------------------ pools
+ * One paged KV pool = the KV of one pipeline stage (a contiguous layer range)
+ * on one physical GPU.  Stage k of a plan covers layers [b[k-1], b[k])
+ * (PartitionPlan::boundaries, modelgraph.hpp:45; stage_loads engine.cpp:115). */
+typedef struct kvx_pool kvx_pool;
+
+int kvx_pool_create(int32_t device, const kvx_geometry* g, int32_t num_layers,
+                    int32_t num_blocks, kvx_pool** out);
+/* CUDA IPC handle of a local pool, for a peer process on the same node. */
+int kvx_pool_export(const kvx_pool* p, uint8_t handle[KVX_IPC_HANDLE_BYTES]);
+/* Maps a peer's pool into `device`'s address space (NVLink P2P). */
+int kvx_pool_import(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_BYTES],
+                    const kvx_geometry* g, int32_t num_layers, int32_t num_blocks,
+                    kvx_pool** out);
+int kvx_pool_info(const kvx_pool* p, void** dptr, uint64_t* bytes, int32_t* device,
+                  int32_t* imported);
+int kvx_pool_destroy(kvx_pool* p);
+/* Synchronous helpers for tests and the bench (not on the transition path). */
+int kvx_pool_zero(kvx_pool* p);
+int kvx_pool_read(const kvx_pool* p, uint64_t offset, uint64_t bytes, void* host);
+int kvx_pool_write(kvx_pool* p, uint64_t offset, uint64_t bytes, const void* host);
+/* Writes the deterministic synthetic KV pattern for
+ * tokens [0, tokens[i]) of requests req[i] into the pool, which holds model
+ * layers [first_layer, first_layer + num_layers), through the block table
+ * bt[req * max_blocks + logical_block] (host array). */
+int kvx_pool_fill_pattern(kvx_pool* p, uint64_t seed, int32_t first_layer, int32_t n,
+                          const int32_t* req, const int64_t* tokens, const int32_t* bt,
+                          int32_t max_requests, int32_t max_blocks);
+
+/* ------------------------------------------------------------- transition */
+typedef struct kvx_plan {
+    int32_t num_stages;           /* K */
+    const int32_t* boundaries;    /* K-1 cut indices */
+    kvx_pool* const* pools;       /* K pools; NULL for a remote old stage */
+} kvx_plan;
+
+typedef struct kvx_transition_desc {
+    kvx_geometry geometry;
+    kvx_plan old_plan;            /* source: the serving pipeline */
+    kvx_plan new_plan;            /* destination: every pool required (local or imported) */
+    int32_t device;               /* local GPU: moves every layer whose old pool lives here */
+    int32_t max_requests;         /* request ids are in [0, max_requests) */
+    int32_t max_blocks;           /* logical blocks per request */
+    int32_t dst_num_blocks;       /* block capacity of every new-stage pool */
+    const int32_t* src_block_table; /* host [max_requests * max_blocks], the old pipeline's */
+    uint64_t epoch;               /* InstanceRt::epoch after ++ (engine.cpp:634) */
+    int32_t max_sync_rounds;      /* EngineConfig::max_sync_rounds (engine.hpp:75), kvx_ctl_* */
+    double kv_bytes_per_token;    /* accounting of kvx_ctl_* (engine.cpp:644); 0 = from geometry */
+    void* stream;                 /* cudaStream_t to run on (not owned); NULL = a private stream */
+} kvx_transition_desc;
+
+typedef struct kvx_transition kvx_transition;
+
+/* Grants the destination: allocates the transition state on `device`.
+ * No bytes move until the first kvx_wave. */
+int kvx_begin(const kvx_transition_desc* d, kvx_transition** out);
+
+/* Enqueues one wave: for each entry, tokens [lo[i], hi[i]) of request req[i]
+ * across every layer.  req must be strictly ascending (the std::map order of
+ * RefactorCtx::sync_target, engine.hpp:153-154); entries with lo == hi are
+ * allowed (the reference snapshots zero-delta requests too, engine.cpp:548).
+ * Asynchronous: destination blocks are allocated and the slabs moved by
+ * device kernels on the handle's stream. */
+int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
+             const int64_t* lo, const int64_t* hi);
+/* Blocks until every enqueued wave finished; *measured_ms = device time of
+ * the waves since the previous wait (CUDA events on the handle's stream). */
+int kvx_wait(kvx_transition* t, uint64_t epoch, double* measured_ms);
+
+typedef struct kvx_commit_result {
+    int64_t violations;  /* Eq. 10, engine.cpp:707-713, evaluated on the device */
+    int32_t* row_ptr;    /* optional [n_live + 1]: compacted block table (CSR) */
+    int32_t* blocks;     /* optional [blocks_cap] */
+    int32_t blocks_cap;
+    int32_t n_blocks;    /* out */
+    int32_t* free_list;  /* optional [free_cap]: blocks of requests no longer live */
+    int32_t free_cap;
+    int32_t n_free;      /* out */
+} kvx_commit_result;
+
+/* Final apply + consistency check + block-table compaction for the live
+ * (req, kv_tokens) set, ascending req.  After a successful commit the
+ * destination pools with the returned block table are the stage's KV. */
+int kvx_commit(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t* req,
+               const int64_t* kv_tokens, kvx_commit_result* out);
+/* Drops every destination allocation, invalidates the epoch (++epoch,
+ * engine.cpp:769).  The source pools were never modified. */
+int kvx_abort(kvx_transition* t);
+int kvx_destroy(kvx_transition* t);
+
+/* Introspection: current epoch, and the dense destination block table
+ * [max_requests * max_blocks] (-1 = unallocated). */
+int kvx_epoch(const kvx_transition* t, uint64_t* epoch);
+int kvx_dst_block_table(kvx_transition* t, int32_t* host_out);
+/* Raw CUDA stream (cudaStream_t) of the handle, e.g. to record events. */
+int kvx_stream(const kvx_transition* t, void** stream);
+/* Device time of each move-kernel launch of this handle, in wave order
+ * (CUDA events around the launch itself), and the algorithmic bytes it moved
+ * (read + written).  Fills min(cap, n) entries; *n_out = n.  Synchronises
+ * on the recorded events. */
+int kvx_move_timings(const kvx_transition* t, int32_t cap, double* move_ms, uint64_t* rw_bytes,
+                     int32_t* n_out);
+/* Bytes this handle moved (reads at the source == writes at the destination). */
+int kvx_bytes_moved(const kvx_transition* t, uint64_t* bytes);
+/* Device-side check of the destination pools this handle can see against
+ * the synthetic pattern, tokens [0, kv[i]) of each live request. */
+int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_t* req,
+                       const int64_t* kv, int64_t* mismatched_words);
+
+/* ---------------------------------------------------- control-plane mirror
+ * RefactorCtx (engine.hpp:149-158) restated over the handle.  live = the
+ * (req, kv_tokens) of every live request homed on the instance, ascending
+ * req, i.e. what snapshot_sync_targets iterates (engine.cpp:548-556). */
+enum {
+    KVX_ACT_DELTA = 0,        /* a delta wave was issued (engine.cpp:666-674) */
+    KVX_ACT_BARRIER_WAIT = 1, /* barrier set, pipe still draining (engine.cpp:676-678) */
+    KVX_ACT_FINAL = 2,        /* final wave issued, commit may follow (engine.cpp:680-687) */
+};
+typedef struct kvx_ctl_state {
+    int32_t rounds;
+    int32_t barrier;
+    int32_t commit_scheduled;
+    int32_t waves;
+    double kv_synced_bytes;   /* EngineResult::kv_synced_bytes contribution */
+    int64_t last_wave_tokens;
+} kvx_ctl_state;
+
+int kvx_ctl_begin(kvx_transition* t, int32_t n, const int32_t* req, const int64_t* kv,
+                  int64_t* tokens_out);
+int kvx_ctl_sync_complete(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
+                          const int64_t* kv, int32_t inflight_batches, int32_t* action_out,
+                          int64_t* tokens_out);
+int kvx_ctl_commit(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
+                   const int64_t* kv, kvx_commit_result* out);
+int kvx_ctl_state_get(const kvx_transition* t, kvx_ctl_state* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVX_H */

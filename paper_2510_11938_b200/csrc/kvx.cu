@@ -1,0 +1,770 @@
+// kvx.cu -- host side of the C-ABI (include/kvx.h): pools, transitions,
+// waves, commit/abort.  Device code lives in kvx_kernels.cuh.
+//
+// One handle == one transition of one pipeline instance on one local GPU
+// (RefactorCtx, /root/reference/proj/include/pipesim/engine.hpp:149-158).
+// In a multi-GPU transition every rank opens its own handle over the same
+// plans; each moves the layers whose OLD stage lives on its GPU and pushes
+// them into the destination pools (local, or a peer's through NVLink P2P).
+// The destination block rule is deterministic, so every rank derives the same
+// destination block table without exchanging it.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kvx.h"
+#include "kvx_internal.h"
+#include "kvx_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define KVX_CUDA(call)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(KVX_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+    } while (0)
+
+#define KVX_LAUNCHED()                                                                    \
+    do {                                                                                  \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                               \
+        cudaError_t e_ = cudaGetLastError();                                              \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(KVX_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Restores the caller's current device (torch keeps its own notion of it).
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+bool geometry_ok(const kvx_geometry* g, std::string* why) {
+    if (!g) return *why = "geometry is null", false;
+    if (g->num_layers < 1 || g->num_kv_heads < 1 || g->head_dim < 1 || g->elem_bytes < 1 ||
+        g->block_tokens < 1)
+        return *why = "geometry fields must be positive", false;
+    const uint64_t tb = (uint64_t)g->num_kv_heads * g->head_dim * g->elem_bytes;
+    if (tb % 16 != 0) return *why = "token_bytes must be a multiple of 16", false;
+    return true;
+}
+
+uint64_t token_bytes(const kvx_geometry& g) {
+    return (uint64_t)g.num_kv_heads * (uint64_t)g.head_dim * (uint64_t)g.elem_bytes;
+}
+uint64_t block_bytes(const kvx_geometry& g) { return 2ull * (uint64_t)g.block_tokens * token_bytes(g); }
+
+int64_t cdiv64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int stage_of_layer(const std::vector<int32_t>& b, int32_t layer) {  // modelgraph.cpp:55-62
+    int s = 0;
+    for (int32_t cut : b) {
+        if (layer < cut) break;
+        ++s;
+    }
+    return s;
+}
+int stage_begin(const std::vector<int32_t>& b, int s) { return s == 0 ? 0 : b[(size_t)s - 1]; }
+
+bool plan_ok(const kvx_plan& p, int32_t L, std::string* why, std::vector<int32_t>* out) {
+    if (p.num_stages < 1 || p.num_stages > L) return *why = "num_stages out of range", false;
+    out->assign(p.boundaries, p.boundaries + (p.num_stages - 1));
+    int32_t prev = 0;
+    for (int32_t b : *out) {
+        if (b <= prev || b >= L) return *why = "boundaries must be strictly increasing in (0, L)", false;
+        prev = b;
+    }
+    if (!p.pools) return *why = "plan pools array is null", false;
+    return true;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ types
+struct kvx_pool {
+    int32_t device = -1;
+    bool imported = false;
+    char* base = nullptr;
+    uint64_t bytes = 0;
+    kvx_geometry g{};
+    int32_t num_layers = 0;
+    int32_t num_blocks = 0;
+};
+
+struct kvx_transition {
+    kvx_geometry g{};
+    int32_t device = -1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    int num_sms = 0;
+    int move_ctas_per_sm = 1;
+    std::vector<int32_t> old_b, new_b;
+    std::vector<kvx_pool*> old_pools, new_pools;
+    int32_t max_requests = 0, max_blocks = 0, dst_num_blocks = 0;
+    uint64_t epoch = 0;
+    enum State { kActive, kCommitted, kAborted } state = kActive;
+
+    // device state
+    int32_t* d_src_bt = nullptr;
+    int32_t* d_dst_bt = nullptr;
+    int64_t* d_synced_hi = nullptr;
+    kvx::LayerPtr* d_layers = nullptr;
+    int32_t n_local_layers = 0;
+    bool has_peer_dst = false;
+    // wave staging: pinned host ring of 2 + device buffer
+    char* h_wave[2] = {nullptr, nullptr};
+    cudaEvent_t h_wave_free[2] = {nullptr, nullptr};
+    int wave_slot = 0;
+    char* d_wave = nullptr;
+    kvx::Seg* d_segs = nullptr;
+    int64_t seg_cap = 0;
+    // commit scratch
+    uint8_t* d_live = nullptr;
+    int32_t* d_commit_i32 = nullptr;  // row_ptr | blocks | free_list
+    int64_t commit_i32_cap = 0;
+    int64_t* d_commit_out = nullptr;
+    // timing
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+    bool timing_open = false;
+    // one (start, end) event pair per move-kernel launch of this handle
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> move_ev;
+    std::vector<uint64_t> move_bytes;
+
+    // host mirror of the destination rule (capacity checks are synchronous)
+    std::vector<int64_t> synced_hi;
+    int32_t alloc = 0;
+    uint64_t bytes_moved = 0;       // by this handle (local-source layers)
+    uint64_t bytes_all_layers = 0;  // reference-accounted, all layers
+
+    kvx::CtlState ctl;  // control-plane mirror (kvx_ctl.cpp)
+};
+
+extern "C" {
+
+const char* kvx_last_error(void) { return g_last_error.c_str(); }
+int kvx_abi_version(void) { return KVX_ABI_VERSION; }
+uint64_t kvx_launch_count(void) { return g_launches.load(); }
+
+int kvx_device_count(int32_t* out) {
+    if (!out) return fail(KVX_EINVAL, "out is null");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = 0;
+        return fail(KVX_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    *out = n;
+    return KVX_OK;
+}
+
+// ------------------------------------------------------------------ pools
+int kvx_pool_create(int32_t device, const kvx_geometry* g, int32_t num_layers, int32_t num_blocks,
+                    kvx_pool** out) {
+    std::string why;
+    if (!out) return fail(KVX_EINVAL, "out is null");
+    *out = nullptr;
+    if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
+    if (num_layers < 1 || num_blocks < 1) return fail(KVX_EINVAL, "num_layers/num_blocks must be >= 1");
+    DeviceGuard dg(device);
+    if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed for pool device");
+    auto* p = new kvx_pool;
+    p->device = device;
+    p->g = *g;
+    p->num_layers = num_layers;
+    p->num_blocks = num_blocks;
+    p->bytes = (uint64_t)num_layers * (uint64_t)num_blocks * block_bytes(*g);
+    cudaError_t e = cudaMalloc(&p->base, p->bytes);
+    if (e != cudaSuccess) {
+        delete p;
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? KVX_ENOSPC : KVX_ECUDA,
+                    std::string("pool cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    *out = p;
+    return KVX_OK;
+}
+
+int kvx_pool_export(const kvx_pool* p, uint8_t handle[KVX_IPC_HANDLE_BYTES]) {
+    if (!p || !handle || p->imported) return fail(KVX_EINVAL, "export needs a local pool");
+    static_assert(sizeof(cudaIpcMemHandle_t) == KVX_IPC_HANDLE_BYTES, "ipc handle size");
+    DeviceGuard dg(p->device);
+    cudaIpcMemHandle_t h;
+    KVX_CUDA(cudaIpcGetMemHandle(&h, p->base));
+    std::memcpy(handle, &h, sizeof(h));
+    return KVX_OK;
+}
+
+int kvx_pool_import(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_BYTES],
+                    const kvx_geometry* g, int32_t num_layers, int32_t num_blocks, kvx_pool** out) {
+    std::string why;
+    if (!out || !handle) return fail(KVX_EINVAL, "null argument");
+    *out = nullptr;
+    if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* ptr = nullptr;
+    KVX_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    auto* p = new kvx_pool;
+    p->device = device;
+    p->imported = true;
+    p->base = static_cast<char*>(ptr);
+    p->g = *g;
+    p->num_layers = num_layers;
+    p->num_blocks = num_blocks;
+    p->bytes = (uint64_t)num_layers * (uint64_t)num_blocks * block_bytes(*g);
+    *out = p;
+    return KVX_OK;
+}
+
+int kvx_pool_info(const kvx_pool* p, void** dptr, uint64_t* bytes, int32_t* device,
+                  int32_t* imported) {
+    if (!p) return fail(KVX_EINVAL, "pool is null");
+    if (dptr) *dptr = p->base;
+    if (bytes) *bytes = p->bytes;
+    if (device) *device = p->device;
+    if (imported) *imported = p->imported ? 1 : 0;
+    return KVX_OK;
+}
+
+int kvx_pool_destroy(kvx_pool* p) {
+    if (!p) return KVX_OK;
+    DeviceGuard dg(p->device);
+    cudaError_t e = p->imported ? cudaIpcCloseMemHandle(p->base) : cudaFree(p->base);
+    delete p;
+    if (e != cudaSuccess) return fail(KVX_ECUDA, std::string("pool free: ") + cudaGetErrorString(e));
+    return KVX_OK;
+}
+
+int kvx_pool_zero(kvx_pool* p) {
+    if (!p) return fail(KVX_EINVAL, "pool is null");
+    DeviceGuard dg(p->device);
+    KVX_CUDA(cudaMemset(p->base, 0, p->bytes));
+    KVX_CUDA(cudaDeviceSynchronize());
+    return KVX_OK;
+}
+
+int kvx_pool_read(const kvx_pool* p, uint64_t offset, uint64_t bytes, void* host) {
+    if (!p || !host || offset + bytes > p->bytes) return fail(KVX_EINVAL, "read out of range");
+    DeviceGuard dg(p->device);
+    KVX_CUDA(cudaMemcpy(host, p->base + offset, bytes, cudaMemcpyDeviceToHost));
+    return KVX_OK;
+}
+
+int kvx_pool_write(kvx_pool* p, uint64_t offset, uint64_t bytes, const void* host) {
+    if (!p || !host || offset + bytes > p->bytes) return fail(KVX_EINVAL, "write out of range");
+    DeviceGuard dg(p->device);
+    KVX_CUDA(cudaMemcpy(p->base + offset, host, bytes, cudaMemcpyHostToDevice));
+    return KVX_OK;
+}
+
+int kvx_pool_fill_pattern(kvx_pool* p, uint64_t seed, int32_t first_layer, int32_t n,
+                          const int32_t* req, const int64_t* tokens, const int32_t* bt,
+                          int32_t max_requests, int32_t max_blocks) {
+    if (!p || p->imported) return fail(KVX_EINVAL, "fill needs a local pool");
+    if (n < 0 || (n > 0 && (!req || !tokens || !bt))) return fail(KVX_EINVAL, "null arrays");
+    if (n == 0) return KVX_OK;
+    int64_t max_tok = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (req[i] < 0 || req[i] >= max_requests) return fail(KVX_EINVAL, "req out of range");
+        if (tokens[i] < 0 || cdiv64(tokens[i], p->g.block_tokens) > max_blocks)
+            return fail(KVX_EINVAL, "tokens exceed max_blocks");
+        max_tok = std::max(max_tok, tokens[i]);
+        for (int64_t b = 0; b < cdiv64(tokens[i], p->g.block_tokens); ++b) {
+            const int32_t id = bt[(int64_t)req[i] * max_blocks + b];
+            if (id < 0 || id >= p->num_blocks) return fail(KVX_EINVAL, "block id out of pool range");
+        }
+    }
+    if (max_tok == 0) return KVX_OK;
+    DeviceGuard dg(p->device);
+    int32_t* d_req = nullptr;
+    int64_t* d_tok = nullptr;
+    int32_t* d_bt = nullptr;
+    const size_t bt_bytes = sizeof(int32_t) * (size_t)max_requests * (size_t)max_blocks;
+    KVX_CUDA(cudaMalloc(&d_req, sizeof(int32_t) * n));
+    KVX_CUDA(cudaMalloc(&d_tok, sizeof(int64_t) * n));
+    KVX_CUDA(cudaMalloc(&d_bt, bt_bytes));
+    KVX_CUDA(cudaMemcpy(d_req, req, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    KVX_CUDA(cudaMemcpy(d_tok, tokens, sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    KVX_CUDA(cudaMemcpy(d_bt, bt, bt_bytes, cudaMemcpyHostToDevice));
+    dim3 grid((unsigned)n, (unsigned)cdiv64(max_tok, p->g.block_tokens));
+    kvx::kvx_fill_kernel<<<grid, 256>>>(p->base, p->num_blocks, first_layer, p->num_layers, d_req,
+                                        d_tok, d_bt, max_blocks, p->g.block_tokens,
+                                        token_bytes(p->g), seed);
+    KVX_LAUNCHED();
+    KVX_CUDA(cudaDeviceSynchronize());
+    cudaFree(d_req);
+    cudaFree(d_tok);
+    cudaFree(d_bt);
+    return KVX_OK;
+}
+
+// ------------------------------------------------------------- transition
+int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
+    std::string why;
+    if (!out || !d) return fail(KVX_EINVAL, "null argument");
+    *out = nullptr;
+    if (!geometry_ok(&d->geometry, &why)) return fail(KVX_EINVAL, why);
+    const kvx_geometry& g = d->geometry;
+    std::vector<int32_t> ob, nb;
+    if (!plan_ok(d->old_plan, g.num_layers, &why, &ob)) return fail(KVX_EINVAL, "old plan: " + why);
+    if (!plan_ok(d->new_plan, g.num_layers, &why, &nb)) return fail(KVX_EINVAL, "new plan: " + why);
+    if (d->max_requests < 1 || d->max_blocks < 1 || d->dst_num_blocks < 1)
+        return fail(KVX_EINVAL, "max_requests/max_blocks/dst_num_blocks must be >= 1");
+    if (!d->src_block_table) return fail(KVX_EINVAL, "src_block_table is null");
+    for (int k = 0; k < d->new_plan.num_stages; ++k) {
+        const kvx_pool* p = d->new_plan.pools[k];
+        if (!p) return fail(KVX_EINVAL, "every new-stage pool is required");
+        const int32_t layers = (k + 1 < d->new_plan.num_stages ? nb[(size_t)k] : g.num_layers) -
+                               stage_begin(nb, k);
+        if (p->num_layers != layers) return fail(KVX_EINVAL, "new pool layer count != stage layer range");
+        if (p->num_blocks < d->dst_num_blocks) return fail(KVX_EINVAL, "new pool smaller than dst_num_blocks");
+        if (!p->imported && p->device != d->device) return fail(KVX_EINVAL, "local new pool on another device");
+        if (p->imported && p->device != d->device) return fail(KVX_EINVAL, "imported pool mapped for another device");
+        if (p->g.num_kv_heads != g.num_kv_heads || p->g.head_dim != g.head_dim ||
+            p->g.elem_bytes != g.elem_bytes || p->g.block_tokens != g.block_tokens)
+            return fail(KVX_EINVAL, "new pool geometry mismatch");
+    }
+    for (int k = 0; k < d->old_plan.num_stages; ++k) {
+        const kvx_pool* p = d->old_plan.pools[k];
+        if (!p) continue;
+        const int32_t layers = (k + 1 < d->old_plan.num_stages ? ob[(size_t)k] : g.num_layers) -
+                               stage_begin(ob, k);
+        if (p->num_layers != layers) return fail(KVX_EINVAL, "old pool layer count != stage layer range");
+        if (p->g.num_kv_heads != g.num_kv_heads || p->g.head_dim != g.head_dim ||
+            p->g.elem_bytes != g.elem_bytes || p->g.block_tokens != g.block_tokens)
+            return fail(KVX_EINVAL, "old pool geometry mismatch");
+    }
+    // Validate the source table against the pools it will be read through.
+    const size_t cells = (size_t)d->max_requests * (size_t)d->max_blocks;
+    int32_t min_old_blocks = INT32_MAX;
+    for (int k = 0; k < d->old_plan.num_stages; ++k)
+        if (d->old_plan.pools[k]) min_old_blocks = std::min(min_old_blocks, d->old_plan.pools[k]->num_blocks);
+    for (size_t c = 0; c < cells; ++c) {
+        const int32_t v = d->src_block_table[c];
+        if (v >= min_old_blocks) return fail(KVX_EINVAL, "src_block_table id beyond an old pool");
+    }
+
+    DeviceGuard dg(d->device);
+    if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed");
+    auto* t = new kvx_transition;
+    t->g = g;
+    t->device = d->device;
+    t->old_b = ob;
+    t->new_b = nb;
+    t->old_pools.assign(d->old_plan.pools, d->old_plan.pools + d->old_plan.num_stages);
+    t->new_pools.assign(d->new_plan.pools, d->new_plan.pools + d->new_plan.num_stages);
+    t->max_requests = d->max_requests;
+    t->max_blocks = d->max_blocks;
+    t->dst_num_blocks = d->dst_num_blocks;
+    t->epoch = d->epoch;
+    t->synced_hi.assign((size_t)d->max_requests, 0);
+    t->ctl.init(d->max_requests, d->max_sync_rounds,
+                d->kv_bytes_per_token > 0.0 ? d->kv_bytes_per_token
+                                            : (double)g.num_layers * (double)block_bytes(g) /
+                                                  (double)g.block_tokens);
+    auto bail = [&](int code) {
+        kvx_destroy(t);
+        return code;
+    };
+    if (cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, d->device) != cudaSuccess)
+        return bail(fail(KVX_ECUDA, "query SM count"));
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kvx::kvx_move_kernel, kvx::kMoveThreads, 0) !=
+        cudaSuccess)
+        return bail(fail(KVX_ECUDA, "occupancy query"));
+    t->move_ctas_per_sm = std::max(1, occ);
+    if (d->stream) {
+        t->stream = static_cast<cudaStream_t>(d->stream);
+        t->own_stream = false;
+    } else if (cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        return bail(fail(KVX_ECUDA, "stream create"));
+    }
+    if (cudaEventCreate(&t->ev_begin) != cudaSuccess || cudaEventCreate(&t->ev_end) != cudaSuccess)
+        return bail(fail(KVX_ECUDA, "event create"));
+    const size_t bt_bytes = sizeof(int32_t) * cells;
+    const size_t wave_bytes = (size_t)d->max_requests * (sizeof(int32_t) + 2 * sizeof(int64_t)) + 64;
+    if (cudaMalloc(&t->d_src_bt, bt_bytes) != cudaSuccess || cudaMalloc(&t->d_dst_bt, bt_bytes) != cudaSuccess ||
+        cudaMalloc(&t->d_synced_hi, sizeof(int64_t) * (size_t)d->max_requests) != cudaSuccess ||
+        cudaMalloc(&t->d_wave, wave_bytes) != cudaSuccess ||
+        cudaMalloc(&t->d_live, (size_t)d->max_requests) != cudaSuccess ||
+        cudaMalloc(&t->d_commit_out, 4 * sizeof(int64_t)) != cudaSuccess)
+        return bail(fail(KVX_ENOSPC, "transition state allocation failed"));
+    for (int s = 0; s < 2; ++s)
+        if (cudaMallocHost(&t->h_wave[s], wave_bytes) != cudaSuccess ||
+            cudaEventCreateWithFlags(&t->h_wave_free[s], cudaEventDisableTiming) != cudaSuccess)
+            return bail(fail(KVX_ECUDA, "pinned staging allocation failed"));
+    if (cudaMemcpyAsync(t->d_src_bt, d->src_block_table, bt_bytes, cudaMemcpyHostToDevice, t->stream) !=
+            cudaSuccess ||
+        cudaMemsetAsync(t->d_dst_bt, 0xff, bt_bytes, t->stream) != cudaSuccess ||
+        cudaMemsetAsync(t->d_synced_hi, 0, sizeof(int64_t) * (size_t)d->max_requests, t->stream) !=
+            cudaSuccess)
+        return bail(fail(KVX_ECUDA, "transition state init"));
+
+    // Per-layer slab bases for the layers this GPU sources.
+    std::vector<kvx::LayerPtr> layers;
+    const uint64_t bb = block_bytes(g);
+    for (int32_t l = 0; l < g.num_layers; ++l) {
+        const int so = stage_of_layer(ob, l), sn = stage_of_layer(nb, l);
+        kvx_pool* src = t->old_pools[(size_t)so];
+        if (!src || src->imported || src->device != d->device) continue;
+        kvx_pool* dst = t->new_pools[(size_t)sn];
+        const uint64_t ls = (uint64_t)(l - stage_begin(ob, so)) * (uint64_t)src->num_blocks * bb;
+        const uint64_t ld = (uint64_t)(l - stage_begin(nb, sn)) * (uint64_t)dst->num_blocks * bb;
+        layers.push_back({src->base + ls, dst->base + ld});
+        if (dst->imported) t->has_peer_dst = true;
+    }
+    t->n_local_layers = (int32_t)layers.size();
+    if (!layers.empty()) {
+        if (cudaMalloc(&t->d_layers, sizeof(kvx::LayerPtr) * layers.size()) != cudaSuccess ||
+            cudaMemcpyAsync(t->d_layers, layers.data(), sizeof(kvx::LayerPtr) * layers.size(),
+                            cudaMemcpyHostToDevice, t->stream) != cudaSuccess)
+            return bail(fail(KVX_ECUDA, "layer table upload"));
+    }
+    if (cudaStreamSynchronize(t->stream) != cudaSuccess) return bail(fail(KVX_ECUDA, "init sync"));
+    *out = t;
+    return KVX_OK;
+}
+
+int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, const int64_t* lo,
+             const int64_t* hi) {
+    if (!t) return fail(KVX_EINVAL, "transition is null");
+    if (epoch != t->epoch) return fail(KVX_ESTALE, "stale epoch");
+    if (t->state != kvx_transition::kActive) return fail(KVX_ESTATE, "transition is not active");
+    if (n < 0 || n > t->max_requests || (n > 0 && (!req || !lo || !hi)))
+        return fail(KVX_EINVAL, "bad wave arrays");
+    // Validate against the host mirror of the destination rule.
+    const int64_t B = t->g.block_tokens;
+    int64_t nseg = 0, new_blocks = 0, tokens = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t r = req[i];
+        if (r < 0 || r >= t->max_requests) return fail(KVX_EINVAL, "req out of range");
+        if (i > 0 && req[i - 1] >= r) return fail(KVX_EINVAL, "wave requests must be strictly ascending");
+        if (hi[i] <= lo[i]) continue;
+        const int64_t s = t->synced_hi[(size_t)r];
+        if (lo[i] < 0 || lo[i] > s) return fail(KVX_EINVAL, "wave interval leaves a gap (lo > synced)");
+        if (cdiv64(hi[i], B) > t->max_blocks) return fail(KVX_ENOSPC, "request exceeds max_blocks");
+        new_blocks += std::max<int64_t>(0, cdiv64(hi[i], B) - cdiv64(s, B));
+        nseg += cdiv64(hi[i], B) - lo[i] / B;
+        tokens += hi[i] - lo[i];
+    }
+    if ((int64_t)t->alloc + new_blocks > t->dst_num_blocks)
+        return fail(KVX_ENOSPC, "destination pools full");
+    DeviceGuard dg(t->device);
+    if (n == 0 || nseg == 0) return KVX_OK;
+    if (nseg > t->seg_cap) {
+        if (t->d_segs) {
+            KVX_CUDA(cudaStreamSynchronize(t->stream));
+            cudaFree(t->d_segs);
+            t->d_segs = nullptr;
+        }
+        const int64_t cap = std::max<int64_t>(nseg, 2 * t->seg_cap);
+        KVX_CUDA(cudaMalloc(&t->d_segs, sizeof(kvx::Seg) * (size_t)cap));
+        t->seg_cap = cap;
+    }
+    // Stage (req | lo | hi) into pinned memory; the slot's previous upload
+    // must have been consumed first.
+    const int slot = t->wave_slot;
+    t->wave_slot ^= 1;
+    KVX_CUDA(cudaEventSynchronize(t->h_wave_free[slot]));
+    char* h = t->h_wave[slot];
+    const size_t off_lo = (((size_t)t->max_requests * sizeof(int32_t)) + 15) & ~size_t(15);
+    const size_t off_hi = off_lo + (size_t)t->max_requests * sizeof(int64_t);
+    std::memcpy(h, req, sizeof(int32_t) * n);
+    std::memcpy(h + off_lo, lo, sizeof(int64_t) * n);
+    std::memcpy(h + off_hi, hi, sizeof(int64_t) * n);
+    if (!t->timing_open) {
+        KVX_CUDA(cudaEventRecord(t->ev_begin, t->stream));
+        t->timing_open = true;
+    }
+    // One H2D copy covering the three arrays at their fixed offsets.
+    KVX_CUDA(cudaMemcpyAsync(t->d_wave, h, off_hi + sizeof(int64_t) * n, cudaMemcpyHostToDevice, t->stream));
+    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
+    const int32_t* d_req = reinterpret_cast<const int32_t*>(t->d_wave);
+    const int64_t* d_lo = reinterpret_cast<const int64_t*>(t->d_wave + off_lo);
+    const int64_t* d_hi = reinterpret_cast<const int64_t*>(t->d_wave + off_hi);
+    kvx::kvx_plan_kernel<<<1, kvx::kPlanThreads, 0, t->stream>>>(
+        d_req, d_lo, d_hi, n, t->d_src_bt, t->d_dst_bt, t->d_synced_hi, t->max_blocks,
+        t->g.block_tokens, t->alloc, t->d_segs);
+    KVX_LAUNCHED();
+    if (t->n_local_layers > 0) {
+        const int64_t units = nseg * t->n_local_layers;
+        const int64_t full = (int64_t)t->num_sms * t->move_ctas_per_sm;
+        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full));
+        std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+        KVX_CUDA(cudaEventCreate(&ev.first));
+        KVX_CUDA(cudaEventCreate(&ev.second));
+        t->move_ev.push_back(ev);
+        t->move_bytes.push_back(2ull * (uint64_t)tokens * 2ull * token_bytes(t->g) *
+                                (uint64_t)t->n_local_layers);
+        KVX_CUDA(cudaEventRecord(ev.first, t->stream));
+        kvx::kvx_move_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
+            t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
+            token_bytes(t->g), t->g.block_tokens, t->has_peer_dst ? 1 : 0);
+        KVX_LAUNCHED();
+        KVX_CUDA(cudaEventRecord(ev.second, t->stream));
+    }
+    KVX_CUDA(cudaEventRecord(t->ev_end, t->stream));
+    // Commit the mirror only once every launch was accepted.
+    for (int32_t i = 0; i < n; ++i)
+        if (hi[i] > t->synced_hi[(size_t)req[i]]) t->synced_hi[(size_t)req[i]] = hi[i];
+    t->alloc += (int32_t)new_blocks;
+    t->bytes_moved += (uint64_t)tokens * 2ull * token_bytes(t->g) * (uint64_t)t->n_local_layers;
+    t->bytes_all_layers += (uint64_t)tokens * 2ull * token_bytes(t->g) * (uint64_t)t->g.num_layers;
+    return KVX_OK;
+}
+
+int kvx_wait(kvx_transition* t, uint64_t epoch, double* measured_ms) {
+    if (!t) return fail(KVX_EINVAL, "transition is null");
+    if (epoch != t->epoch) return fail(KVX_ESTALE, "stale epoch");
+    DeviceGuard dg(t->device);
+    KVX_CUDA(cudaStreamSynchronize(t->stream));
+    float ms = 0.f;
+    if (t->timing_open) {
+        KVX_CUDA(cudaEventElapsedTime(&ms, t->ev_begin, t->ev_end));
+        t->timing_open = false;
+    }
+    if (measured_ms) *measured_ms = ms;
+    return KVX_OK;
+}
+
+int kvx_commit(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t* req,
+               const int64_t* kv_tokens, kvx_commit_result* out) {
+    if (!t) return fail(KVX_EINVAL, "transition is null");
+    if (epoch != t->epoch) return fail(KVX_ESTALE, "stale epoch");
+    if (t->state != kvx_transition::kActive) return fail(KVX_ESTATE, "transition is not active");
+    if (n_live < 0 || n_live > t->max_requests || (n_live > 0 && (!req || !kv_tokens)))
+        return fail(KVX_EINVAL, "bad live arrays");
+    for (int32_t i = 0; i < n_live; ++i) {
+        if (req[i] < 0 || req[i] >= t->max_requests) return fail(KVX_EINVAL, "req out of range");
+        if (i > 0 && req[i - 1] >= req[i]) return fail(KVX_EINVAL, "live requests must be strictly ascending");
+    }
+    DeviceGuard dg(t->device);
+    // Exact output sizes from the host mirror (synced_hi is mirrored).
+    const int64_t B = t->g.block_tokens;
+    std::vector<uint8_t> live((size_t)t->max_requests, 0);
+    int64_t nb_live = 0, nb_free = 0;
+    for (int32_t i = 0; i < n_live; ++i) {
+        live[(size_t)req[i]] = 1;
+        nb_live += cdiv64(t->synced_hi[(size_t)req[i]], B);
+    }
+    for (int32_t r = 0; r < t->max_requests; ++r)
+        if (!live[(size_t)r]) nb_free += cdiv64(t->synced_hi[(size_t)r], B);
+    const int64_t need = (n_live + 1) + nb_live + nb_free;
+    if (need > t->commit_i32_cap) {
+        if (t->d_commit_i32) cudaFree(t->d_commit_i32);
+        t->d_commit_i32 = nullptr;
+        KVX_CUDA(cudaMalloc(&t->d_commit_i32, sizeof(int32_t) * (size_t)std::max<int64_t>(need, 1)));
+        t->commit_i32_cap = need;
+    }
+    int32_t* d_row_ptr = t->d_commit_i32;
+    int32_t* d_blocks = d_row_ptr + (n_live + 1);
+    int32_t* d_free = d_blocks + nb_live;
+    // Reuse the wave staging for the live set.
+    const int slot = t->wave_slot;
+    t->wave_slot ^= 1;
+    KVX_CUDA(cudaEventSynchronize(t->h_wave_free[slot]));
+    char* h = t->h_wave[slot];
+    const size_t off_kv = (((size_t)t->max_requests * sizeof(int32_t)) + 15) & ~size_t(15);
+    if (n_live > 0) {
+        std::memcpy(h, req, sizeof(int32_t) * n_live);
+        std::memcpy(h + off_kv, kv_tokens, sizeof(int64_t) * n_live);
+        KVX_CUDA(cudaMemcpyAsync(t->d_wave, h, off_kv + sizeof(int64_t) * n_live, cudaMemcpyHostToDevice,
+                                 t->stream));
+    }
+    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
+    kvx::kvx_commit_kernel<<<1, kvx::kCommitThreads, 0, t->stream>>>(
+        reinterpret_cast<const int32_t*>(t->d_wave), reinterpret_cast<const int64_t*>(t->d_wave + off_kv),
+        n_live, t->d_dst_bt, t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens,
+        d_row_ptr, d_blocks, d_free, t->d_commit_out);
+    KVX_LAUNCHED();
+    int64_t res[3] = {0, 0, 0};
+    KVX_CUDA(cudaMemcpyAsync(res, t->d_commit_out, sizeof(res), cudaMemcpyDeviceToHost, t->stream));
+    if (out && out->row_ptr && n_live + 1 > 0)
+        KVX_CUDA(cudaMemcpyAsync(out->row_ptr, d_row_ptr, sizeof(int32_t) * (size_t)(n_live + 1),
+                                 cudaMemcpyDeviceToHost, t->stream));
+    if (out && out->blocks && nb_live > 0) {
+        if (out->blocks_cap < nb_live) return fail(KVX_EINVAL, "blocks_cap too small");
+        KVX_CUDA(cudaMemcpyAsync(out->blocks, d_blocks, sizeof(int32_t) * (size_t)nb_live,
+                                 cudaMemcpyDeviceToHost, t->stream));
+    }
+    if (out && out->free_list && nb_free > 0) {
+        if (out->free_cap < nb_free) return fail(KVX_EINVAL, "free_cap too small");
+        KVX_CUDA(cudaMemcpyAsync(out->free_list, d_free, sizeof(int32_t) * (size_t)nb_free,
+                                 cudaMemcpyDeviceToHost, t->stream));
+    }
+    KVX_CUDA(cudaStreamSynchronize(t->stream));
+    if (res[1] != nb_live || res[2] != nb_free)
+        return fail(KVX_ECUDA, "device compaction disagrees with the host mirror");
+    if (out) {
+        out->violations = res[0];
+        out->n_blocks = (int32_t)res[1];
+        out->n_free = (int32_t)res[2];
+    }
+    t->state = kvx_transition::kCommitted;
+    ++t->epoch;  // engine.cpp:752
+    t->timing_open = false;
+    return KVX_OK;
+}
+
+int kvx_abort(kvx_transition* t) {
+    if (!t) return fail(KVX_EINVAL, "transition is null");
+    if (t->state != kvx_transition::kActive) return fail(KVX_ESTATE, "transition is not active");
+    DeviceGuard dg(t->device);
+    KVX_CUDA(cudaStreamSynchronize(t->stream));  // in-flight waves land in pools we now drop
+    t->state = kvx_transition::kAborted;
+    ++t->epoch;  // engine.cpp:769
+    t->alloc = 0;
+    std::fill(t->synced_hi.begin(), t->synced_hi.end(), 0);
+    const size_t bt_bytes = sizeof(int32_t) * (size_t)t->max_requests * (size_t)t->max_blocks;
+    KVX_CUDA(cudaMemsetAsync(t->d_dst_bt, 0xff, bt_bytes, t->stream));
+    KVX_CUDA(cudaMemsetAsync(t->d_synced_hi, 0, sizeof(int64_t) * (size_t)t->max_requests, t->stream));
+    KVX_CUDA(cudaStreamSynchronize(t->stream));
+    t->timing_open = false;
+    return KVX_OK;
+}
+
+int kvx_destroy(kvx_transition* t) {
+    if (!t) return KVX_OK;
+    DeviceGuard dg(t->device);
+    if (t->stream) cudaStreamSynchronize(t->stream);
+    cudaFree(t->d_src_bt);
+    cudaFree(t->d_dst_bt);
+    cudaFree(t->d_synced_hi);
+    cudaFree(t->d_layers);
+    cudaFree(t->d_wave);
+    cudaFree(t->d_segs);
+    cudaFree(t->d_live);
+    cudaFree(t->d_commit_i32);
+    cudaFree(t->d_commit_out);
+    for (int s = 0; s < 2; ++s) {
+        if (t->h_wave[s]) cudaFreeHost(t->h_wave[s]);
+        if (t->h_wave_free[s]) cudaEventDestroy(t->h_wave_free[s]);
+    }
+    if (t->ev_begin) cudaEventDestroy(t->ev_begin);
+    if (t->ev_end) cudaEventDestroy(t->ev_end);
+    for (auto& ev : t->move_ev) {
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    if (t->stream && t->own_stream) cudaStreamDestroy(t->stream);
+    delete t;
+    return KVX_OK;
+}
+
+int kvx_epoch(const kvx_transition* t, uint64_t* epoch) {
+    if (!t || !epoch) return fail(KVX_EINVAL, "null argument");
+    *epoch = t->epoch;
+    return KVX_OK;
+}
+
+int kvx_dst_block_table(kvx_transition* t, int32_t* host_out) {
+    if (!t || !host_out) return fail(KVX_EINVAL, "null argument");
+    DeviceGuard dg(t->device);
+    KVX_CUDA(cudaMemcpyAsync(host_out, t->d_dst_bt,
+                             sizeof(int32_t) * (size_t)t->max_requests * (size_t)t->max_blocks,
+                             cudaMemcpyDeviceToHost, t->stream));
+    KVX_CUDA(cudaStreamSynchronize(t->stream));
+    return KVX_OK;
+}
+
+int kvx_stream(const kvx_transition* t, void** stream) {
+    if (!t || !stream) return fail(KVX_EINVAL, "null argument");
+    *stream = t->stream;
+    return KVX_OK;
+}
+
+int kvx_move_timings(const kvx_transition* t, int32_t cap, double* move_ms, uint64_t* rw_bytes,
+                     int32_t* n_out) {
+    if (!t || !n_out || cap < 0) return fail(KVX_EINVAL, "bad arguments");
+    DeviceGuard dg(t->device);
+    const int32_t n = (int32_t)t->move_ev.size();
+    for (int32_t i = 0; i < n && i < cap; ++i) {
+        float ms = 0.f;
+        KVX_CUDA(cudaEventSynchronize(t->move_ev[(size_t)i].second));
+        KVX_CUDA(cudaEventElapsedTime(&ms, t->move_ev[(size_t)i].first, t->move_ev[(size_t)i].second));
+        if (move_ms) move_ms[i] = ms;
+        if (rw_bytes) rw_bytes[i] = t->move_bytes[(size_t)i];
+    }
+    *n_out = n;
+    return KVX_OK;
+}
+
+int kvx_bytes_moved(const kvx_transition* t, uint64_t* bytes) {
+    if (!t || !bytes) return fail(KVX_EINVAL, "null argument");
+    *bytes = t->bytes_moved;
+    return KVX_OK;
+}
+
+int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_t* req,
+                       const int64_t* kv, int64_t* mismatched_words) {
+    if (!t || !mismatched_words || n < 0 || (n > 0 && (!req || !kv))) return fail(KVX_EINVAL, "bad arguments");
+    *mismatched_words = 0;
+    if (n == 0) return KVX_OK;
+    DeviceGuard dg(t->device);
+    int64_t max_tok = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (req[i] < 0 || req[i] >= t->max_requests) return fail(KVX_EINVAL, "req out of range");
+        if (kv[i] < 0 || cdiv64(kv[i], t->g.block_tokens) > t->max_blocks)
+            return fail(KVX_EINVAL, "kv exceeds max_blocks");
+        max_tok = std::max(max_tok, kv[i]);
+    }
+    if (max_tok == 0) return KVX_OK;
+    int32_t* d_req = nullptr;
+    int64_t* d_kv = nullptr;
+    unsigned long long* d_bad = nullptr;
+    KVX_CUDA(cudaMalloc(&d_req, sizeof(int32_t) * n));
+    KVX_CUDA(cudaMalloc(&d_kv, sizeof(int64_t) * n));
+    KVX_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+    KVX_CUDA(cudaMemcpyAsync(d_req, req, sizeof(int32_t) * n, cudaMemcpyHostToDevice, t->stream));
+    KVX_CUDA(cudaMemcpyAsync(d_kv, kv, sizeof(int64_t) * n, cudaMemcpyHostToDevice, t->stream));
+    KVX_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), t->stream));
+    dim3 grid((unsigned)n, (unsigned)cdiv64(max_tok, t->g.block_tokens));
+    for (size_t k = 0; k < t->new_pools.size(); ++k) {
+        const kvx_pool* p = t->new_pools[k];
+        if (p->imported) continue;  // the owning rank verifies it
+        kvx::kvx_verify_kernel<<<grid, 256, 0, t->stream>>>(
+            p->base, p->num_blocks, stage_begin(t->new_b, (int)k), p->num_layers, d_req, d_kv,
+            t->d_dst_bt, t->max_blocks, t->g.block_tokens, token_bytes(t->g), seed, d_bad);
+        KVX_LAUNCHED();
+    }
+    unsigned long long bad = 0;
+    KVX_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, t->stream));
+    KVX_CUDA(cudaStreamSynchronize(t->stream));
+    cudaFree(d_req);
+    cudaFree(d_kv);
+    cudaFree(d_bad);
+    *mismatched_words = (int64_t)bad;
+    return KVX_OK;
+}
+
+}  // extern "C"
+
+// ----------------------------------------------- hooks for kvx_ctl.cpp
+namespace kvx {
+CtlState& ctl_of(kvx_transition* t) { return t->ctl; }
+const CtlState& ctl_of(const kvx_transition* t) { return t->ctl; }
+uint64_t epoch_of(const kvx_transition* t) { return t->epoch; }
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace kvx

@@ -1,0 +1,360 @@
+// kvx_kernels.cuh -- sm_100a device code of the inflight-refactor KV transition.
+//
+// Kernels (all launched on the transition's own stream):
+//   kvx_plan_kernel    one CTA: destination block allocation (block-wide
+//                      exclusive scan of per-request new-block counts),
+//                      block-table rewrite, synced high-water marks and the
+//                      per-block copy segments of the wave.  Restates the
+//                      "which tokens move" half of engine.cpp:637-687 at
+//                      block granularity.
+//   kvx_move_kernel    persistent grid (SMs x resident CTAs): one
+//                      (segment, layer) slab per CTA iteration, 16-byte
+//                      vectorised coalesced loads/stores, 8 loads in flight
+//                      per thread.  Writes through peer pointers when the
+//                      destination pool is another GPU's (NVLink P2P push).
+//   kvx_bulk_kernel    same work list, TMA bulk engine path: one elected
+//                      thread per CTA streams slabs global -> shared ->
+//                      global with cp.async.bulk + mbarrier, multi-stage ring.
+//   kvx_commit_kernel  one CTA: Eq. 10 check per live request
+//                      (engine.cpp:707-713) with warp ballots, block-table
+//                      compaction of live rows (CSR) and free-list build for
+//                      rows that are no longer live (ballot + prefix scan).
+//   kvx_fill_kernel / kvx_verify_kernel   synthetic payload (test + bench).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kvx {
+
+struct Seg {  // one logical block of one request inside one wave
+    int32_t src_blk;
+    int32_t dst_blk;
+    int32_t t0;  // first token inside the block
+    int32_t t1;  // one past the last token
+};
+
+struct LayerPtr {  // base of layer l's slab array in the old / new pool
+    char* src;
+    char* dst;
+};
+
+// ---------------------------------------------------------------- payload
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t token_hash(uint64_t seed, int32_t req, int32_t layer,
+                                                        int32_t kv, int64_t tok) {
+    uint64_t h = mix64(seed ^ (uint64_t)(uint32_t)req);
+    h = mix64(h ^ (((uint64_t)(uint32_t)layer << 1) | (uint64_t)(kv & 1)));
+    return mix64(h ^ (uint64_t)tok);
+}
+__host__ __device__ __forceinline__ uint32_t word(uint64_t th, uint32_t w) {
+    return (uint32_t)(((th + (uint64_t)w * 0x9E3779B97F4A7C15ull) * 0xBF58476D1CE4E5B9ull) >> 48);
+}
+__device__ __forceinline__ uint4 pattern_vec(uint64_t th, uint32_t vec) {
+    const uint32_t w = vec * 8u;
+    uint4 v;
+    v.x = word(th, w + 0) | (word(th, w + 1) << 16);
+    v.y = word(th, w + 2) | (word(th, w + 3) << 16);
+    v.z = word(th, w + 4) | (word(th, w + 5) << 16);
+    v.w = word(th, w + 6) | (word(th, w + 7) << 16);
+    return v;
+}
+
+// ------------------------------------------------------------ scan helper
+// Block-wide exclusive scan of two int32 counters at once (1024 threads).
+template <int kThreads>
+__device__ __forceinline__ int2 block_exclusive_scan2(int2 v, int2* total) {
+    static_assert(kThreads % 32 == 0 && kThreads <= 1024, "threads");
+    __shared__ int2 warp_sums[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int2 inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int ax = __shfl_up_sync(0xffffffffu, inc.x, d);
+        const int ay = __shfl_up_sync(0xffffffffu, inc.y, d);
+        if (lane >= d) {
+            inc.x += ax;
+            inc.y += ay;
+        }
+    }
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int2 s = lane < kThreads / 32 ? warp_sums[lane] : make_int2(0, 0);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int ax = __shfl_up_sync(0xffffffffu, s.x, d);
+            const int ay = __shfl_up_sync(0xffffffffu, s.y, d);
+            if (lane >= d) {
+                s.x += ax;
+                s.y += ay;
+            }
+        }
+        warp_sums[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const int2 before = wid > 0 ? warp_sums[wid - 1] : make_int2(0, 0);
+    *total = warp_sums[kThreads / 32 - 1];
+    __syncthreads();  // warp_sums reused by the next call
+    return make_int2(before.x + inc.x - v.x, before.y + inc.y - v.y);
+}
+
+__device__ __forceinline__ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// -------------------------------------------------------------- planning
+constexpr int kPlanThreads = 1024;
+
+// Wave entries are strictly ascending request ids (validated on the host),
+// so rows never collide.  Destination rule: the new blocks of a request are
+// logical blocks [ceil(synced_hi/B), ceil(hi/B)); their ids are the bump
+// pointer plus the exclusive scan of the per-entry counts, in entry order.
+__global__ void __launch_bounds__(kPlanThreads, 1)
+kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
+                const int64_t* __restrict__ hi, int32_t n, const int32_t* __restrict__ src_bt,
+                int32_t* __restrict__ dst_bt, int64_t* __restrict__ synced_hi, int32_t max_blocks,
+                int32_t block_tokens, int32_t alloc_base, Seg* __restrict__ segs) {
+    const int64_t B = block_tokens;
+    int2 carry = make_int2(0, 0);
+    for (int32_t base = 0; base < n; base += kPlanThreads) {
+        const int32_t i = base + (int32_t)threadIdx.x;
+        int32_t r = -1;
+        int64_t l = 0, h = 0, s = 0;
+        int2 cnt = make_int2(0, 0);  // (new blocks, segments)
+        if (i < n) {
+            r = req[i];
+            l = lo[i];
+            h = hi[i];
+            s = synced_hi[r];
+            if (h > l) {
+                const int64_t have = cdiv(s, B), need = cdiv(h, B);
+                cnt.x = need > have ? (int32_t)(need - have) : 0;
+                cnt.y = (int32_t)(need - l / B);
+            }
+        }
+        int2 tot;
+        const int2 off = block_exclusive_scan2<kPlanThreads>(cnt, &tot);
+        if (i < n && h > l) {
+            int32_t* row = dst_bt + (int64_t)r * max_blocks;
+            const int32_t* srow = src_bt + (int64_t)r * max_blocks;
+            const int64_t have = cdiv(s, B);
+            for (int32_t k = 0; k < cnt.x; ++k) row[have + k] = alloc_base + carry.x + off.x + k;
+            if (h > s) synced_hi[r] = h;
+            const int64_t b0 = l / B;
+            Seg* out = segs + carry.y + off.y;
+            for (int32_t k = 0; k < cnt.y; ++k) {
+                const int64_t b = b0 + k;
+                const int64_t t0 = l > b * B ? l - b * B : 0;
+                const int64_t t1 = h < (b + 1) * B ? h - b * B : B;
+                out[k] = Seg{srow[b], row[b], (int32_t)t0, (int32_t)t1};
+            }
+        }
+        carry.x += tot.x;
+        carry.y += tot.y;
+    }
+}
+
+// ------------------------------------------------------------ LSU mover
+constexpr int kMoveThreads = 512;
+constexpr int kMoveUnroll = 8;
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// CTA-cooperative copy of nvec 16-byte vectors.
+__device__ __forceinline__ void cta_copy(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                         uint32_t nvec) {
+    uint32_t i = threadIdx.x;
+    const uint32_t step = kMoveThreads * kMoveUnroll;
+    for (; i + (kMoveUnroll - 1) * kMoveThreads < nvec; i += step) {
+        uint4 v[kMoveUnroll];
+#pragma unroll
+        for (int u = 0; u < kMoveUnroll; ++u) v[u] = ld_stream(src + i + u * kMoveThreads);
+#pragma unroll
+        for (int u = 0; u < kMoveUnroll; ++u) st_stream(dst + i + u * kMoveThreads, v[u]);
+    }
+    for (; i < nvec; i += kMoveThreads) st_stream(dst + i, ld_stream(src + i));
+}
+
+// Work unit u -> (layer = u / nseg, segment = u % nseg): consecutive CTAs walk
+// consecutive destination blocks of one layer (the dense rule makes them
+// contiguous), sources are wherever the old block table points.
+__global__ void __launch_bounds__(kMoveThreads)
+kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
+                int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
+                int32_t fence_system) {
+    const int64_t units = (int64_t)nseg * nlayers;
+    const uint64_t half = block_bytes >> 1;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t layer = (int32_t)(u / nseg);
+        const Seg sg = segs[u - (int64_t)layer * nseg];
+        const LayerPtr lp = layers[layer];
+        const char* src = lp.src + (uint64_t)sg.src_blk * block_bytes;
+        char* dst = lp.dst + (uint64_t)sg.dst_blk * block_bytes;
+        if (sg.t0 == 0 && sg.t1 == block_tokens) {
+            cta_copy(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src),
+                     (uint32_t)(block_bytes >> 4));
+        } else {
+            const uint64_t off = (uint64_t)sg.t0 * token_bytes;
+            const uint32_t nvec = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * token_bytes) >> 4);
+            cta_copy(reinterpret_cast<uint4*>(dst + off), reinterpret_cast<const uint4*>(src + off),
+                     nvec);
+            cta_copy(reinterpret_cast<uint4*>(dst + half + off),
+                     reinterpret_cast<const uint4*>(src + half + off), nvec);
+        }
+    }
+    if (fence_system) __threadfence_system();  // peer (NVLink) stores visible before host sync
+}
+
+// ------------------------------------------------------------- commit
+constexpr int kCommitThreads = 1024;
+
+// Phase A (this kernel, one CTA): live flags, Eq. 10 violations, CSR row
+// pointers and free-list offsets; phase B writes the blocks (same kernel,
+// after the scans).  live_flag is a scratch [max_requests] array.
+__global__ void __launch_bounds__(kCommitThreads, 1)
+kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ kv, int32_t n,
+                  const int32_t* __restrict__ dst_bt, const int64_t* __restrict__ synced_hi,
+                  uint8_t* __restrict__ live_flag, int32_t max_requests, int32_t max_blocks,
+                  int32_t block_tokens, int32_t* __restrict__ row_ptr,
+                  int32_t* __restrict__ blocks, int32_t* __restrict__ free_list,
+                  int64_t* __restrict__ out /* [0]=violations [1]=n_blocks [2]=n_free */) {
+    __shared__ unsigned long long s_viol;
+    if (threadIdx.x == 0) s_viol = 0;
+    for (int32_t r = threadIdx.x; r < max_requests; r += kCommitThreads) live_flag[r] = 0;
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < n; i += kCommitThreads) live_flag[req[i]] = 1;
+    __syncthreads();
+    const int64_t B = block_tokens;
+
+    // Live rows: violation ballot + CSR of the allocated blocks.
+    int2 carry = make_int2(0, 0);
+    for (int32_t base = 0; base < n; base += kCommitThreads) {
+        const int32_t i = base + (int32_t)threadIdx.x;
+        int32_t nb = 0;
+        bool bad = false;
+        int32_t r = -1;
+        if (i < n) {
+            r = req[i];
+            const int64_t s = synced_hi[r];
+            bad = s != kv[i];  // engine.cpp:712
+            nb = (int32_t)cdiv(s, B);
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, bad);
+        if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(&s_viol, (unsigned long long)__popc(ballot));
+        int2 tot;
+        const int2 off = block_exclusive_scan2<kCommitThreads>(make_int2(nb, 0), &tot);
+        if (i < n) {
+            const int32_t o = carry.x + off.x;
+            if (row_ptr) row_ptr[i] = o;
+            if (blocks)
+                for (int32_t k = 0; k < nb; ++k) blocks[o + k] = dst_bt[(int64_t)r * max_blocks + k];
+        }
+        carry.x += tot.x;
+    }
+    if (threadIdx.x == 0 && row_ptr) row_ptr[n] = carry.x;
+    const int32_t n_blocks = carry.x;
+
+    // Dead rows (allocated but no longer live): ballot-compacted free list.
+    carry = make_int2(0, 0);
+    for (int32_t base = 0; base < max_requests; base += kCommitThreads) {
+        const int32_t r = base + (int32_t)threadIdx.x;
+        int32_t nb = 0;
+        if (r < max_requests && !live_flag[r]) nb = (int32_t)cdiv(synced_hi[r], B);
+        int2 tot;
+        const int2 off = block_exclusive_scan2<kCommitThreads>(make_int2(nb, 0), &tot);
+        if (nb > 0 && free_list)
+            for (int32_t k = 0; k < nb; ++k)
+                free_list[carry.x + off.x + k] = dst_bt[(int64_t)r * max_blocks + k];
+        carry.x += tot.x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        out[0] = (int64_t)s_viol;
+        out[1] = n_blocks;
+        out[2] = carry.x;
+    }
+}
+
+// ---------------------------------------------------- payload kernels
+// grid = (entries, max logical blocks); one CTA per (request, logical block),
+// looping over the pool's layers and the block's K/V token rows.
+__global__ void __launch_bounds__(256)
+kvx_fill_kernel(char* __restrict__ pool, int32_t pool_blocks, int32_t first_layer,
+                int32_t num_layers, const int32_t* __restrict__ req,
+                const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
+                int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed) {
+    const int32_t i = blockIdx.x, b = blockIdx.y;
+    const int32_t r = req[i];
+    const int64_t t_begin = (int64_t)b * block_tokens;
+    if (t_begin >= tokens[i]) return;
+    const int64_t t_end = min(tokens[i], t_begin + block_tokens);
+    const int32_t blk = bt[(int64_t)r * max_blocks + b];
+    const uint64_t block_bytes = 2ull * block_tokens * token_bytes;
+    const uint32_t vecs = (uint32_t)(token_bytes >> 4);
+    const int32_t rows = (int32_t)(t_end - t_begin);
+    for (int32_t l = 0; l < num_layers; ++l) {
+        char* slab = pool + ((uint64_t)l * pool_blocks + blk) * block_bytes;
+        for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
+            const int32_t kvi = kvr / rows, t = kvr % rows;
+            const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
+            uint4* row = reinterpret_cast<uint4*>(slab + ((uint64_t)kvi * block_tokens + t) * token_bytes);
+            for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) row[v] = pattern_vec(th, v);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+kvx_verify_kernel(const char* __restrict__ pool, int32_t pool_blocks, int32_t first_layer,
+                  int32_t num_layers, const int32_t* __restrict__ req,
+                  const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
+                  int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed,
+                  unsigned long long* __restrict__ mismatches) {
+    const int32_t i = blockIdx.x, b = blockIdx.y;
+    const int32_t r = req[i];
+    const int64_t t_begin = (int64_t)b * block_tokens;
+    if (t_begin >= tokens[i]) return;
+    const int64_t t_end = min(tokens[i], t_begin + block_tokens);
+    const int32_t blk = bt[(int64_t)r * max_blocks + b];
+    const uint32_t vecs = (uint32_t)(token_bytes >> 4);
+    const int32_t rows = (int32_t)(t_end - t_begin);
+    unsigned long long bad = 0;
+    if (blk < 0) {
+        bad = threadIdx.x == 0 ? (unsigned long long)num_layers * 2 * rows * vecs * 8 : 0;
+    } else {
+        const uint64_t block_bytes = 2ull * block_tokens * token_bytes;
+        for (int32_t l = 0; l < num_layers; ++l) {
+            const char* slab = pool + ((uint64_t)l * pool_blocks + blk) * block_bytes;
+            for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
+                const int32_t kvi = kvr / rows, t = kvr % rows;
+                const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
+                const uint4* row =
+                    reinterpret_cast<const uint4*>(slab + ((uint64_t)kvi * block_tokens + t) * token_bytes);
+                for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) {
+                    const uint4 want = pattern_vec(th, v), got = row[v];
+                    const uint32_t d[4] = {want.x ^ got.x, want.y ^ got.y, want.z ^ got.z, want.w ^ got.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) bad += ((d[q] & 0xffffu) != 0) + ((d[q] >> 16) != 0);
+                }
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatches, bad);
+}
+
+}  // namespace kvx

@@ -1,0 +1,415 @@
+"""ctypes binding of the kvx C-ABI (include/kvx.h) -- the Python face of the
+B200-native inflight-refactor KV transition.
+
+Mirrors the reference's transition interface (RefactorCtx and the engine
+handlers of /root/reference/proj/src/engine.cpp:532-772) with the same names
+and meaning:
+
+    t = Transition(geometry, old_plan, new_plan, device, ...)   # begin_refactor grant
+    t.begin_refactor(live)                   # wave 0        engine.cpp:637-647
+    t.on_kv_sync_complete(live, inflight)    # delta/barrier/final engine.cpp:651-688
+    t.on_refactor_commit(live)               # Eq. 10 + compaction engine.cpp:690-713
+    t.abort_refactor()                       # revocation    engine.cpp:759-772
+
+`live` is the (request, kv_tokens) set of live requests homed on the
+instance, as ``(req: int32[n], kv: int64[n])`` ascending in req.
+
+There is no CPU fallback: if ``_lib/libkvx.so`` is missing the import fails
+loudly (build it with ``python -m paper_2510_11938_b200.build``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libkvx.so")
+
+KVX_OK, KVX_EINVAL, KVX_ESTALE, KVX_ENOSPC, KVX_ECUDA, KVX_ESTATE = 0, -1, -2, -3, -4, -5
+ACT_DELTA, ACT_BARRIER_WAIT, ACT_FINAL = 0, 1, 2
+IPC_HANDLE_BYTES = 64
+
+
+class KvxError(RuntimeError):
+    """A non-zero kvx status.  ``code`` is the KVX_E* value."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"kvx error {code}: {msg}")
+        self.code = code
+
+
+class StaleEpoch(KvxError):
+    """Epoch mismatch -- the reference drops such events (engine.cpp:654,693)."""
+
+
+class NoSpace(KvxError):
+    """Destination full -- the reference turns this into a hold (engine.cpp:563)."""
+
+
+class Geometry(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("elem_bytes", C.c_int32), ("block_tokens", C.c_int32)]
+
+    @property
+    def token_bytes(self) -> int:
+        return self.num_kv_heads * self.head_dim * self.elem_bytes
+
+    @property
+    def block_bytes(self) -> int:
+        return 2 * self.block_tokens * self.token_bytes
+
+    @property
+    def kv_bytes_per_token(self) -> int:
+        """ExecModelParams::kv_bytes_per_token (modelgraph.hpp:115)."""
+        return 2 * self.num_layers * self.token_bytes
+
+
+class _Plan(C.Structure):
+    _fields_ = [("num_stages", C.c_int32), ("boundaries", C.POINTER(C.c_int32)),
+                ("pools", C.POINTER(C.c_void_p))]
+
+
+class _Desc(C.Structure):
+    _fields_ = [("geometry", Geometry), ("old_plan", _Plan), ("new_plan", _Plan),
+                ("device", C.c_int32), ("max_requests", C.c_int32), ("max_blocks", C.c_int32),
+                ("dst_num_blocks", C.c_int32), ("src_block_table", C.POINTER(C.c_int32)),
+                ("epoch", C.c_uint64), ("max_sync_rounds", C.c_int32),
+                ("kv_bytes_per_token", C.c_double), ("stream", C.c_void_p)]
+
+
+class _CommitResult(C.Structure):
+    _fields_ = [("violations", C.c_int64), ("row_ptr", C.POINTER(C.c_int32)),
+                ("blocks", C.POINTER(C.c_int32)), ("blocks_cap", C.c_int32),
+                ("n_blocks", C.c_int32), ("free_list", C.POINTER(C.c_int32)),
+                ("free_cap", C.c_int32), ("n_free", C.c_int32)]
+
+
+class _CtlState(C.Structure):
+    _fields_ = [("rounds", C.c_int32), ("barrier", C.c_int32), ("commit_scheduled", C.c_int32),
+                ("waves", C.c_int32), ("kv_synced_bytes", C.c_double),
+                ("last_wave_tokens", C.c_int64)]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the kvx CUDA library is the only implementation of this "
+            "path (no CPU fallback). Build it with `python -m paper_2510_11938_b200.build`.")
+    lib = C.CDLL(LIB_PATH)
+    P, I32, I64, U64, VP = C.POINTER, C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
+    sig = {
+        "kvx_last_error": (C.c_char_p, []),
+        "kvx_abi_version": (C.c_int, []),
+        "kvx_launch_count": (U64, []),
+        "kvx_device_count": (C.c_int, [P(I32)]),
+        "kvx_pool_create": (C.c_int, [I32, P(Geometry), I32, I32, P(VP)]),
+        "kvx_pool_export": (C.c_int, [VP, C.c_char_p]),
+        "kvx_pool_import": (C.c_int, [I32, C.c_char_p, P(Geometry), I32, I32, P(VP)]),
+        "kvx_pool_info": (C.c_int, [VP, P(VP), P(U64), P(I32), P(I32)]),
+        "kvx_pool_destroy": (C.c_int, [VP]),
+        "kvx_pool_zero": (C.c_int, [VP]),
+        "kvx_pool_read": (C.c_int, [VP, U64, U64, VP]),
+        "kvx_pool_write": (C.c_int, [VP, U64, U64, VP]),
+        "kvx_pool_fill_pattern": (C.c_int, [VP, U64, I32, I32, P(I32), P(I64), P(I32), I32, I32]),
+        "kvx_begin": (C.c_int, [P(_Desc), P(VP)]),
+        "kvx_wave": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(I64)]),
+        "kvx_wait": (C.c_int, [VP, U64, P(C.c_double)]),
+        "kvx_commit": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(_CommitResult)]),
+        "kvx_abort": (C.c_int, [VP]),
+        "kvx_destroy": (C.c_int, [VP]),
+        "kvx_epoch": (C.c_int, [VP, P(U64)]),
+        "kvx_dst_block_table": (C.c_int, [VP, P(I32)]),
+        "kvx_stream": (C.c_int, [VP, P(VP)]),
+        "kvx_bytes_moved": (C.c_int, [VP, P(U64)]),
+        "kvx_move_timings": (C.c_int, [VP, I32, P(C.c_double), P(U64), P(I32)]),
+        "kvx_verify_pattern": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(I64)]),
+        "kvx_ctl_begin": (C.c_int, [VP, I32, P(I32), P(I64), P(I64)]),
+        "kvx_ctl_sync_complete": (C.c_int, [VP, U64, I32, P(I32), P(I64), I32, P(I32), P(I64)]),
+        "kvx_ctl_commit": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(_CommitResult)]),
+        "kvx_ctl_state_get": (C.c_int, [VP, P(_CtlState)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTED = tuple(n for n in dir(_lib) if n.startswith("kvx_"))
+
+
+def lib() -> C.CDLL:
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == KVX_OK:
+        return
+    msg = _lib.kvx_last_error().decode(errors="replace")
+    cls = {KVX_ESTALE: StaleEpoch, KVX_ENOSPC: NoSpace}.get(rc, KvxError)
+    raise cls(rc, msg)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _p32(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _p64(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def launch_count() -> int:
+    return int(_lib.kvx_launch_count())
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    rc = _lib.kvx_device_count(C.byref(n))
+    return int(n.value) if rc == KVX_OK else 0
+
+
+def geometry(num_layers: int, num_kv_heads: int, head_dim: int = 128, elem_bytes: int = 2,
+             block_tokens: int = 16) -> Geometry:
+    return Geometry(num_layers, num_kv_heads, head_dim, elem_bytes, block_tokens)
+
+
+def stage_ranges(num_layers: int, boundaries: Sequence[int]) -> list:
+    """stage_loads (engine.cpp:115-126): [(begin, end)] per stage."""
+    cuts = [0, *boundaries, num_layers]
+    return [(cuts[k], cuts[k + 1]) for k in range(len(cuts) - 1)]
+
+
+class Pool:
+    """One stage's paged KV pool on one GPU (local or imported from a peer)."""
+
+    def __init__(self, device: int, geom: Geometry, num_layers: int, num_blocks: int,
+                 _handle: Optional[int] = None, imported: bool = False):
+        self.geom, self.num_layers, self.num_blocks = geom, num_layers, num_blocks
+        self.device, self.imported = device, imported
+        if _handle is None:
+            h = C.c_void_p()
+            _check(_lib.kvx_pool_create(device, C.byref(geom), num_layers, num_blocks, C.byref(h)))
+            self._h = h
+        else:
+            self._h = C.c_void_p(_handle)
+
+    @classmethod
+    def import_ipc(cls, device: int, handle: bytes, geom: Geometry, num_layers: int,
+                   num_blocks: int) -> "Pool":
+        h = C.c_void_p()
+        _check(_lib.kvx_pool_import(device, handle, C.byref(geom), num_layers, num_blocks,
+                                    C.byref(h)))
+        return cls(device, geom, num_layers, num_blocks, _handle=h.value, imported=True)
+
+    def export_ipc(self) -> bytes:
+        buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(_lib.kvx_pool_export(self._h, buf))
+        return buf.raw
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    @property
+    def nbytes(self) -> int:
+        return self.num_layers * self.num_blocks * self.geom.block_bytes
+
+    def zero(self) -> None:
+        _check(_lib.kvx_pool_zero(self._h))
+
+    def read(self, offset: int = 0, nbytes: Optional[int] = None) -> np.ndarray:
+        nbytes = self.nbytes - offset if nbytes is None else nbytes
+        out = np.empty(nbytes, dtype=np.uint8)
+        _check(_lib.kvx_pool_read(self._h, offset, nbytes, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def write(self, data: np.ndarray, offset: int = 0) -> None:
+        data = np.ascontiguousarray(data).view(np.uint8)
+        _check(_lib.kvx_pool_write(self._h, offset, data.nbytes, data.ctypes.data_as(C.c_void_p)))
+
+    def fill_pattern(self, seed: int, first_layer: int, req, tokens, block_table: np.ndarray) -> None:
+        req, tokens = _i32(req), _i64(tokens)
+        bt = _i32(block_table)
+        _check(_lib.kvx_pool_fill_pattern(self._h, seed, first_layer, len(req), _p32(req),
+                                          _p64(tokens), _p32(bt), bt.shape[0], bt.shape[1]))
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            _check(_lib.kvx_pool_destroy(self._h))
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class CommitResult:
+    violations: int
+    row_ptr: np.ndarray
+    blocks: np.ndarray
+    free_list: np.ndarray
+
+
+class Transition:
+    """One inflight refactor of one pipeline instance (RefactorCtx,
+    engine.hpp:149-158), on one local GPU."""
+
+    def __init__(self, geom: Geometry, old_boundaries: Sequence[int], old_pools: Sequence[Optional[Pool]],
+                 new_boundaries: Sequence[int], new_pools: Sequence[Pool], device: int,
+                 max_requests: int, max_blocks: int, dst_num_blocks: int,
+                 src_block_table: np.ndarray, epoch: int = 1, max_sync_rounds: int = 8,
+                 kv_bytes_per_token: float = 0.0, stream: int = 0):
+        self.geom = geom
+        self.max_requests, self.max_blocks = max_requests, max_blocks
+        self._ob = _i32(list(old_boundaries))
+        self._nb = _i32(list(new_boundaries))
+        self._old = list(old_pools)
+        self._new = list(new_pools)
+        self._op = (C.c_void_p * len(self._old))(*[p.handle.value if p else None for p in self._old])
+        self._np = (C.c_void_p * len(self._new))(*[p.handle.value for p in self._new])
+        src = _i32(src_block_table)
+        if src.shape != (max_requests, max_blocks):
+            raise ValueError("src_block_table must be [max_requests, max_blocks]")
+        d = _Desc()
+        d.geometry = geom
+        d.old_plan = _Plan(len(self._old), _p32(self._ob), C.cast(self._op, C.POINTER(C.c_void_p)))
+        d.new_plan = _Plan(len(self._new), _p32(self._nb), C.cast(self._np, C.POINTER(C.c_void_p)))
+        d.device = device
+        d.max_requests, d.max_blocks, d.dst_num_blocks = max_requests, max_blocks, dst_num_blocks
+        d.src_block_table = _p32(src)
+        d.epoch = epoch
+        d.max_sync_rounds = max_sync_rounds
+        d.kv_bytes_per_token = kv_bytes_per_token
+        d.stream = stream or None
+        h = C.c_void_p()
+        _check(_lib.kvx_begin(C.byref(d), C.byref(h)))
+        self._h = h
+
+    # ------------------------------------------------------------ data plane
+    @property
+    def epoch(self) -> int:
+        e = C.c_uint64()
+        _check(_lib.kvx_epoch(self._h, C.byref(e)))
+        return int(e.value)
+
+    def wave(self, req, lo, hi, epoch: Optional[int] = None) -> None:
+        req, lo, hi = _i32(req), _i64(lo), _i64(hi)
+        _check(_lib.kvx_wave(self._h, self.epoch if epoch is None else epoch, len(req), _p32(req),
+                             _p64(lo), _p64(hi)))
+
+    def wait(self, epoch: Optional[int] = None) -> float:
+        ms = C.c_double()
+        _check(_lib.kvx_wait(self._h, self.epoch if epoch is None else epoch, C.byref(ms)))
+        return float(ms.value)
+
+    def _commit_buffers(self, n: int):
+        cap = self.max_requests * self.max_blocks
+        row_ptr = np.zeros(n + 1, dtype=np.int32)
+        blocks = np.zeros(max(cap, 1), dtype=np.int32)
+        free = np.zeros(max(cap, 1), dtype=np.int32)
+        res = _CommitResult(0, _p32(row_ptr), _p32(blocks), len(blocks), 0, _p32(free), len(free), 0)
+        return res, row_ptr, blocks, free
+
+    def commit(self, req, kv, epoch: Optional[int] = None) -> CommitResult:
+        req, kv = _i32(req), _i64(kv)
+        res, row_ptr, blocks, free = self._commit_buffers(len(req))
+        _check(_lib.kvx_commit(self._h, self.epoch if epoch is None else epoch, len(req), _p32(req),
+                               _p64(kv), C.byref(res)))
+        return CommitResult(int(res.violations), row_ptr, blocks[:res.n_blocks].copy(),
+                            free[:res.n_free].copy())
+
+    def abort(self) -> None:
+        _check(_lib.kvx_abort(self._h))
+
+    def dst_block_table(self) -> np.ndarray:
+        out = np.empty((self.max_requests, self.max_blocks), dtype=np.int32)
+        _check(_lib.kvx_dst_block_table(self._h, _p32(out)))
+        return out
+
+    def stream_ptr(self) -> int:
+        s = C.c_void_p()
+        _check(_lib.kvx_stream(self._h, C.byref(s)))
+        return int(s.value or 0)
+
+    def move_timings(self) -> list:
+        """[(ms, read+write bytes)] of every move-kernel launch, wave order."""
+        n = C.c_int32()
+        _check(_lib.kvx_move_timings(self._h, 0, None, None, C.byref(n)))
+        ms = (C.c_double * max(n.value, 1))()
+        b = (C.c_uint64 * max(n.value, 1))()
+        _check(_lib.kvx_move_timings(self._h, n.value, ms, b, C.byref(n)))
+        return [(float(ms[i]), int(b[i])) for i in range(n.value)]
+
+    def bytes_moved(self) -> int:
+        b = C.c_uint64()
+        _check(_lib.kvx_bytes_moved(self._h, C.byref(b)))
+        return int(b.value)
+
+    def verify_pattern(self, seed: int, req, kv) -> int:
+        req, kv = _i32(req), _i64(kv)
+        bad = C.c_int64()
+        _check(_lib.kvx_verify_pattern(self._h, seed, len(req), _p32(req), _p64(kv), C.byref(bad)))
+        return int(bad.value)
+
+    # --------------------------------------------- reference-shaped handlers
+    def begin_refactor(self, live: Tuple[np.ndarray, np.ndarray]) -> int:
+        """Wave 0 over every live token (engine.cpp:637-647); returns tokens."""
+        req, kv = _i32(live[0]), _i64(live[1])
+        tok = C.c_int64()
+        _check(_lib.kvx_ctl_begin(self._h, len(req), _p32(req), _p64(kv), C.byref(tok)))
+        return int(tok.value)
+
+    def on_kv_sync_complete(self, live, inflight_batches: int = 0,
+                            epoch: Optional[int] = None) -> Tuple[int, int]:
+        """engine.cpp:651-688 -> (action, tokens of the wave issued)."""
+        req, kv = _i32(live[0]), _i64(live[1])
+        act, tok = C.c_int32(), C.c_int64()
+        _check(_lib.kvx_ctl_sync_complete(self._h, self.epoch if epoch is None else epoch, len(req),
+                                          _p32(req), _p64(kv), inflight_batches, C.byref(act),
+                                          C.byref(tok)))
+        return int(act.value), int(tok.value)
+
+    def on_refactor_commit(self, live, epoch: Optional[int] = None) -> CommitResult:
+        """engine.cpp:690-713: final apply, Eq. 10 on the device, compaction."""
+        req, kv = _i32(live[0]), _i64(live[1])
+        res, row_ptr, blocks, free = self._commit_buffers(len(req))
+        _check(_lib.kvx_ctl_commit(self._h, self.epoch if epoch is None else epoch, len(req),
+                                   _p32(req), _p64(kv), C.byref(res)))
+        return CommitResult(int(res.violations), row_ptr, blocks[:res.n_blocks].copy(),
+                            free[:res.n_free].copy())
+
+    def abort_refactor(self) -> None:
+        """engine.cpp:759-772."""
+        self.abort()
+
+    def ctl_state(self) -> dict:
+        s = _CtlState()
+        _check(_lib.kvx_ctl_state_get(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in _CtlState._fields_}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _check(_lib.kvx_destroy(self._h))
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
