@@ -32,7 +32,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -42,6 +41,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2510_11938_b200 import shard as S  # noqa: E402
 from paper_2510_11938_b200 import workload as W  # noqa: E402
 
 CONFIGS = {
@@ -69,107 +69,61 @@ def peaks():
         return 6650.0, "fallback"
 
 
-# ----------------------------------------------------------------- placement
-def stage_of(bounds, layer):
-    s = 0
-    for b in bounds:
-        if layer < b:
-            break
-        s += 1
-    return s
-
-
-def placement(L, ob, nb, n_gpus, mode="affinity"):
-    """Logical stages -> physical GPUs.  Old stage k on GPU floor(k*N/K_old);
-    new stage j on the GPU that already holds most of its layers (the
-    reference's warm-start affinity, cluster.cpp:525-536), ties to the lowest
-    id; 'disjoint' shifts every new stage by N/2 GPUs so all its KV crosses
-    NVLink (the reference's disjoint-GPU grant, engine.cpp:584-591)."""
-    k_old, k_new = len(ob) + 1, len(nb) + 1
-    old_dev = [k * n_gpus // k_old for k in range(k_old)]
-    new_dev = []
-    for j, (b, e) in enumerate(W.stage_ranges(L, nb)):
-        share = {}
-        for l in range(b, e):
-            d = old_dev[stage_of(ob, l)]
-            share[d] = share.get(d, 0) + 1
-        best = sorted(share.items(), key=lambda kv: (-kv[1], kv[0]))[0][0]
-        if mode == "disjoint" and n_gpus > 1:
-            best = (best + n_gpus // 2) % n_gpus
-        new_dev.append(best)
-    return old_dev, new_dev
-
-
-def link_bytes(L, ob, nb, old_dev, new_dev, layer_bytes, n_gpus):
-    """Per-GPU (HBM read+write, NVLink out, NVLink in) bytes of one transition
-    given the bytes moved per layer."""
-    hbm = [0] * n_gpus
-    out = [0] * n_gpus
-    inn = [0] * n_gpus
-    for l in range(L):
-        s, d = old_dev[stage_of(ob, l)], new_dev[stage_of(nb, l)]
-        hbm[s] += layer_bytes
-        hbm[d] += layer_bytes
-        if s != d:
-            out[s] += layer_bytes
-            inn[d] += layer_bytes
-    return hbm, out, inn
-
-
 # ------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled in-process through NVML (one call
+    per 20 ms from a thread) while the timed region runs."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, index: int, period_s: float = 0.02):
+        self.index, self.period = index, period_s
         self.rows = []
-        self.proc = None
         self.err = None
+        self._stop = threading.Event()
+        self._thr = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
-        except Exception as e:  # nvidia-smi absent
-            self.err = str(e)
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # NVML absent
+            self.err = f"nvml: {e}"
+            return
+        self._thr = threading.Thread(target=self._run, daemon=True)
+        self._thr.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append((time.time(), line.strip()))
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.rows.append((time.time(), sm, rs))
+            except Exception as e:
+                self.err = str(e)
+                return
+            self._stop.wait(self.period)
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._thr:
+            self._thr.join(timeout=2)
 
     def summary(self, t0: float, t1: float):
-        if self.err or not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
-                    "note": self.err or "no nvidia-smi samples"}
-        sel = [r for (t, r) in self.rows if t0 - 0.06 <= t <= t1 + 0.06] or [r for _, r in self.rows[-3:]]
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in sel:
-            parts = [p.strip() for p in r.split(",")]
-            try:
-                sm.append(float(parts[2]))
-                smax.append(float(parts[3]))
-                for n, v in zip(names, parts[5:9]):
-                    if v.lower() == "active":
-                        reasons.add(n)
-            except (ValueError, IndexError):
-                continue
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sel = [r for r in self.rows if t0 - 0.025 <= r[0] <= t1 + 0.025] or self.rows[-3:]
+        if not sel:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": self.err or "no samples"}
+        reasons = set()
+        for _, _, rs in sel:
+            for bit, name in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r[1] for r in sel), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sel), "source": "nvml"}
 
 
 # ------------------------------------------------------------------ workload
@@ -340,32 +294,19 @@ def main():
     t = plan.t
     L = plan.L
     g = kvx.geometry(L, plan.H, plan.D)
-    old_dev, new_dev = placement(L, t.old_boundaries, t.new_boundaries, n_gpus, args.placement)
+    old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, n_gpus, args.placement)
 
-    # ---- pools on this GPU; new-stage pools exchanged through CUDA IPC
-    old_pools = [None] * (len(t.old_boundaries) + 1)
-    for k, (b, e) in enumerate(W.stage_ranges(L, t.old_boundaries)):
-        if old_dev[k] == rank:
-            p = kvx.Pool(dev, g, e - b, plan.old_blocks)
-            p.fill_pattern(SEED, b, plan.live, plan.tokens[plan.live], plan.src_bt)
-            old_pools[k] = p
-    new_pools = [None] * (len(t.new_boundaries) + 1)
-    handles = {}
-    for j, (b, e) in enumerate(W.stage_ranges(L, t.new_boundaries)):
-        if new_dev[j] == rank:
-            p = kvx.Pool(dev, g, e - b, plan.dst_blocks)
-            p.zero()
-            new_pools[j] = p
-            if world > 1:
-                handles[j] = p.export_ipc()
+    # ---- pools on this GPU; new-stage pools of peers mapped through CUDA IPC
+    def gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    old_pools, new_pools = S.setup_rank_pools(
+        kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, dev, plan.old_blocks,
+        plan.dst_blocks, all_gather=gather if world > 1 else None,
+        fill=(SEED, plan.live, plan.tokens[plan.live], plan.src_bt))
     if world > 1:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, handles)
-        for r, hs in enumerate(gathered):
-            for j, h in hs.items():
-                if r != rank:
-                    b, e = W.stage_ranges(L, t.new_boundaries)[int(j)]
-                    new_pools[int(j)] = kvx.Pool.import_ipc(dev, h, g, e - b, plan.dst_blocks)
         dist.barrier()
 
     stream = torch.cuda.Stream(device=dev)
@@ -468,7 +409,7 @@ def main():
     # ---- roofline of the dominant kernel
     peak, peak_kind = peaks()
     layer_bytes = plan.wave0_tokens * 2 * plan.token_bytes  # K+V bytes per layer in wave 0
-    hbm, out, inn = link_bytes(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev, layer_bytes,
+    hbm, out, inn = S.link_bytes(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev, layer_bytes,
                                n_gpus)
     nvl_peak = 770.0  # measured peer copy GB/s per direction (B200_PROFILING.md)
     t_roof = max(max(h / (peak * 1e9) for h in hbm), max(o / (nvl_peak * 1e9) for o in out),
@@ -487,6 +428,18 @@ def main():
                 "traffic": None, "kernel": "kvx_move_kernel (wave 0, slowest rank)",
                 "t_roof_ms": round(t_roof * 1e3, 4), "launch_ms": round(w0_avg, 4),
                 "peak_source": f"hbm {peak_kind}; nvlink 770 GB/s measured peer copy"}
+
+    # ordered teardown: unmap peers' pools, then free our own
+    for p in old_pools + new_pools:
+        if p is not None and p.imported:
+            p.close()
+    if world > 1:
+        dist.barrier()
+    for p in old_pools + new_pools:
+        if p is not None and not p.imported:
+            p.close()
+    if world > 1:
+        dist.barrier()
 
     if rank != 0:
         if world > 1:

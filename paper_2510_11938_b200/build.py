@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libkvx.so")
 SOURCES = ["kvx.cu", "kvx_ctl.cpp"]
-HEADERS = ["kvx_kernels.cuh", "kvx_internal.h"]
+HEADERS = ["kvx_kernels.cuh", "kvx_internal.h", "kvx_arena.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall",

@@ -10,7 +10,9 @@
 // destination block table without exchanging it.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -18,6 +20,7 @@
 #include <vector>
 
 #include "kvx.h"
+#include "kvx_arena.h"
 #include "kvx_internal.h"
 #include "kvx_kernels.cuh"
 
@@ -118,6 +121,8 @@ struct kvx_transition {
     bool own_stream = true;
     int num_sms = 0;
     int move_ctas_per_sm = 1;
+    int bulk_ctas_per_sm = 1;
+    bool use_bulk = false;  // TMA bulk mover for local destinations
     std::vector<int32_t> old_b, new_b;
     std::vector<kvx_pool*> old_pools, new_pools;
     int32_t max_requests = 0, max_blocks = 0, dst_num_blocks = 0;
@@ -142,6 +147,7 @@ struct kvx_transition {
     uint8_t* d_live = nullptr;
     int32_t* d_commit_i32 = nullptr;  // row_ptr | blocks | free_list
     int64_t commit_i32_cap = 0;
+    size_t bt_bytes = 0, wave_bytes = 0, layers_bytes = 0;
     int64_t* d_commit_out = nullptr;
     // timing
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
@@ -395,25 +401,42 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         cudaSuccess)
         return bail(fail(KVX_ECUDA, "occupancy query"));
     t->move_ctas_per_sm = std::max(1, occ);
+    {
+        const int smem = kvx::kBulkStages * (int)kvx::kBulkChunk;
+        if (cudaFuncSetAttribute(kvx::kvx_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+                cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kvx::kvx_bulk_kernel, kvx::kBulkThreads, smem) !=
+                cudaSuccess)
+            return bail(fail(KVX_ECUDA, "bulk kernel attributes"));
+        t->bulk_ctas_per_sm = std::max(1, occ);
+        // Bulk (TMA engine) mover by default for local destinations; the LSU
+        // mover stays for peer (NVLink) destinations and on request.
+        const char* impl = getenv("KVX_MOVE_IMPL");
+        t->use_bulk = !(impl && std::string(impl) == "lsu");
+    }
     if (d->stream) {
         t->stream = static_cast<cudaStream_t>(d->stream);
         t->own_stream = false;
     } else if (cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking) != cudaSuccess) {
         return bail(fail(KVX_ECUDA, "stream create"));
     }
-    if (cudaEventCreate(&t->ev_begin) != cudaSuccess || cudaEventCreate(&t->ev_end) != cudaSuccess)
+    kvx::Arena& A = kvx::Arena::of(d->device);
+    if (A.event(&t->ev_begin, true) != cudaSuccess || A.event(&t->ev_end, true) != cudaSuccess)
         return bail(fail(KVX_ECUDA, "event create"));
     const size_t bt_bytes = sizeof(int32_t) * cells;
     const size_t wave_bytes = (size_t)d->max_requests * (sizeof(int32_t) + 2 * sizeof(int64_t)) + 64;
-    if (cudaMalloc(&t->d_src_bt, bt_bytes) != cudaSuccess || cudaMalloc(&t->d_dst_bt, bt_bytes) != cudaSuccess ||
-        cudaMalloc(&t->d_synced_hi, sizeof(int64_t) * (size_t)d->max_requests) != cudaSuccess ||
-        cudaMalloc(&t->d_wave, wave_bytes) != cudaSuccess ||
-        cudaMalloc(&t->d_live, (size_t)d->max_requests) != cudaSuccess ||
-        cudaMalloc(&t->d_commit_out, 4 * sizeof(int64_t)) != cudaSuccess)
+    t->bt_bytes = bt_bytes;
+    t->wave_bytes = wave_bytes;
+    if (A.dev_alloc((void**)&t->d_src_bt, bt_bytes) != cudaSuccess ||
+        A.dev_alloc((void**)&t->d_dst_bt, bt_bytes) != cudaSuccess ||
+        A.dev_alloc((void**)&t->d_synced_hi, sizeof(int64_t) * (size_t)d->max_requests) != cudaSuccess ||
+        A.dev_alloc((void**)&t->d_wave, wave_bytes) != cudaSuccess ||
+        A.dev_alloc((void**)&t->d_live, (size_t)d->max_requests) != cudaSuccess ||
+        A.dev_alloc((void**)&t->d_commit_out, 4 * sizeof(int64_t)) != cudaSuccess)
         return bail(fail(KVX_ENOSPC, "transition state allocation failed"));
     for (int s = 0; s < 2; ++s)
-        if (cudaMallocHost(&t->h_wave[s], wave_bytes) != cudaSuccess ||
-            cudaEventCreateWithFlags(&t->h_wave_free[s], cudaEventDisableTiming) != cudaSuccess)
+        if (A.host_alloc((void**)&t->h_wave[s], wave_bytes) != cudaSuccess ||
+            A.event(&t->h_wave_free[s], false) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "pinned staging allocation failed"));
     if (cudaMemcpyAsync(t->d_src_bt, d->src_block_table, bt_bytes, cudaMemcpyHostToDevice, t->stream) !=
             cudaSuccess ||
@@ -421,6 +444,17 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         cudaMemsetAsync(t->d_synced_hi, 0, sizeof(int64_t) * (size_t)d->max_requests, t->stream) !=
             cudaSuccess)
         return bail(fail(KVX_ECUDA, "transition state init"));
+
+    // Worst-case wave and commit buffers up front, so no allocation happens
+    // between the grant and the commit (a wave has at most max_blocks
+    // segments per request; commit needs row_ptr + live blocks + free list).
+    {
+        t->seg_cap = (int64_t)(kvx::size_class(sizeof(kvx::Seg) * cells) / sizeof(kvx::Seg));
+        t->commit_i32_cap = (int64_t)(d->max_requests + 1) + 2 * (int64_t)cells;
+        if (A.dev_alloc((void**)&t->d_segs, sizeof(kvx::Seg) * (size_t)t->seg_cap) != cudaSuccess ||
+            A.dev_alloc((void**)&t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap) != cudaSuccess)
+            return bail(fail(KVX_ENOSPC, "transition scratch allocation failed"));
+    }
 
     // Per-layer slab bases for the layers this GPU sources.
     std::vector<kvx::LayerPtr> layers;
@@ -437,7 +471,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     }
     t->n_local_layers = (int32_t)layers.size();
     if (!layers.empty()) {
-        if (cudaMalloc(&t->d_layers, sizeof(kvx::LayerPtr) * layers.size()) != cudaSuccess ||
+        t->layers_bytes = sizeof(kvx::LayerPtr) * layers.size();
+        if (A.dev_alloc((void**)&t->d_layers, t->layers_bytes) != cudaSuccess ||
             cudaMemcpyAsync(t->d_layers, layers.data(), sizeof(kvx::LayerPtr) * layers.size(),
                             cudaMemcpyHostToDevice, t->stream) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "layer table upload"));
@@ -474,13 +509,15 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     DeviceGuard dg(t->device);
     if (n == 0 || nseg == 0) return KVX_OK;
     if (nseg > t->seg_cap) {
+        kvx::Arena& A = kvx::Arena::of(t->device);
         if (t->d_segs) {
             KVX_CUDA(cudaStreamSynchronize(t->stream));
-            cudaFree(t->d_segs);
+            A.dev_free(t->d_segs, sizeof(kvx::Seg) * (size_t)t->seg_cap);
             t->d_segs = nullptr;
         }
-        const int64_t cap = std::max<int64_t>(nseg, 2 * t->seg_cap);
-        KVX_CUDA(cudaMalloc(&t->d_segs, sizeof(kvx::Seg) * (size_t)cap));
+        const int64_t cap = (int64_t)(kvx::size_class(sizeof(kvx::Seg) * (size_t)std::max<int64_t>(nseg, 2 * t->seg_cap)) /
+                                      sizeof(kvx::Seg));
+        KVX_CUDA(A.dev_alloc((void**)&t->d_segs, sizeof(kvx::Seg) * (size_t)cap));
         t->seg_cap = cap;
     }
     // Stage (req | lo | hi) into pinned memory; the slot's previous upload
@@ -513,15 +550,23 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         const int64_t full = (int64_t)t->num_sms * t->move_ctas_per_sm;
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full));
         std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-        KVX_CUDA(cudaEventCreate(&ev.first));
-        KVX_CUDA(cudaEventCreate(&ev.second));
+        KVX_CUDA(kvx::Arena::of(t->device).event(&ev.first, true));
+        KVX_CUDA(kvx::Arena::of(t->device).event(&ev.second, true));
         t->move_ev.push_back(ev);
         t->move_bytes.push_back(2ull * (uint64_t)tokens * 2ull * token_bytes(t->g) *
                                 (uint64_t)t->n_local_layers);
         KVX_CUDA(cudaEventRecord(ev.first, t->stream));
-        kvx::kvx_move_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
-            t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
-            token_bytes(t->g), t->g.block_tokens, t->has_peer_dst ? 1 : 0);
+        if (t->use_bulk && !t->has_peer_dst) {
+            const int64_t full_b = (int64_t)t->num_sms * t->bulk_ctas_per_sm;
+            const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
+            kvx::kvx_bulk_kernel<<<grid_b, kvx::kBulkThreads, kvx::kBulkStages * kvx::kBulkChunk, t->stream>>>(
+                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
+                token_bytes(t->g), t->g.block_tokens);
+        } else {
+            kvx::kvx_move_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
+                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
+                token_bytes(t->g), t->g.block_tokens, t->has_peer_dst ? 1 : 0);
+        }
         KVX_LAUNCHED();
         KVX_CUDA(cudaEventRecord(ev.second, t->stream));
     }
@@ -573,10 +618,15 @@ int kvx_commit(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t*
         if (!live[(size_t)r]) nb_free += cdiv64(t->synced_hi[(size_t)r], B);
     const int64_t need = (n_live + 1) + nb_live + nb_free;
     if (need > t->commit_i32_cap) {
-        if (t->d_commit_i32) cudaFree(t->d_commit_i32);
+        kvx::Arena& A = kvx::Arena::of(t->device);
+        if (t->d_commit_i32) {
+            KVX_CUDA(cudaStreamSynchronize(t->stream));
+            A.dev_free(t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap);
+        }
         t->d_commit_i32 = nullptr;
-        KVX_CUDA(cudaMalloc(&t->d_commit_i32, sizeof(int32_t) * (size_t)std::max<int64_t>(need, 1)));
-        t->commit_i32_cap = need;
+        const int64_t cap = std::max<int64_t>(need, 1);
+        KVX_CUDA(A.dev_alloc((void**)&t->d_commit_i32, sizeof(int32_t) * (size_t)cap));
+        t->commit_i32_cap = cap;
     }
     int32_t* d_row_ptr = t->d_commit_i32;
     int32_t* d_blocks = d_row_ptr + (n_live + 1);
@@ -649,24 +699,25 @@ int kvx_destroy(kvx_transition* t) {
     if (!t) return KVX_OK;
     DeviceGuard dg(t->device);
     if (t->stream) cudaStreamSynchronize(t->stream);
-    cudaFree(t->d_src_bt);
-    cudaFree(t->d_dst_bt);
-    cudaFree(t->d_synced_hi);
-    cudaFree(t->d_layers);
-    cudaFree(t->d_wave);
-    cudaFree(t->d_segs);
-    cudaFree(t->d_live);
-    cudaFree(t->d_commit_i32);
-    cudaFree(t->d_commit_out);
+    kvx::Arena& A = kvx::Arena::of(t->device);
+    A.dev_free(t->d_src_bt, t->bt_bytes);
+    A.dev_free(t->d_dst_bt, t->bt_bytes);
+    A.dev_free(t->d_synced_hi, sizeof(int64_t) * (size_t)t->max_requests);
+    A.dev_free(t->d_layers, t->layers_bytes);
+    A.dev_free(t->d_wave, t->wave_bytes);
+    A.dev_free(t->d_segs, sizeof(kvx::Seg) * (size_t)t->seg_cap);
+    A.dev_free(t->d_live, (size_t)t->max_requests);
+    A.dev_free(t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap);
+    A.dev_free(t->d_commit_out, 4 * sizeof(int64_t));
     for (int s = 0; s < 2; ++s) {
-        if (t->h_wave[s]) cudaFreeHost(t->h_wave[s]);
-        if (t->h_wave_free[s]) cudaEventDestroy(t->h_wave_free[s]);
+        A.host_free(t->h_wave[s], t->wave_bytes);
+        A.event_free(t->h_wave_free[s], false);
     }
-    if (t->ev_begin) cudaEventDestroy(t->ev_begin);
-    if (t->ev_end) cudaEventDestroy(t->ev_end);
+    A.event_free(t->ev_begin, true);
+    A.event_free(t->ev_end, true);
     for (auto& ev : t->move_ev) {
-        cudaEventDestroy(ev.first);
-        cudaEventDestroy(ev.second);
+        A.event_free(ev.first, true);
+        A.event_free(ev.second, true);
     }
     if (t->stream && t->own_stream) cudaStreamDestroy(t->stream);
     delete t;

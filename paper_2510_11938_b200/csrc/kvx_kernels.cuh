@@ -220,6 +220,185 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     if (fence_system) __threadfence_system();  // peer (NVLink) stores visible before host sync
 }
 
+// ------------------------------------------------------- TMA bulk mover
+// One elected thread per CTA streams the CTA's (segment, layer) work through
+// a kBulkStages-deep shared-memory ring with the bulk-copy engine:
+//   cp.async.bulk global->shared (completes on an mbarrier with tx bytes),
+//   cp.async.bulk shared->global (bulk_group; .read completion frees the slot).
+// No registers carry payload; the SM's LSU pipe is idle.  Same work list and
+// unit order as kvx_move_kernel.
+constexpr int kBulkStages = 6;
+constexpr uint32_t kBulkChunk = 32768;  // bytes per stage (16-byte multiple)
+constexpr int kBulkThreads = 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
+                 "r"(smem_u32(smem)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= kBulkChunk bytes
+    const Seg* segs;
+    const LayerPtr* layers;
+    int32_t nseg;
+    int64_t units, u, ustep;
+    uint64_t block_bytes, token_bytes;
+    int32_t block_tokens;
+    // current run
+    const char* src;
+    char* dst;
+    uint64_t left;
+    int run;       // 0 or 1 (K then V of a partial block)
+    uint64_t run_bytes, off0;
+    const char* base_src;
+    char* base_dst;
+
+    __device__ bool load_unit() {
+        while (u < units) {
+            const int32_t layer = (int32_t)(u / nseg);
+            const Seg sg = segs[u - (int64_t)layer * nseg];
+            const LayerPtr lp = layers[layer];
+            base_src = lp.src + (uint64_t)sg.src_blk * block_bytes;
+            base_dst = lp.dst + (uint64_t)sg.dst_blk * block_bytes;
+            if (sg.t0 == 0 && sg.t1 == block_tokens) {
+                run = 1;  // one run covering K and V
+                off0 = 0;
+                run_bytes = block_bytes;
+            } else {
+                run = 0;
+                off0 = (uint64_t)sg.t0 * token_bytes;
+                run_bytes = (uint64_t)(sg.t1 - sg.t0) * token_bytes;
+            }
+            src = base_src + off0;
+            dst = base_dst + off0;
+            left = run_bytes;
+            return true;
+        }
+        return false;
+    }
+    __device__ bool next(const char** s, char** d, uint32_t* n) {
+        while (left == 0) {
+            if (run == 0) {  // move on to the V half of the partial block
+                run = 1;
+                src = base_src + (block_bytes >> 1) + off0;
+                dst = base_dst + (block_bytes >> 1) + off0;
+                left = run_bytes;
+                break;
+            }
+            u += ustep;
+            if (!load_unit()) return false;
+        }
+        const uint32_t c = left > kBulkChunk ? kBulkChunk : (uint32_t)left;
+        *s = src;
+        *d = dst;
+        *n = c;
+        src += c;
+        dst += c;
+        left -= c;
+        return true;
+    }
+};
+
+__global__ void __launch_bounds__(kBulkThreads, 1)
+kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
+                int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[kBulkStages];
+    if (threadIdx.x != 0) return;
+    for (int i = 0; i < kBulkStages; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+    ChunkIter it;
+    it.segs = segs;
+    it.layers = layers;
+    it.nseg = nseg;
+    it.units = (int64_t)nseg * nlayers;
+    it.u = blockIdx.x;
+    it.ustep = gridDim.x;
+    it.block_bytes = block_bytes;
+    it.token_bytes = token_bytes;
+    it.block_tokens = block_tokens;
+    it.left = 0;
+    it.run = 1;
+    if (!it.load_unit()) return;
+
+    char* pend_dst[kBulkStages];
+    uint32_t pend_n[kBulkStages];
+    int64_t issued = 0, stored = 0;
+    bool more = true;
+    // prologue: fill the ring
+    for (int st = 0; st < kBulkStages && more; ++st) {
+        const char* s;
+        char* d;
+        uint32_t n;
+        more = it.next(&s, &d, &n);
+        if (!more) break;
+        mbar_expect_tx(&bars[st], n);
+        bulk_g2s(smem + (size_t)st * kBulkChunk, s, n, &bars[st]);
+        pend_dst[st] = d;
+        pend_n[st] = n;
+        ++issued;
+    }
+    while (stored < issued) {
+        const int st = (int)(stored % kBulkStages);
+        const uint32_t parity = (uint32_t)((stored / kBulkStages) & 1);
+        mbar_wait(&bars[st], parity);
+        bulk_s2g(pend_dst[st], smem + (size_t)st * kBulkChunk, pend_n[st]);
+        bulk_commit();
+        ++stored;
+        // refill the slot stored one iteration ago once its store has read smem
+        if (more && stored >= 2) {
+            const int rs = (int)((stored - 2) % kBulkStages);
+            const char* s;
+            char* d;
+            uint32_t n;
+            more = it.next(&s, &d, &n);
+            if (more) {
+                bulk_wait_read<1>();
+                mbar_expect_tx(&bars[rs], n);
+                bulk_g2s(smem + (size_t)rs * kBulkChunk, s, n, &bars[rs]);
+                pend_dst[rs] = d;
+                pend_n[rs] = n;
+                ++issued;
+            }
+        }
+    }
+    bulk_wait_all();
+}
+
 // ------------------------------------------------------------- commit
 constexpr int kCommitThreads = 1024;
 
