@@ -1,0 +1,34 @@
+"""Drop-in proof: the UNMODIFIED reference engine (oracle/_ref/libpipesim.a)
+drives the kvx C-ABI at its own wave / commit / abort points
+(tests/native/engine_kvx.cpp) and real paged KV moves on the GPU.  Every
+commit's device-side Eq. 10 count must equal the reference's, and every live
+destination word must equal the payload."""
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "native", "_build", "engine_kvx")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("scenario,commits,aborts", [("criterion12", 2, 0), ("consolidate", 1, 0),
+                                                     ("revoke", 0, 1)])
+def test_reference_engine_drives_kvx(gpu_count, scenario, commits, aborts):
+    assert os.path.exists(BIN), "build it with __graft_entry__.build() (needs the reference sources)"
+    out = subprocess.run([BIN, scenario], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    summary = lines[-1]
+    assert summary["refactor_commits"] == commits and summary["refactor_aborts"] == aborts
+    assert summary["kv_violations_device"] == summary["kv_violations_reference"] == 0
+    assert summary["mismatched_words"] == 0
+    assert summary["transitions"] == commits + aborts
+    kinds = [l["kind"] for l in lines[:-1]]
+    assert kinds.count("commit") == commits and kinds.count("abort") == aborts
+    for l in lines[:-1]:
+        if l["kind"] == "commit":
+            assert l["live"] > 0 and l["blocks"] > 0
