@@ -368,6 +368,8 @@ def main():
     w0_bytes = mv[0][0][1] if mv and mv[0] else 0
     w0_avg = sum(w0_ms) / len(w0_ms) if w0_ms else float("nan")
     all_move_ms = sum(x[0] for m in mv for x in m)
+    n_waves = max((len(m) for m in mv), default=0)
+    wave_ms = [round(statistics.median(m[i][0] for m in mv if len(m) > i), 4) for i in range(n_waves)]
 
     tm = torch.tensor([dev_ms, stall_med, float(launches), w0_avg, float(w0_bytes)], dtype=torch.float64,
                       device=dev)
@@ -462,7 +464,8 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                 "ms_per_step": round(e2e_s * 1e3 / e2e_steps, 4)},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clocks,
-        "move_kernel_ms_per_step": round(all_move_ms / K, 4),
+        "move_kernel_ms_per_step": round(all_move_ms / K, 4), "move_ms_by_wave": wave_ms,
+        "mover": os.environ.get("KVX_MOVE_IMPL", "bulk") + ":" + os.environ.get("KVX_BULK_CFG", "0"),
     }
     if n_gpus == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1

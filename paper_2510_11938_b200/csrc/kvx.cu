@@ -103,6 +103,25 @@ bool plan_ok(const kvx_plan& p, int32_t L, std::string* why, std::vector<int32_t
 
 }  // namespace
 
+// ---------------------------------------------------------- bulk variants
+// (ring depth, chunk bytes) of the TMA bulk mover; selectable with
+// KVX_BULK_CFG=<index> for tuning, index 0 is the default.
+namespace {
+using BulkFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, uint64_t, int32_t);
+struct BulkVariant {
+    int stages;
+    uint32_t chunk;
+    BulkFn fn;
+};
+const BulkVariant kBulkVariants[] = {
+    {6, 32768, kvx::kvx_bulk_kernel<6, 32768>},  {4, 49152, kvx::kvx_bulk_kernel<4, 49152>},
+    {3, 65536, kvx::kvx_bulk_kernel<3, 65536>},  {12, 16384, kvx::kvx_bulk_kernel<12, 16384>},
+    {3, 32768, kvx::kvx_bulk_kernel<3, 32768>},  {8, 16384, kvx::kvx_bulk_kernel<8, 16384>},
+    {2, 65536, kvx::kvx_bulk_kernel<2, 65536>},  {4, 16384, kvx::kvx_bulk_kernel<4, 16384>},
+};
+constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
+}  // namespace
+
 // ------------------------------------------------------------------ types
 struct kvx_pool {
     int32_t device = -1;
@@ -122,7 +141,9 @@ struct kvx_transition {
     int num_sms = 0;
     int move_ctas_per_sm = 1;
     int bulk_ctas_per_sm = 1;
-    bool use_bulk = false;  // TMA bulk mover for local destinations
+    int bulk_variant = 0;
+    bool use_bulk = false;   // TMA bulk mover for local destinations
+    bool peer_bulk = false;  // ... and for peer (NVLink) destinations
     std::vector<int32_t> old_b, new_b;
     std::vector<kvx_pool*> old_pools, new_pools;
     int32_t max_requests = 0, max_blocks = 0, dst_num_blocks = 0;
@@ -402,18 +423,23 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         return bail(fail(KVX_ECUDA, "occupancy query"));
     t->move_ctas_per_sm = std::max(1, occ);
     {
-        const int smem = kvx::kBulkStages * (int)kvx::kBulkChunk;
-        if (cudaFuncSetAttribute(kvx::kvx_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-                cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kvx::kvx_bulk_kernel, kvx::kBulkThreads, smem) !=
-                cudaSuccess)
+        const char* cfg = getenv("KVX_BULK_CFG");
+        t->bulk_variant = cfg ? std::max(0, std::min(kNumBulkVariants - 1, atoi(cfg))) : 0;
+        const BulkVariant& bv = kBulkVariants[t->bulk_variant];
+        const int smem = bv.stages * (int)bv.chunk;
+        if (cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bv.fn, kvx::kBulkThreads, smem) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "bulk kernel attributes"));
         t->bulk_ctas_per_sm = std::max(1, occ);
         // Bulk (TMA engine) mover by default for local destinations; the LSU
-        // mover stays for peer (NVLink) destinations and on request.
+        // mover for peer (NVLink) destinations unless KVX_PEER_BULK=1, and
+        // everywhere with KVX_MOVE_IMPL=lsu.
         const char* impl = getenv("KVX_MOVE_IMPL");
         t->use_bulk = !(impl && std::string(impl) == "lsu");
+        const char* pb = getenv("KVX_PEER_BULK");
+        t->peer_bulk = t->use_bulk && pb && std::string(pb) == "1";
     }
+
     if (d->stream) {
         t->stream = static_cast<cudaStream_t>(d->stream);
         t->own_stream = false;
@@ -556,10 +582,11 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         t->move_bytes.push_back(2ull * (uint64_t)tokens * 2ull * token_bytes(t->g) *
                                 (uint64_t)t->n_local_layers);
         KVX_CUDA(cudaEventRecord(ev.first, t->stream));
-        if (t->use_bulk && !t->has_peer_dst) {
+        if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
+            const BulkVariant& bv = kBulkVariants[t->bulk_variant];
             const int64_t full_b = (int64_t)t->num_sms * t->bulk_ctas_per_sm;
             const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
-            kvx::kvx_bulk_kernel<<<grid_b, kvx::kBulkThreads, kvx::kBulkStages * kvx::kBulkChunk, t->stream>>>(
+            bv.fn<<<grid_b, kvx::kBulkThreads, (size_t)bv.stages * bv.chunk, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
                 token_bytes(t->g), t->g.block_tokens);
         } else {

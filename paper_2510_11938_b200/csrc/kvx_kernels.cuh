@@ -227,8 +227,8 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
 //   cp.async.bulk shared->global (bulk_group; .read completion frees the slot).
 // No registers carry payload; the SM's LSU pipe is idle.  Same work list and
 // unit order as kvx_move_kernel.
-constexpr int kBulkStages = 6;
-constexpr uint32_t kBulkChunk = 32768;  // bytes per stage (16-byte multiple)
+constexpr int kBulkStages = 6;           // default ring depth
+constexpr uint32_t kBulkChunk = 32768;   // default bytes per stage (16-byte multiple)
 constexpr int kBulkThreads = 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -270,13 +270,14 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= kBulkChunk bytes
+struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
     const Seg* segs;
     const LayerPtr* layers;
     int32_t nseg;
     int64_t units, u, ustep;
     uint64_t block_bytes, token_bytes;
     int32_t block_tokens;
+    uint32_t chunk;
     // current run
     const char* src;
     char* dst;
@@ -321,7 +322,7 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= kBulkChunk byte
             u += ustep;
             if (!load_unit()) return false;
         }
-        const uint32_t c = left > kBulkChunk ? kBulkChunk : (uint32_t)left;
+        const uint32_t c = left > chunk ? chunk : (uint32_t)left;
         *s = src;
         *d = dst;
         *n = c;
@@ -332,13 +333,14 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= kBulkChunk byte
     }
 };
 
-__global__ void __launch_bounds__(kBulkThreads, 1)
+template <int kStages, uint32_t kChunk>
+__global__ void __launch_bounds__(kBulkThreads)
 kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
                 int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[kBulkStages];
+    __shared__ __align__(8) uint64_t bars[kStages];
     if (threadIdx.x != 0) return;
-    for (int i = 0; i < kBulkStages; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < kStages; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
     ChunkIter it;
@@ -351,37 +353,38 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     it.block_bytes = block_bytes;
     it.token_bytes = token_bytes;
     it.block_tokens = block_tokens;
+    it.chunk = kChunk;
     it.left = 0;
     it.run = 1;
     if (!it.load_unit()) return;
 
-    char* pend_dst[kBulkStages];
-    uint32_t pend_n[kBulkStages];
+    char* pend_dst[kStages];
+    uint32_t pend_n[kStages];
     int64_t issued = 0, stored = 0;
     bool more = true;
     // prologue: fill the ring
-    for (int st = 0; st < kBulkStages && more; ++st) {
+    for (int st = 0; st < kStages && more; ++st) {
         const char* s;
         char* d;
         uint32_t n;
         more = it.next(&s, &d, &n);
         if (!more) break;
         mbar_expect_tx(&bars[st], n);
-        bulk_g2s(smem + (size_t)st * kBulkChunk, s, n, &bars[st]);
+        bulk_g2s(smem + (size_t)st * kChunk, s, n, &bars[st]);
         pend_dst[st] = d;
         pend_n[st] = n;
         ++issued;
     }
     while (stored < issued) {
-        const int st = (int)(stored % kBulkStages);
-        const uint32_t parity = (uint32_t)((stored / kBulkStages) & 1);
+        const int st = (int)(stored % kStages);
+        const uint32_t parity = (uint32_t)((stored / kStages) & 1);
         mbar_wait(&bars[st], parity);
-        bulk_s2g(pend_dst[st], smem + (size_t)st * kBulkChunk, pend_n[st]);
+        bulk_s2g(pend_dst[st], smem + (size_t)st * kChunk, pend_n[st]);
         bulk_commit();
         ++stored;
         // refill the slot stored one iteration ago once its store has read smem
         if (more && stored >= 2) {
-            const int rs = (int)((stored - 2) % kBulkStages);
+            const int rs = (int)((stored - 2) % kStages);
             const char* s;
             char* d;
             uint32_t n;
@@ -389,7 +392,7 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
             if (more) {
                 bulk_wait_read<1>();
                 mbar_expect_tx(&bars[rs], n);
-                bulk_g2s(smem + (size_t)rs * kBulkChunk, s, n, &bars[rs]);
+                bulk_g2s(smem + (size_t)rs * kChunk, s, n, &bars[rs]);
                 pend_dst[rs] = d;
                 pend_n[rs] = n;
                 ++issued;

@@ -12,11 +12,11 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo "launches rc=$?" >> $out/ncu_status.txt
 # 2. DRAM traffic of the C3 wave-0 move kernel (a bench-size launch)
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed \
-    --clock-control none -k regex:kvx_move_kernel -s 6 -c 1 --csv \
+    --clock-control none -k regex:kvx_bulk_kernel -s 6 -c 1 --csv \
     --log-file $out/traffic_c3.csv $C3 > $out/ncu_traffic.log 2>&1
 echo "traffic rc=$?" >> $out/ncu_status.txt
 # 3. full section set on the same kernel at the C1 size (2 GiB wave 0)
 $C1 > $out/plain_c1.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:kvx_move_kernel -s 6 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:kvx_bulk_kernel -s 6 -c 1 \
     -o $out/move_c1 $C1 > $out/ncu_full.log 2>&1
 echo "full rc=$?" >> $out/ncu_status.txt
