@@ -186,6 +186,38 @@ int kvx_bytes_moved(const kvx_transition* t, uint64_t* bytes);
 int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_t* req,
                        const int64_t* kv, int64_t* mismatched_words);
 
+/* ------------------------------------------- stage-boundary activation handoff
+ * Alternative to the barrier drain (engine.cpp:676-678): the in-flight
+ * micro-batches are moved to the new pipeline instead of finishing on the
+ * old one.  A batch holding the output of old stage `after_stage` goes to the
+ * new stage owning layer old_boundaries[after_stage] and resumes there
+ * (same layer range semantics as stage_loads, engine.cpp:115-126); a batch
+ * that has not finished any stage (after_stage < 0) is re-dispatched at new
+ * stage 0 with no bytes.  Destination = a caller-provided activation arena
+ * per new stage (device pointer, local or peer-mapped); each arena is filled
+ * by a bump pointer in batch order, offsets aligned to 256 B.  Slots are
+ * computed for every batch (deterministic on every rank); bytes move only
+ * for batches whose old stage lives on this handle's GPU.  row_bytes (hidden
+ * size x element bytes) must be a multiple of 16, src 16-byte aligned. */
+typedef struct kvx_microbatch {
+    int64_t batch_id;
+    int32_t after_stage;   /* last OLD stage whose output the batch holds; -1 = none */
+    int32_t tokens;        /* activation rows */
+    const void* src;       /* device pointer on the GPU of old stage after_stage */
+} kvx_microbatch;
+
+typedef struct kvx_handoff_slot {
+    int64_t batch_id;
+    int32_t new_stage;     /* new owner */
+    int32_t resume_layer;  /* first layer the new owner runs for this batch */
+    uint64_t offset;       /* byte offset in the new stage's activation arena */
+    uint64_t bytes;
+} kvx_handoff_slot;
+
+int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n,
+                const kvx_microbatch* mb, void* const* arenas, const uint64_t* arena_bytes,
+                kvx_handoff_slot* slots_out);
+
 /* ---------------------------------------------------- control-plane mirror
  * RefactorCtx (engine.hpp:149-158) restated over the handle.  live = the
  * (req, kv_tokens) of every live request homed on the instance, ascending

@@ -301,6 +301,41 @@ struct Observer {
 
     void emit(const json& j) { (*out) << j.dump() << "\n"; }
 
+    // The in-flight micro-batches the barrier leaves to drain
+    // (engine.cpp:142-149,449-464): computing in a stage, queued at a stage
+    // inbound, or in transit between stages.  `after` = the last old stage
+    // whose output the batch holds (-1: none yet); `act_bytes` = the
+    // reference's modelled hop size scale_activation(plan, after, units)
+    // (modelgraph.cpp:220-233, engine.cpp:136-140).  Tokens per unit: the
+    // prompt for a prefill pass, 1 for a decode pass.
+    json microbatches(const Engine::InstanceRt& inst) {
+        const auto& plan = e->cfg_.granularities.plans[(size_t)inst.plan_index].plan;
+        json arr = json::array();
+        auto add = [&](const Engine::MicroBatch& b, const char* where, int after) {
+            json units = json::array();
+            for (const auto& u : b.units) {
+                const auto& rt = e->reqs_[(size_t)u.req];
+                units.push_back({u.req, u.pass, u.pass == 0 ? rt.prompt_tokens : 1});
+            }
+            json j;
+            j["batch"] = b.id;
+            j["where"] = where;
+            j["after"] = after;
+            j["units"] = units;
+            j["act_bytes"] = after >= 0 ? scale_activation(plan, after, (int)b.units.size(),
+                                                           e->cfg_.exec.batch_scaling)
+                                        : 0.0;
+            arr.push_back(j);
+        };
+        for (size_t s = 0; s < inst.stages.size(); ++s) {
+            const auto& st = inst.stages[s];
+            if (st.current) add(*st.current, "current", (int)s - 1);
+            for (const auto& b : st.inbound) add(b, "inbound", (int)s - 1);
+        }
+        for (const auto& [id, b] : inst.in_transit) add(b, "transit", b.transit_from);
+        return arr;
+    }
+
     void observe(double t_ms) {
         const EngineResult& res = e->result_;
         for (const auto& ip : e->instances_) {
@@ -363,6 +398,7 @@ struct Observer {
                 j["rounds"] = ctx.rounds;
                 j["inflight_batches"] = inst.inflight_batches;
                 j["live"] = live;
+                j["microbatches"] = microbatches(inst);
                 emit(j);
             }
             if (ctx.rounds != s.rounds || ctx.commit_scheduled != s.commit_scheduled) {

@@ -392,3 +392,33 @@ int32_t kvo_activation_owner(int32_t old_stages, const int32_t* ob, int32_t new_
     if (from_old_stage < 0 || from_old_stage + 1 >= old_stages) return -1;
     return kvo_stage_of_layer(new_stages, nb, ob[from_old_stage]);
 }
+
+int kvo_handoff_plan(int32_t old_stages, const int32_t* ob, int32_t new_stages, const int32_t* nb,
+                     uint64_t row_bytes, int32_t n, const int32_t* after, const int32_t* tokens,
+                     const uint64_t* arena_bytes, int32_t* new_stage, int32_t* resume_layer,
+                     uint64_t* offset, uint64_t* bytes) {
+    uint64_t bump[256];
+    if (new_stages > 256) return -1;
+    for (int32_t k = 0; k < new_stages; ++k) bump[k] = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (after[i] < 0 || after[i] + 1 >= old_stages) {
+            /* nothing computed yet (or already past the last stage): re-dispatch */
+            new_stage[i] = 0;
+            resume_layer[i] = 0;
+            offset[i] = 0;
+            bytes[i] = 0;
+            continue;
+        }
+        const int32_t layer = ob[after[i]];
+        const int32_t k = kvo_stage_of_layer(new_stages, nb, layer);
+        const uint64_t b = (uint64_t)tokens[i] * row_bytes;
+        const uint64_t off = (bump[k] + 255u) & ~(uint64_t)255u;
+        if (off + b > arena_bytes[k]) return -1;
+        new_stage[i] = k;
+        resume_layer[i] = layer;
+        offset[i] = off;
+        bytes[i] = b;
+        bump[k] = off + b;
+    }
+    return 0;
+}

@@ -154,6 +154,19 @@ int32_t kvo_activation_owner(int32_t old_stages, const int32_t* old_boundaries,
                              int32_t new_stages, const int32_t* new_boundaries,
                              int32_t from_old_stage);
 
+/* Handoff plan for n in-flight micro-batches (instead of the barrier drain,
+ * engine.cpp:676-678).  Batch i holds the output of old stage after[i]
+ * (-1: none yet), tokens[i] rows of row_bytes each.  It goes to the new
+ * stage owning layer old_boundary[after[i]] and resumes there; batches with
+ * after < 0 are re-dispatched at new stage 0, layer 0, with no bytes.  Each
+ * new stage's arena is filled by a bump pointer in batch order, offsets
+ * aligned to 256 B.  Outputs per batch: new stage, resume layer, offset,
+ * bytes.  Returns 0, or -1 if an arena (arena_bytes[k]) would overflow. */
+int kvo_handoff_plan(int32_t old_stages, const int32_t* old_boundaries, int32_t new_stages,
+                     const int32_t* new_boundaries, uint64_t row_bytes, int32_t n,
+                     const int32_t* after, const int32_t* tokens, const uint64_t* arena_bytes,
+                     int32_t* new_stage, int32_t* resume_layer, uint64_t* offset, uint64_t* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,6 +71,8 @@ def lib() -> C.CDLL:
             "kvo_commit": (I64, [P(Geo), P(Dst), I32, P(I32), P(I64), P(I32), P(I32), P(I32), P(I32), P(I32)]),
             "kvo_verify": (I64, [P(Geo), U64, P(Dst), I32, P(I32), PP, I32, P(I32), P(I64)]),
             "kvo_activation_owner": (I32, [I32, P(I32), I32, P(I32), I32]),
+            "kvo_handoff_plan": (C.c_int, [I32, P(I32), I32, P(I32), U64, I32, P(I32), P(I32), P(U64),
+                                           P(I32), P(I32), P(U64), P(U64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -219,3 +221,18 @@ def activation_owner(old_b, new_b, from_old_stage: int) -> int:
     ob, nb = _i32(list(old_b)), _i32(list(new_b))
     return int(lib().kvo_activation_owner(len(ob) + 1, _p(ob, C.c_int32), len(nb) + 1,
                                           _p(nb, C.c_int32), from_old_stage))
+
+
+def handoff_plan(old_b, new_b, row_bytes: int, after, tokens, arena_bytes):
+    """kvo_handoff_plan -> (rc, new_stage, resume_layer, offset, bytes)."""
+    ob, nb = _i32(list(old_b)), _i32(list(new_b))
+    after, tokens = _i32(after), _i32(tokens)
+    cap = np.ascontiguousarray(arena_bytes, dtype=np.uint64)
+    n = len(after)
+    ns, rl = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    off, by = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+    rc = lib().kvo_handoff_plan(len(ob) + 1, _p(ob, C.c_int32), len(nb) + 1, _p(nb, C.c_int32),
+                                row_bytes, n, _p(after, C.c_int32), _p(tokens, C.c_int32),
+                                _p(cap, C.c_uint64), _p(ns, C.c_int32), _p(rl, C.c_int32),
+                                _p(off, C.c_uint64), _p(by, C.c_uint64))
+    return int(rc), ns, rl, off, by

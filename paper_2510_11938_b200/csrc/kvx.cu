@@ -177,6 +177,12 @@ struct kvx_transition {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> move_ev;
     std::vector<uint64_t> move_bytes;
 
+    // activation handoff pieces (grown on demand, freed at destroy)
+    kvx::Piece* d_pieces = nullptr;
+    kvx::Piece* h_pieces = nullptr;
+    int64_t piece_cap = 0;
+    cudaEvent_t pieces_free = nullptr;
+
     // host mirror of the destination rule (capacity checks are synchronous)
     std::vector<int64_t> synced_hi;
     int32_t alloc = 0;
@@ -431,13 +437,13 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bv.fn, kvx::kBulkThreads, smem) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "bulk kernel attributes"));
         t->bulk_ctas_per_sm = std::max(1, occ);
-        // Bulk (TMA engine) mover by default for local destinations; the LSU
-        // mover for peer (NVLink) destinations unless KVX_PEER_BULK=1, and
-        // everywhere with KVX_MOVE_IMPL=lsu.
+        // Bulk (TMA engine) mover by default, for local and peer (NVLink)
+        // destinations alike; KVX_PEER_BULK=0 keeps the LSU mover for peer
+        // pushes, KVX_MOVE_IMPL=lsu everywhere.
         const char* impl = getenv("KVX_MOVE_IMPL");
         t->use_bulk = !(impl && std::string(impl) == "lsu");
         const char* pb = getenv("KVX_PEER_BULK");
-        t->peer_bulk = t->use_bulk && pb && std::string(pb) == "1";
+        t->peer_bulk = t->use_bulk && !(pb && std::string(pb) == "0");
     }
 
     if (d->stream) {
@@ -742,12 +748,94 @@ int kvx_destroy(kvx_transition* t) {
     }
     A.event_free(t->ev_begin, true);
     A.event_free(t->ev_end, true);
+    A.dev_free(t->d_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
+    A.host_free(t->h_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
+    A.event_free(t->pieces_free, false);
     for (auto& ev : t->move_ev) {
         A.event_free(ev.first, true);
         A.event_free(ev.second, true);
     }
     if (t->stream && t->own_stream) cudaStreamDestroy(t->stream);
     delete t;
+    return KVX_OK;
+}
+
+int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n,
+                const kvx_microbatch* mb, void* const* arenas, const uint64_t* arena_bytes,
+                kvx_handoff_slot* slots_out) {
+    if (!t) return fail(KVX_EINVAL, "transition is null");
+    if (epoch != t->epoch) return fail(KVX_ESTALE, "stale epoch");
+    if (t->state != kvx_transition::kActive) return fail(KVX_ESTATE, "transition is not active");
+    if (n < 0 || (n > 0 && (!mb || !slots_out)) || !arenas || !arena_bytes || row_bytes % 16 != 0)
+        return fail(KVX_EINVAL, "bad handoff arguments");
+    const int k_old = (int)t->old_b.size() + 1, k_new = (int)t->new_b.size() + 1;
+    std::vector<uint64_t> bump((size_t)k_new, 0);
+    std::vector<kvx::Piece> pieces;
+    for (int32_t i = 0; i < n; ++i) {
+        kvx_handoff_slot& sl = slots_out[i];
+        sl.batch_id = mb[i].batch_id;
+        if (mb[i].tokens < 0) return fail(KVX_EINVAL, "negative tokens");
+        const int32_t a = mb[i].after_stage;
+        if (a < 0 || a + 1 >= k_old) {  // nothing computed yet: re-dispatch at the new head
+            sl.new_stage = 0;
+            sl.resume_layer = 0;
+            sl.offset = 0;
+            sl.bytes = 0;
+            continue;
+        }
+        const int32_t layer = t->old_b[(size_t)a];
+        const int k = stage_of_layer(t->new_b, layer);
+        const uint64_t b = (uint64_t)mb[i].tokens * row_bytes;
+        const uint64_t off = (bump[(size_t)k] + 255u) & ~(uint64_t)255u;
+        if (off + b > arena_bytes[k]) return fail(KVX_ENOSPC, "activation arena full");
+        sl.new_stage = k;
+        sl.resume_layer = layer;
+        sl.offset = off;
+        sl.bytes = b;
+        bump[(size_t)k] = off + b;
+        const kvx_pool* src_pool = t->old_pools[(size_t)a];
+        const bool local = src_pool && !src_pool->imported && src_pool->device == t->device;
+        if (!local || b == 0) continue;
+        if (!mb[i].src || !arenas[k] || (reinterpret_cast<uintptr_t>(mb[i].src) & 15) ||
+            (reinterpret_cast<uintptr_t>(arenas[k]) & 15))
+            return fail(KVX_EINVAL, "activation pointers must be non-null and 16-byte aligned");
+        pieces.push_back({static_cast<const char*>(mb[i].src), static_cast<char*>(arenas[k]) + off, b});
+    }
+    if (pieces.empty()) return KVX_OK;
+    DeviceGuard dg(t->device);
+    kvx::Arena& A = kvx::Arena::of(t->device);
+    if (!t->pieces_free) KVX_CUDA(A.event(&t->pieces_free, false));
+    KVX_CUDA(cudaEventSynchronize(t->pieces_free));  // previous handoff's upload consumed
+    if ((int64_t)pieces.size() > t->piece_cap) {
+        A.dev_free(t->d_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
+        A.host_free(t->h_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
+        t->d_pieces = nullptr;
+        t->h_pieces = nullptr;
+        const int64_t cap = (int64_t)(kvx::size_class(sizeof(kvx::Piece) * pieces.size()) / sizeof(kvx::Piece));
+        KVX_CUDA(cudaStreamSynchronize(t->stream));
+        KVX_CUDA(A.dev_alloc((void**)&t->d_pieces, sizeof(kvx::Piece) * (size_t)cap));
+        KVX_CUDA(A.host_alloc((void**)&t->h_pieces, sizeof(kvx::Piece) * (size_t)cap));
+        t->piece_cap = cap;
+    }
+    std::memcpy(t->h_pieces, pieces.data(), sizeof(kvx::Piece) * pieces.size());
+    KVX_CUDA(cudaMemcpyAsync(t->d_pieces, t->h_pieces, sizeof(kvx::Piece) * pieces.size(),
+                             cudaMemcpyHostToDevice, t->stream));
+    KVX_CUDA(cudaEventRecord(t->pieces_free, t->stream));
+    constexpr int kStages = 4;
+    constexpr uint32_t kChunk = 32768;
+    static bool attr_set = false;
+    if (!attr_set) {
+        KVX_CUDA(cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kStages, kChunk>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * (int)kChunk));
+        attr_set = true;
+    }
+    uint64_t total = 0;
+    for (const auto& p : pieces) total += p.bytes;
+    const int64_t want = std::max<int64_t>(1, (int64_t)(total / (256 * 1024)));
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)t->num_sms, std::min<int64_t>(want, (int64_t)pieces.size()));
+    kvx::kvx_copy_list_kernel<kStages, kChunk><<<grid, kvx::kBulkThreads, kStages * kChunk, t->stream>>>(
+        t->d_pieces, (int64_t)pieces.size());
+    KVX_LAUNCHED();
     return KVX_OK;
 }
 

@@ -333,37 +333,17 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
     }
 };
 
-template <int kStages, uint32_t kChunk>
-__global__ void __launch_bounds__(kBulkThreads)
-kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
-                int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[kStages];
-    if (threadIdx.x != 0) return;
+// Generic single-thread bulk streaming loop over any chunk iterator with
+// `bool next(const char**, char**, uint32_t*)`.
+template <int kStages, uint32_t kChunk, class Iter>
+__device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint64_t* bars) {
     for (int i = 0; i < kStages; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-
-    ChunkIter it;
-    it.segs = segs;
-    it.layers = layers;
-    it.nseg = nseg;
-    it.units = (int64_t)nseg * nlayers;
-    it.u = blockIdx.x;
-    it.ustep = gridDim.x;
-    it.block_bytes = block_bytes;
-    it.token_bytes = token_bytes;
-    it.block_tokens = block_tokens;
-    it.chunk = kChunk;
-    it.left = 0;
-    it.run = 1;
-    if (!it.load_unit()) return;
-
     char* pend_dst[kStages];
     uint32_t pend_n[kStages];
     int64_t issued = 0, stored = 0;
     bool more = true;
-    // prologue: fill the ring
-    for (int st = 0; st < kStages && more; ++st) {
+    for (int st = 0; st < kStages && more; ++st) {  // prologue: fill the ring
         const char* s;
         char* d;
         uint32_t n;
@@ -400,6 +380,81 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
         }
     }
     bulk_wait_all();
+}
+
+template <int kStages, uint32_t kChunk>
+__global__ void __launch_bounds__(kBulkThreads)
+kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
+                int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[kStages];
+    if (threadIdx.x != 0) return;
+    ChunkIter it;
+    it.segs = segs;
+    it.layers = layers;
+    it.nseg = nseg;
+    it.units = (int64_t)nseg * nlayers;
+    it.u = blockIdx.x;
+    it.ustep = gridDim.x;
+    it.block_bytes = block_bytes;
+    it.token_bytes = token_bytes;
+    it.block_tokens = block_tokens;
+    it.chunk = kChunk;
+    it.left = 0;
+    it.run = 1;
+    if (!it.load_unit()) return;
+    bulk_stream<kStages, kChunk>(it, smem, bars);
+}
+
+// ------------------------------------------------- generic copy list
+// Activation handoff (and any batched device copy): a list of (src, dst,
+// bytes) pieces, 16-byte aligned, streamed by the same bulk engine loop.
+struct Piece {
+    const char* src;
+    char* dst;
+    uint64_t bytes;
+};
+
+struct PieceIter {
+    const Piece* p;
+    int64_t n, i, step;
+    const char* src;
+    char* dst;
+    uint64_t left;
+    uint32_t chunk;
+    __device__ bool next(const char** s, char** d, uint32_t* c) {
+        while (left == 0) {
+            i += step;
+            if (i >= n) return false;
+            src = p[i].src;
+            dst = p[i].dst;
+            left = p[i].bytes;
+        }
+        const uint32_t k = left > chunk ? chunk : (uint32_t)left;
+        *s = src;
+        *d = dst;
+        *c = k;
+        src += k;
+        dst += k;
+        left -= k;
+        return true;
+    }
+};
+
+template <int kStages, uint32_t kChunk>
+__global__ void __launch_bounds__(kBulkThreads)
+kvx_copy_list_kernel(const Piece* __restrict__ pieces, int64_t n) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[kStages];
+    if (threadIdx.x != 0 || (int64_t)blockIdx.x >= n) return;
+    PieceIter it;
+    it.p = pieces;
+    it.n = n;
+    it.step = gridDim.x;
+    it.i = (int64_t)blockIdx.x - it.step;
+    it.left = 0;
+    it.chunk = kChunk;
+    bulk_stream<kStages, kChunk>(it, smem, bars);
 }
 
 // ------------------------------------------------------------- commit

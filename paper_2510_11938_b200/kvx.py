@@ -88,6 +88,16 @@ class _CommitResult(C.Structure):
                 ("free_cap", C.c_int32), ("n_free", C.c_int32)]
 
 
+class MicroBatch(C.Structure):
+    _fields_ = [("batch_id", C.c_int64), ("after_stage", C.c_int32), ("tokens", C.c_int32),
+                ("src", C.c_void_p)]
+
+
+class HandoffSlot(C.Structure):
+    _fields_ = [("batch_id", C.c_int64), ("new_stage", C.c_int32), ("resume_layer", C.c_int32),
+                ("offset", C.c_uint64), ("bytes", C.c_uint64)]
+
+
 class _CtlState(C.Structure):
     _fields_ = [("rounds", C.c_int32), ("barrier", C.c_int32), ("commit_scheduled", C.c_int32),
                 ("waves", C.c_int32), ("kv_synced_bytes", C.c_double),
@@ -127,6 +137,7 @@ def _load() -> C.CDLL:
         "kvx_bytes_moved": (C.c_int, [VP, P(U64)]),
         "kvx_move_timings": (C.c_int, [VP, I32, P(C.c_double), P(U64), P(I32)]),
         "kvx_verify_pattern": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(I64)]),
+        "kvx_handoff": (C.c_int, [VP, U64, U64, I32, P(MicroBatch), P(VP), P(U64), P(HandoffSlot)]),
         "kvx_ctl_begin": (C.c_int, [VP, I32, P(I32), P(I64), P(I64)]),
         "kvx_ctl_sync_complete": (C.c_int, [VP, U64, I32, P(I32), P(I64), I32, P(I32), P(I64)]),
         "kvx_ctl_commit": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(_CommitResult)]),
@@ -366,6 +377,21 @@ class Transition:
         bad = C.c_int64()
         _check(_lib.kvx_verify_pattern(self._h, seed, len(req), _p32(req), _p64(kv), C.byref(bad)))
         return int(bad.value)
+
+    def handoff(self, row_bytes: int, batches, arenas, arena_bytes, epoch: Optional[int] = None):
+        """Stage-boundary activation handoff.  batches: [(batch_id, after_stage,
+        tokens, src_device_ptr)]; arenas: per-new-stage device pointers.
+        Returns [(batch_id, new_stage, resume_layer, offset, bytes)]."""
+        n = len(batches)
+        mb = (MicroBatch * max(n, 1))(*[MicroBatch(int(b), int(a), int(tk), int(p) or None)
+                                        for b, a, tk, p in batches])
+        ar = (C.c_void_p * len(arenas))(*[int(a) or None for a in arenas])
+        cap = (C.c_uint64 * len(arena_bytes))(*[int(x) for x in arena_bytes])
+        out = (HandoffSlot * max(n, 1))()
+        _check(_lib.kvx_handoff(self._h, self.epoch if epoch is None else epoch, row_bytes, n, mb,
+                                ar, cap, out))
+        return [(out[i].batch_id, out[i].new_stage, out[i].resume_layer, out[i].offset, out[i].bytes)
+                for i in range(n)]
 
     # --------------------------------------------- reference-shaped handlers
     def begin_refactor(self, live: Tuple[np.ndarray, np.ndarray]) -> int:

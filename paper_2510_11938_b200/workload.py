@@ -44,12 +44,23 @@ class Wave:
 
 
 @dataclass
+class MicroBatchRec:
+    """An in-flight micro-batch at the barrier (engine.cpp:449-464)."""
+    batch: int
+    where: str          # current | inbound | transit
+    after: int          # last old stage whose output it holds (-1: none)
+    tokens: int         # activation rows: prompt for prefill units, 1 per decode unit
+    act_bytes: float    # reference's modelled hop size (scale_activation)
+
+
+@dataclass
 class Barrier:
     """engine.cpp:676: the barrier fell; live set + in-flight batches it saw."""
     rounds: int
     inflight_batches: int
     req: np.ndarray
     kv: np.ndarray
+    microbatches: list = field(default_factory=list)
 
 
 @dataclass
@@ -117,8 +128,10 @@ def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
             cur[r["instance"]].events.append(w)
         elif k == "barrier":
             e = np.array(r["live"], dtype=np.int64).reshape(-1, 2)
+            mbs = [MicroBatchRec(m["batch"], m["where"], m["after"], int(sum(u[2] for u in m["units"])),
+                                 m["act_bytes"]) for m in r.get("microbatches", [])]
             cur[r["instance"]].events.append(Barrier(r["rounds"], r["inflight_batches"],
-                                                     e[:, 0].astype(np.int32), e[:, 1].copy()))
+                                                     e[:, 0].astype(np.int32), e[:, 1].copy(), mbs))
         elif k == "commit_state":
             e = np.array(r["live"], dtype=np.int64).reshape(-1, 2)
             t = cur[r["instance"]]
