@@ -799,7 +799,11 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
         if (!mb[i].src || !arenas[k] || (reinterpret_cast<uintptr_t>(mb[i].src) & 15) ||
             (reinterpret_cast<uintptr_t>(arenas[k]) & 15))
             return fail(KVX_EINVAL, "activation pointers must be non-null and 16-byte aligned");
-        pieces.push_back({static_cast<const char*>(mb[i].src), static_cast<char*>(arenas[k]) + off, b});
+        // 64 KiB sub-pieces so one large activation spreads over many CTAs
+        const char* src = static_cast<const char*>(mb[i].src);
+        char* dst = static_cast<char*>(arenas[k]) + off;
+        for (uint64_t o = 0; o < b; o += 65536)
+            pieces.push_back({src + o, dst + o, std::min<uint64_t>(65536, b - o)});
     }
     if (pieces.empty()) return KVX_OK;
     DeviceGuard dg(t->device);
@@ -829,10 +833,7 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * (int)kChunk));
         attr_set = true;
     }
-    uint64_t total = 0;
-    for (const auto& p : pieces) total += p.bytes;
-    const int64_t want = std::max<int64_t>(1, (int64_t)(total / (256 * 1024)));
-    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)t->num_sms, std::min<int64_t>(want, (int64_t)pieces.size()));
+    const unsigned grid = (unsigned)std::min<int64_t>(2 * (int64_t)t->num_sms, (int64_t)pieces.size());
     kvx::kvx_copy_list_kernel<kStages, kChunk><<<grid, kvx::kBulkThreads, kStages * kChunk, t->stream>>>(
         t->d_pieces, (int64_t)pieces.size());
     KVX_LAUNCHED();
