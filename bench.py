@@ -268,6 +268,7 @@ def main():
     ap.add_argument("--placement", default="affinity", choices=["affinity", "disjoint"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-weights", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -441,6 +442,36 @@ def main():
                    "note": "in-flight micro-batches of the reference's barrier moved to their new "
                            "owners instead of drained (hidden x fp16 rows)"}
 
+    # ---- stage weight migration: the new stages' parameters
+    #      gathered by layer range on the device (N=1; fp16 weights of the shape)
+    weights = None
+    if world == 1 and not args.no_weights:
+        params = {"llama2-13b": 26.0e9, "llama2-7b": 13.5e9, "llama2-70b": 138.0e9}[CONFIGS[args.config][1]]
+        lb = int(params / L) // 4096 * 4096
+        if lb * L * 2 < 120e9:
+            wold = [torch.empty((e - b) * lb, dtype=torch.uint8, device=dev)
+                    for b, e in W.stage_ranges(L, t.old_boundaries)]
+            wnew = [torch.empty((e - b) * lb, dtype=torch.uint8, device=dev)
+                    for b, e in W.stage_ranges(L, t.new_boundaries)]
+            wt = []
+            for rep in range(4):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                kvx.weights_migrate(dev, L, lb, t.old_boundaries, [x.data_ptr() for x in wold],
+                                    t.new_boundaries, [x.data_ptr() for x in wnew], stream=sp)
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                if rep:
+                    wt.append(a.elapsed_time(b))
+            wms = statistics.median(wt)
+            wbytes = lb * L
+            weights = {"bytes": wbytes, "ms": round(wms, 3), "GB_s": round(wbytes / (wms * 1e-3) / 1e9, 1),
+                       "hbm_frac": round(2 * wbytes / (wms * 1e-3) / 1e9 / peaks()[0], 4),
+                       "reference_load_ms": plan.t.load_ready_ms - plan.t.t_ms,
+                       "note": "device-to-device layer-range gather of the new stages' weights; the "
+                               "reference models this as host/storage loads (load_ready_ms)"}
+            del wold, wnew
+
     # ---- roofline of the dominant kernel
     peak, peak_kind = peaks()
     layer_bytes = plan.wave0_tokens * 2 * plan.token_bytes  # K+V bytes per layer in wave 0
@@ -497,6 +528,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                 "ms_per_step": round(e2e_s * 1e3 / e2e_steps, 4)},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "handoff": handoff,
+        "weights": weights,
         "move_kernel_ms_per_step": round(all_move_ms / K, 4), "move_ms_by_wave": wave_ms,
         "mover": os.environ.get("KVX_MOVE_IMPL", "bulk") + ":" + os.environ.get("KVX_BULK_CFG", "0"),
     }

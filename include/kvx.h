@@ -218,6 +218,24 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
                 const kvx_microbatch* mb, void* const* arenas, const uint64_t* arena_bytes,
                 kvx_handoff_slot* slots_out);
 
+/* ------------------------------------------------- stage weight migration
+ * The parameters a new stage needs before commit (the reference models them
+ * as per-server loads the commit waits on: engine.cpp:621-631,686 and
+ * warm_start_latency_ms, cluster.cpp:525-536).  Each stage's weights are one
+ * contiguous layer-major buffer of layer_bytes per layer.  For every layer
+ * whose old stage buffer is local (old_ptrs[k] non-NULL, on `device`), the
+ * layer is copied into the new stage buffer that owns it (local, or a
+ * peer-mapped pointer over NVLink) by the bulk copy engine kernel; layers
+ * with from_host[l] == 1 are instead loaded from the pinned host cache
+ * host_cache + l * layer_bytes (the reference's host tier).  Asynchronous on
+ * `stream` (NULL = the legacy default stream); *device_bytes / *host_bytes
+ * receive the bytes scheduled. */
+int kvx_weights_migrate(int32_t device, void* stream, int32_t num_layers, uint64_t layer_bytes,
+                        int32_t old_stages, const int32_t* old_boundaries, void* const* old_ptrs,
+                        int32_t new_stages, const int32_t* new_boundaries, void* const* new_ptrs,
+                        const void* host_cache, const uint8_t* from_host, uint64_t* device_bytes,
+                        uint64_t* host_bytes);
+
 /* ---------------------------------------------------- control-plane mirror
  * RefactorCtx (engine.hpp:149-158) restated over the handle.  live = the
  * (req, kv_tokens) of every live request homed on the instance, ascending

@@ -301,6 +301,33 @@ struct Observer {
 
     void emit(const json& j) { (*out) << j.dump() << "\n"; }
 
+    // Per-server parameter loads of the new stages, as begin_refactor
+    // computed them (engine.cpp:621-631): each stage's op range, bytes and
+    // whether the server's host cache covers it (cluster.cpp:176-195), plus
+    // the reference's warm_start_latency_ms (cluster.cpp:525-536).
+    json param_loads(const Engine::InstanceRt& inst, const Engine::RefactorCtx& ctx) {
+        const auto loads = e->stage_loads(ctx.target_plan);
+        const std::string& model = e->models_[(size_t)inst.model].name;
+        std::map<int, std::vector<StageLoad>> per_server;
+        for (size_t k = 0; k < ctx.new_gpus.size(); ++k)
+            per_server[e->hrg_.gpu(ctx.new_gpus[k]).server_id].push_back(loads[k]);
+        json arr = json::array();
+        for (const auto& [server, ls] : per_server) {
+            json st = json::array();
+            for (const auto& l : ls)
+                st.push_back({l.begin_op, l.end_op, l.bytes,
+                              e->affinity_.cache_covers(server, model, l.begin_op, l.end_op)});
+            json j;
+            j["server"] = server;
+            j["stages"] = st;
+            j["host_bw"] = e->hrg_.server(server).host_bw_bytes_per_ms;
+            j["storage_bw"] = e->hrg_.storage_bw_bytes_per_ms;
+            j["latency_ms"] = warm_start_latency_ms(e->hrg_, e->affinity_, server, model, ls);
+            arr.push_back(j);
+        }
+        return arr;
+    }
+
     // The in-flight micro-batches the barrier leaves to drain
     // (engine.cpp:142-149,449-464): computing in a stage, queued at a stage
     // inbound, or in transit between stages.  `after` = the last old stage
@@ -376,6 +403,8 @@ struct Observer {
                 j["new"] = plan_json(*e, ctx.target_plan);
                 j["new_gpus"] = ctx.new_gpus;
                 j["load_ready_ms"] = ctx.load_ready_ms;
+                j["begin_ms"] = begin_ms[inst.id];  // now_ms of begin_refactor
+                j["param_loads"] = param_loads(inst, ctx);
                 emit(j);
             }
             if (ctx.barrier && !s.barrier) {
@@ -431,8 +460,11 @@ struct Observer {
         }
     }
 
+    std::map<std::int64_t, double> begin_ms;  // time of the last RefactorBegin per instance
+
     void before(const SimEvent& ev) {
         observe(ev.time_ms);
+        if (ev.kind == EventKind::RefactorBegin) begin_ms[ev.instance_id] = ev.time_ms;
         if (ev.kind == EventKind::RefactorCommit) {
             auto& inst = *e->instances_[static_cast<std::size_t>(ev.instance_id)];
             if (inst.state != Engine::InstState::Refactoring || !inst.refactor) return;

@@ -422,3 +422,27 @@ int kvo_handoff_plan(int32_t old_stages, const int32_t* ob, int32_t new_stages, 
     }
     return 0;
 }
+
+void kvo_weights_plan(int32_t num_layers, uint64_t layer_bytes, int32_t old_stages,
+                      const int32_t* ob, int32_t new_stages, const int32_t* nb, int32_t* src_stage,
+                      uint64_t* src_off, int32_t* dst_stage, uint64_t* dst_off) {
+    for (int32_t l = 0; l < num_layers; ++l) {
+        const int32_t so = kvo_stage_of_layer(old_stages, ob, l);
+        const int32_t sn = kvo_stage_of_layer(new_stages, nb, l);
+        src_stage[l] = so;
+        dst_stage[l] = sn;
+        src_off[l] = (uint64_t)(l - kvo_stage_begin(old_stages, ob, so)) * layer_bytes;
+        dst_off[l] = (uint64_t)(l - kvo_stage_begin(new_stages, nb, sn)) * layer_bytes;
+    }
+}
+
+double kvo_warm_start_ms(int32_t n, const double* stage_bytes, const uint8_t* cached,
+                         double host_bw, double storage_bw) {
+    /* cluster.cpp:525-536 */
+    double total = 0.0;
+    for (int32_t k = 0; k < n; ++k) {
+        if (stage_bytes[k] <= 0.0) continue;
+        total += stage_bytes[k] / (cached[k] ? host_bw : storage_bw);
+    }
+    return total;
+}

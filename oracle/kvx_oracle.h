@@ -167,6 +167,23 @@ int kvo_handoff_plan(int32_t old_stages, const int32_t* old_boundaries, int32_t 
                      const int32_t* after, const int32_t* tokens, const uint64_t* arena_bytes,
                      int32_t* new_stage, int32_t* resume_layer, uint64_t* offset, uint64_t* bytes);
 
+/* Stage weight migration: the new stage k needs the parameters of layers
+ * [nb[k-1], nb[k]) (stage_loads, engine.cpp:115-126), which the reference
+ * loads from host cache or storage before commit (engine.cpp:621-631,686;
+ * warm_start_latency_ms, cluster.cpp:525-536).  With layer-major contiguous
+ * stage buffers, layer l moves from old stage so(l) at offset
+ * (l - begin(so)) * layer_bytes to new stage sn(l) at (l - begin(sn)) *
+ * layer_bytes.  Fills per-layer (src_stage, src_off, dst_stage, dst_off). */
+void kvo_weights_plan(int32_t num_layers, uint64_t layer_bytes, int32_t old_stages,
+                      const int32_t* old_boundaries, int32_t new_stages,
+                      const int32_t* new_boundaries, int32_t* src_stage, uint64_t* src_off,
+                      int32_t* dst_stage, uint64_t* dst_off);
+/* The reference's own parameter-load time for one server's new stages:
+ * sum over stages of bytes / (host bw if the range is host-cached, else
+ * storage bw) -- warm_start_latency_ms restated (cached[k] = cache_covers). */
+double kvo_warm_start_ms(int32_t n, const double* stage_bytes, const uint8_t* cached,
+                         double host_bw_bytes_per_ms, double storage_bw_bytes_per_ms);
+
 #ifdef __cplusplus
 }
 #endif

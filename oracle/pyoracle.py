@@ -71,6 +71,8 @@ def lib() -> C.CDLL:
             "kvo_commit": (I64, [P(Geo), P(Dst), I32, P(I32), P(I64), P(I32), P(I32), P(I32), P(I32), P(I32)]),
             "kvo_verify": (I64, [P(Geo), U64, P(Dst), I32, P(I32), PP, I32, P(I32), P(I64)]),
             "kvo_activation_owner": (I32, [I32, P(I32), I32, P(I32), I32]),
+            "kvo_weights_plan": (None, [I32, U64, I32, P(I32), I32, P(I32), P(I32), P(U64), P(I32), P(U64)]),
+            "kvo_warm_start_ms": (C.c_double, [I32, P(C.c_double), P(C.c_uint8), C.c_double, C.c_double]),
             "kvo_handoff_plan": (C.c_int, [I32, P(I32), I32, P(I32), U64, I32, P(I32), P(I32), P(U64),
                                            P(I32), P(I32), P(U64), P(U64)]),
         }
@@ -236,3 +238,19 @@ def handoff_plan(old_b, new_b, row_bytes: int, after, tokens, arena_bytes):
                                 _p(cap, C.c_uint64), _p(ns, C.c_int32), _p(rl, C.c_int32),
                                 _p(off, C.c_uint64), _p(by, C.c_uint64))
     return int(rc), ns, rl, off, by
+
+
+def weights_plan(num_layers, layer_bytes, old_b, new_b):
+    ob, nb = _i32(list(old_b)), _i32(list(new_b))
+    ss, ds = np.zeros(num_layers, np.int32), np.zeros(num_layers, np.int32)
+    so, do = np.zeros(num_layers, np.uint64), np.zeros(num_layers, np.uint64)
+    lib().kvo_weights_plan(num_layers, layer_bytes, len(ob) + 1, _p(ob, C.c_int32), len(nb) + 1,
+                           _p(nb, C.c_int32), _p(ss, C.c_int32), _p(so, C.c_uint64),
+                           _p(ds, C.c_int32), _p(do, C.c_uint64))
+    return ss, so, ds, do
+
+
+def warm_start_ms(stage_bytes, cached, host_bw, storage_bw) -> float:
+    b = np.ascontiguousarray(stage_bytes, dtype=np.float64)
+    c = np.ascontiguousarray(cached, dtype=np.uint8)
+    return float(lib().kvo_warm_start_ms(len(b), _p(b, C.c_double), _p(c, C.c_uint8), host_bw, storage_bw))

@@ -840,6 +840,86 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
     return KVX_OK;
 }
 
+namespace {
+struct PieceRelease {  // returns a call's descriptor buffers to the arena once the stream passed them
+    int device;
+    void* d;
+    void* h;
+    size_t bytes;
+};
+void CUDART_CB release_pieces(void* arg) {
+    auto* r = static_cast<PieceRelease*>(arg);
+    kvx::Arena& A = kvx::Arena::of(r->device);
+    A.dev_free(r->d, r->bytes);
+    A.host_free(r->h, r->bytes);
+    delete r;
+}
+}  // namespace
+
+int kvx_weights_migrate(int32_t device, void* stream, int32_t num_layers, uint64_t layer_bytes,
+                        int32_t old_stages, const int32_t* old_boundaries, void* const* old_ptrs,
+                        int32_t new_stages, const int32_t* new_boundaries, void* const* new_ptrs,
+                        const void* host_cache, const uint8_t* from_host, uint64_t* device_bytes,
+                        uint64_t* host_bytes) {
+    std::string why;
+    if (num_layers < 1 || layer_bytes == 0 || layer_bytes % 16 != 0 || !old_ptrs || !new_ptrs)
+        return fail(KVX_EINVAL, "weights: bad layer count / layer_bytes (multiple of 16) / pointers");
+    const kvx_plan op{old_stages, old_boundaries, nullptr}, np{new_stages, new_boundaries, nullptr};
+    std::vector<int32_t> ob, nb;
+    kvx_plan op2 = op, np2 = np;
+    kvx_pool* dummy = nullptr;
+    op2.pools = &dummy;
+    np2.pools = &dummy;
+    if (!plan_ok(op2, num_layers, &why, &ob)) return fail(KVX_EINVAL, "weights old plan: " + why);
+    if (!plan_ok(np2, num_layers, &why, &nb)) return fail(KVX_EINVAL, "weights new plan: " + why);
+    std::vector<kvx::Piece> pieces;
+    uint64_t dev_b = 0, host_b = 0;
+    DeviceGuard dg(device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (int32_t l = 0; l < num_layers; ++l) {
+        const int so = stage_of_layer(ob, l), sn = stage_of_layer(nb, l);
+        char* dst = static_cast<char*>(new_ptrs[sn]);
+        if (!dst) return fail(KVX_EINVAL, "weights: every new stage buffer is required");
+        dst += (uint64_t)(l - stage_begin(nb, sn)) * layer_bytes;
+        if (from_host && from_host[l]) {
+            if (!host_cache) return fail(KVX_EINVAL, "weights: from_host without a host cache");
+            // host tier: only the rank that would otherwise source the layer loads it
+            if (!old_ptrs[so]) continue;
+            KVX_CUDA(cudaMemcpyAsync(dst, static_cast<const char*>(host_cache) + (uint64_t)l * layer_bytes,
+                                     layer_bytes, cudaMemcpyHostToDevice, st));
+            host_b += layer_bytes;
+            continue;
+        }
+        if (!old_ptrs[so]) continue;  // another rank owns this layer's source
+        const char* src = static_cast<const char*>(old_ptrs[so]) + (uint64_t)(l - stage_begin(ob, so)) * layer_bytes;
+        for (uint64_t o = 0; o < layer_bytes; o += (1u << 20))
+            pieces.push_back({src + o, dst + o, std::min<uint64_t>(1u << 20, layer_bytes - o)});
+        dev_b += layer_bytes;
+    }
+    if (device_bytes) *device_bytes = dev_b;
+    if (host_bytes) *host_bytes = host_b;
+    if (pieces.empty()) return KVX_OK;
+    int sms = 0;
+    KVX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    kvx::Arena& A = kvx::Arena::of(device);
+    const size_t bytes = sizeof(kvx::Piece) * pieces.size();
+    void *d = nullptr, *h = nullptr;
+    KVX_CUDA(A.dev_alloc(&d, bytes));
+    KVX_CUDA(A.host_alloc(&h, bytes));
+    std::memcpy(h, pieces.data(), bytes);
+    KVX_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+    constexpr int kStages = 6;
+    constexpr uint32_t kChunk = 32768;
+    KVX_CUDA(cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kStages, kChunk>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * (int)kChunk));
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms, (int64_t)pieces.size());
+    kvx::kvx_copy_list_kernel<kStages, kChunk><<<grid, kvx::kBulkThreads, kStages * kChunk, st>>>(
+        static_cast<const kvx::Piece*>(d), (int64_t)pieces.size());
+    KVX_LAUNCHED();
+    KVX_CUDA(cudaLaunchHostFunc(st, release_pieces, new PieceRelease{device, d, h, bytes}));
+    return KVX_OK;
+}
+
 int kvx_epoch(const kvx_transition* t, uint64_t* epoch) {
     if (!t || !epoch) return fail(KVX_EINVAL, "null argument");
     *epoch = t->epoch;

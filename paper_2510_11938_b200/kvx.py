@@ -138,6 +138,8 @@ def _load() -> C.CDLL:
         "kvx_move_timings": (C.c_int, [VP, I32, P(C.c_double), P(U64), P(I32)]),
         "kvx_verify_pattern": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(I64)]),
         "kvx_handoff": (C.c_int, [VP, U64, U64, I32, P(MicroBatch), P(VP), P(U64), P(HandoffSlot)]),
+        "kvx_weights_migrate": (C.c_int, [I32, VP, I32, U64, I32, P(I32), P(VP), I32, P(I32), P(VP),
+                                          VP, P(C.c_uint8), P(U64), P(U64)]),
         "kvx_ctl_begin": (C.c_int, [VP, I32, P(I32), P(I64), P(I64)]),
         "kvx_ctl_sync_complete": (C.c_int, [VP, U64, I32, P(I32), P(I64), I32, P(I32), P(I64)]),
         "kvx_ctl_commit": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(_CommitResult)]),
@@ -439,3 +441,22 @@ class Transition:
             self.close()
         except Exception:
             pass
+
+
+def weights_migrate(device: int, num_layers: int, layer_bytes: int, old_boundaries, old_ptrs,
+                    new_boundaries, new_ptrs, stream: int = 0, host_cache: int = 0,
+                    from_host=None) -> Tuple[int, int]:
+    """Stage weight migration (kvx_weights_migrate): returns (device bytes,
+    host-tier bytes) scheduled on `stream`."""
+    ob, nb = _i32(list(old_boundaries)), _i32(list(new_boundaries))
+    op = (C.c_void_p * len(old_ptrs))(*[int(p) or None for p in old_ptrs])
+    np_ = (C.c_void_p * len(new_ptrs))(*[int(p) or None for p in new_ptrs])
+    fh = None
+    if from_host is not None:
+        fh_arr = np.ascontiguousarray(from_host, dtype=np.uint8)
+        fh = fh_arr.ctypes.data_as(C.POINTER(C.c_uint8))
+    db, hb = C.c_uint64(), C.c_uint64()
+    _check(_lib.kvx_weights_migrate(device, stream or None, num_layers, layer_bytes, len(ob) + 1, _p32(ob),
+                                    op, len(nb) + 1, _p32(nb), np_, host_cache or None, fh,
+                                    C.byref(db), C.byref(hb)))
+    return int(db.value), int(hb.value)

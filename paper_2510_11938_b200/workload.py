@@ -74,6 +74,9 @@ class TransitionSpec:
     new_stages: int
     new_boundaries: List[int]
     new_gpus: List[int]
+    t_ms: float = 0.0
+    load_ready_ms: float = 0.0
+    param_loads: list = field(default_factory=list)  # per server: stages, bws, reference latency
     waves: List[Wave] = field(default_factory=list)
     events: list = field(default_factory=list)  # Wave | Barrier, in engine order
     outcome: str = "open"              # commit | abort
@@ -117,7 +120,9 @@ def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
         if k == "begin":
             t = TransitionSpec(head["name"], r["instance"], r["epoch"], r["old"]["stages"],
                                list(r["old"]["boundaries"]), r["new"]["stages"],
-                               list(r["new"]["boundaries"]), list(r["new_gpus"]))
+                               list(r["new"]["boundaries"]), list(r["new_gpus"]),
+                               r.get("begin_ms", r["t_ms"]),
+                               r["load_ready_ms"], r.get("param_loads", []))
             cur[r["instance"]] = t
             trans.append(t)
         elif k == "wave":
