@@ -162,6 +162,14 @@ typedef struct kvx_commit_result {
  * destination pools with the returned block table are the stage's KV. */
 int kvx_commit(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t* req,
                const int64_t* kv_tokens, kvx_commit_result* out);
+/* The same commit split in two: _async enqueues the check + compaction and
+ * the copy of its results into pinned memory, bumps the epoch (later waves
+ * are stale) and returns without a host sync; _collect waits for it and
+ * fills `out`.  Lets the engine resume routing (engine.cpp:747-756) while
+ * the commit's bookkeeping is still on the device. */
+int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t* req,
+                     const int64_t* kv_tokens);
+int kvx_commit_collect(kvx_transition* t, kvx_commit_result* out);
 /* Drops every destination allocation, invalidates the epoch (++epoch,
  * engine.cpp:769).  The source pools were never modified. */
 int kvx_abort(kvx_transition* t);
@@ -261,6 +269,9 @@ int kvx_ctl_sync_complete(kvx_transition* t, uint64_t epoch, int32_t n, const in
                           int64_t* tokens_out);
 int kvx_ctl_commit(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
                    const int64_t* kv, kvx_commit_result* out);
+int kvx_ctl_commit_async(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
+                         const int64_t* kv);
+int kvx_ctl_commit_collect(kvx_transition* t, kvx_commit_result* out);
 int kvx_ctl_state_get(const kvx_transition* t, kvx_ctl_state* out);
 
 #ifdef __cplusplus

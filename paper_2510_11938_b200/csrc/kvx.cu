@@ -148,7 +148,7 @@ struct kvx_transition {
     std::vector<kvx_pool*> old_pools, new_pools;
     int32_t max_requests = 0, max_blocks = 0, dst_num_blocks = 0;
     uint64_t epoch = 0;
-    enum State { kActive, kCommitted, kAborted } state = kActive;
+    enum State { kActive, kCommitPending, kCommitted, kAborted } state = kActive;
 
     // device state
     int32_t* d_src_bt = nullptr;
@@ -170,6 +170,12 @@ struct kvx_transition {
     int64_t commit_i32_cap = 0;
     size_t bt_bytes = 0, wave_bytes = 0, layers_bytes = 0;
     int64_t* d_commit_out = nullptr;
+    // pinned landing zone of an async commit: [int64 x4 | row_ptr | blocks | free]
+    char* h_commit = nullptr;
+    size_t h_commit_bytes = 0;
+    cudaEvent_t ev_commit = nullptr;
+    int32_t pend_n_live = 0;
+    int64_t pend_nb_live = 0, pend_nb_free = 0;
     // timing
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     bool timing_open = false;
@@ -483,8 +489,11 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     {
         t->seg_cap = (int64_t)(kvx::size_class(sizeof(kvx::Seg) * cells) / sizeof(kvx::Seg));
         t->commit_i32_cap = (int64_t)(d->max_requests + 1) + 2 * (int64_t)cells;
+        t->h_commit_bytes = 32 + sizeof(int32_t) * (size_t)t->commit_i32_cap;
         if (A.dev_alloc((void**)&t->d_segs, sizeof(kvx::Seg) * (size_t)t->seg_cap) != cudaSuccess ||
-            A.dev_alloc((void**)&t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap) != cudaSuccess)
+            A.dev_alloc((void**)&t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap) != cudaSuccess ||
+            A.host_alloc((void**)&t->h_commit, t->h_commit_bytes) != cudaSuccess ||
+            A.event(&t->ev_commit, false) != cudaSuccess)
             return bail(fail(KVX_ENOSPC, "transition scratch allocation failed"));
     }
 
@@ -509,7 +518,9 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
                             cudaMemcpyHostToDevice, t->stream) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "layer table upload"));
     }
-    if (cudaStreamSynchronize(t->stream) != cudaSuccess) return bail(fail(KVX_ECUDA, "init sync"));
+    // No host sync: the uploads above were staged from pageable memory
+    // (copied out before cudaMemcpyAsync returned) and are stream-ordered
+    // before every wave.
     *out = t;
     return KVX_OK;
 }
@@ -627,8 +638,8 @@ int kvx_wait(kvx_transition* t, uint64_t epoch, double* measured_ms) {
     return KVX_OK;
 }
 
-int kvx_commit(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t* req,
-               const int64_t* kv_tokens, kvx_commit_result* out) {
+int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t* req,
+                     const int64_t* kv_tokens) {
     if (!t) return fail(KVX_EINVAL, "transition is null");
     if (epoch != t->epoch) return fail(KVX_ESTALE, "stale epoch");
     if (t->state != kvx_transition::kActive) return fail(KVX_ESTATE, "transition is not active");
@@ -650,17 +661,7 @@ int kvx_commit(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t*
     for (int32_t r = 0; r < t->max_requests; ++r)
         if (!live[(size_t)r]) nb_free += cdiv64(t->synced_hi[(size_t)r], B);
     const int64_t need = (n_live + 1) + nb_live + nb_free;
-    if (need > t->commit_i32_cap) {
-        kvx::Arena& A = kvx::Arena::of(t->device);
-        if (t->d_commit_i32) {
-            KVX_CUDA(cudaStreamSynchronize(t->stream));
-            A.dev_free(t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap);
-        }
-        t->d_commit_i32 = nullptr;
-        const int64_t cap = std::max<int64_t>(need, 1);
-        KVX_CUDA(A.dev_alloc((void**)&t->d_commit_i32, sizeof(int32_t) * (size_t)cap));
-        t->commit_i32_cap = cap;
-    }
+    if (need > t->commit_i32_cap) return fail(KVX_ECUDA, "commit scratch undersized");  // sized at begin
     int32_t* d_row_ptr = t->d_commit_i32;
     int32_t* d_blocks = d_row_ptr + (n_live + 1);
     int32_t* d_free = d_blocks + nb_live;
@@ -682,33 +683,52 @@ int kvx_commit(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t*
         n_live, t->d_dst_bt, t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens,
         d_row_ptr, d_blocks, d_free, t->d_commit_out);
     KVX_LAUNCHED();
-    int64_t res[3] = {0, 0, 0};
-    KVX_CUDA(cudaMemcpyAsync(res, t->d_commit_out, sizeof(res), cudaMemcpyDeviceToHost, t->stream));
-    if (out && out->row_ptr && n_live + 1 > 0)
-        KVX_CUDA(cudaMemcpyAsync(out->row_ptr, d_row_ptr, sizeof(int32_t) * (size_t)(n_live + 1),
-                                 cudaMemcpyDeviceToHost, t->stream));
-    if (out && out->blocks && nb_live > 0) {
-        if (out->blocks_cap < nb_live) return fail(KVX_EINVAL, "blocks_cap too small");
-        KVX_CUDA(cudaMemcpyAsync(out->blocks, d_blocks, sizeof(int32_t) * (size_t)nb_live,
-                                 cudaMemcpyDeviceToHost, t->stream));
-    }
-    if (out && out->free_list && nb_free > 0) {
-        if (out->free_cap < nb_free) return fail(KVX_EINVAL, "free_cap too small");
-        KVX_CUDA(cudaMemcpyAsync(out->free_list, d_free, sizeof(int32_t) * (size_t)nb_free,
-                                 cudaMemcpyDeviceToHost, t->stream));
-    }
-    KVX_CUDA(cudaStreamSynchronize(t->stream));
-    if (res[1] != nb_live || res[2] != nb_free)
+    // results land in pinned memory; kvx_commit_collect reads them
+    KVX_CUDA(cudaMemcpyAsync(t->h_commit, t->d_commit_out, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, t->stream));
+    KVX_CUDA(cudaMemcpyAsync(t->h_commit + 32, t->d_commit_i32, sizeof(int32_t) * (size_t)need,
+                             cudaMemcpyDeviceToHost, t->stream));
+    KVX_CUDA(cudaEventRecord(t->ev_commit, t->stream));
+    t->pend_n_live = n_live;
+    t->pend_nb_live = nb_live;
+    t->pend_nb_free = nb_free;
+    t->state = kvx_transition::kCommitPending;
+    ++t->epoch;  // engine.cpp:752 -- the commit is decided; later waves are stale
+    t->timing_open = false;
+    return KVX_OK;
+}
+
+int kvx_commit_collect(kvx_transition* t, kvx_commit_result* out) {
+    if (!t) return fail(KVX_EINVAL, "transition is null");
+    if (t->state != kvx_transition::kCommitPending) return fail(KVX_ESTATE, "no commit pending");
+    DeviceGuard dg(t->device);
+    KVX_CUDA(cudaEventSynchronize(t->ev_commit));
+    int64_t res[3];
+    std::memcpy(res, t->h_commit, sizeof(res));
+    if (res[1] != t->pend_nb_live || res[2] != t->pend_nb_free)
         return fail(KVX_ECUDA, "device compaction disagrees with the host mirror");
+    const int32_t* h32 = reinterpret_cast<const int32_t*>(t->h_commit + 32);
     if (out) {
+        if (out->blocks && out->blocks_cap < t->pend_nb_live) return fail(KVX_EINVAL, "blocks_cap too small");
+        if (out->free_list && out->free_cap < t->pend_nb_free) return fail(KVX_EINVAL, "free_cap too small");
+        if (out->row_ptr) std::memcpy(out->row_ptr, h32, sizeof(int32_t) * (size_t)(t->pend_n_live + 1));
+        if (out->blocks)
+            std::memcpy(out->blocks, h32 + t->pend_n_live + 1, sizeof(int32_t) * (size_t)t->pend_nb_live);
+        if (out->free_list)
+            std::memcpy(out->free_list, h32 + t->pend_n_live + 1 + t->pend_nb_live,
+                        sizeof(int32_t) * (size_t)t->pend_nb_free);
         out->violations = res[0];
         out->n_blocks = (int32_t)res[1];
         out->n_free = (int32_t)res[2];
     }
     t->state = kvx_transition::kCommitted;
-    ++t->epoch;  // engine.cpp:752
-    t->timing_open = false;
     return KVX_OK;
+}
+
+int kvx_commit(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t* req,
+               const int64_t* kv_tokens, kvx_commit_result* out) {
+    const int rc = kvx_commit_async(t, epoch, n_live, req, kv_tokens);
+    if (rc != KVX_OK) return rc;
+    return kvx_commit_collect(t, out);
 }
 
 int kvx_abort(kvx_transition* t) {
@@ -742,6 +762,8 @@ int kvx_destroy(kvx_transition* t) {
     A.dev_free(t->d_live, (size_t)t->max_requests);
     A.dev_free(t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap);
     A.dev_free(t->d_commit_out, 4 * sizeof(int64_t));
+    A.host_free(t->h_commit, t->h_commit_bytes);
+    A.event_free(t->ev_commit, false);
     for (int s = 0; s < 2; ++s) {
         A.host_free(t->h_wave[s], t->wave_bytes);
         A.event_free(t->h_wave_free[s], false);

@@ -122,8 +122,8 @@ int kvx_ctl_sync_complete(kvx_transition* t, uint64_t epoch, int32_t n, const in
     return KVX_OK;
 }
 
-int kvx_ctl_commit(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
-                   const int64_t* kv, kvx_commit_result* out) {
+int kvx_ctl_commit_async(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
+                         const int64_t* kv) {
     if (!t) return kvx::set_error(KVX_EINVAL, "transition is null");
     if (epoch != kvx::epoch_of(t)) return kvx::set_error(KVX_ESTALE, "stale epoch");  // engine.cpp:693
     CtlState& c = kvx::ctl_of(t);
@@ -133,13 +133,29 @@ int kvx_ctl_commit(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* 
     int64_t host_violations = 0;  // engine.cpp:707-713
     for (int32_t i = 0; i < n; ++i)
         if (c.synced[(size_t)req[i]] != kv[i]) ++host_violations;
+    const int rc = kvx_commit_async(t, epoch, n, req, kv);
+    if (rc != KVX_OK) return rc;
+    c.host_violations = host_violations;
+    return KVX_OK;
+}
+
+int kvx_ctl_commit_collect(kvx_transition* t, kvx_commit_result* out) {
+    if (!t) return kvx::set_error(KVX_EINVAL, "transition is null");
+    CtlState& c = kvx::ctl_of(t);
     kvx_commit_result local{};
     kvx_commit_result* res = out ? out : &local;
-    const int rc = kvx_commit(t, epoch, n, req, kv, res);
+    const int rc = kvx_commit_collect(t, res);
     if (rc != KVX_OK) return rc;
-    if (res->violations != host_violations)
+    if (res->violations != c.host_violations)
         return kvx::set_error(KVX_ECUDA, "device Eq. 10 check disagrees with the control mirror");
     return KVX_OK;
+}
+
+int kvx_ctl_commit(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
+                   const int64_t* kv, kvx_commit_result* out) {
+    const int rc = kvx_ctl_commit_async(t, epoch, n, req, kv);
+    if (rc != KVX_OK) return rc;
+    return kvx_ctl_commit_collect(t, out);
 }
 
 int kvx_ctl_state_get(const kvx_transition* t, kvx_ctl_state* out) {

@@ -26,6 +26,7 @@ struct CtlState {
     double kv_bytes_per_token = 0.0;
     double kv_synced_bytes = 0.0;
     int64_t last_wave_tokens = 0;
+    int64_t host_violations = 0;    // Eq. 10 on the mirror, checked against the device at collect
 
     void init(int32_t max_requests, int32_t max_rounds, double bpt) {
         synced.assign((size_t)max_requests, 0);

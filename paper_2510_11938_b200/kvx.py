@@ -143,6 +143,10 @@ def _load() -> C.CDLL:
         "kvx_ctl_begin": (C.c_int, [VP, I32, P(I32), P(I64), P(I64)]),
         "kvx_ctl_sync_complete": (C.c_int, [VP, U64, I32, P(I32), P(I64), I32, P(I32), P(I64)]),
         "kvx_ctl_commit": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(_CommitResult)]),
+        "kvx_ctl_commit_async": (C.c_int, [VP, U64, I32, P(I32), P(I64)]),
+        "kvx_ctl_commit_collect": (C.c_int, [VP, P(_CommitResult)]),
+        "kvx_commit_async": (C.c_int, [VP, U64, I32, P(I32), P(I64)]),
+        "kvx_commit_collect": (C.c_int, [VP, P(_CommitResult)]),
         "kvx_ctl_state_get": (C.c_int, [VP, P(_CtlState)]),
     }
     for name, (res, args) in sig.items():
@@ -413,12 +417,20 @@ class Transition:
                                           C.byref(tok)))
         return int(act.value), int(tok.value)
 
-    def on_refactor_commit(self, live, epoch: Optional[int] = None) -> CommitResult:
-        """engine.cpp:690-713: final apply, Eq. 10 on the device, compaction."""
+    def on_refactor_commit(self, live, epoch: Optional[int] = None,
+                           wait: bool = True) -> Optional[CommitResult]:
+        """engine.cpp:690-713: final apply, Eq. 10 on the device, compaction.
+        wait=False returns at once (kvx_ctl_commit_async); collect_commit()
+        then returns the result."""
         req, kv = _i32(live[0]), _i64(live[1])
-        res, row_ptr, blocks, free = self._commit_buffers(len(req))
-        _check(_lib.kvx_ctl_commit(self._h, self.epoch if epoch is None else epoch, len(req),
-                                   _p32(req), _p64(kv), C.byref(res)))
+        _check(_lib.kvx_ctl_commit_async(self._h, self.epoch if epoch is None else epoch, len(req),
+                                         _p32(req), _p64(kv)))
+        self._pending_live = len(req)
+        return self.collect_commit() if wait else None
+
+    def collect_commit(self) -> CommitResult:
+        res, row_ptr, blocks, free = self._commit_buffers(self._pending_live)
+        _check(_lib.kvx_ctl_commit_collect(self._h, C.byref(res)))
         return CommitResult(int(res.violations), row_ptr, blocks[:res.n_blocks].copy(),
                             free[:res.n_free].copy())
 
