@@ -106,6 +106,26 @@ int kvx_pool_fill_pattern(kvx_pool* p, uint64_t seed, int32_t first_layer, int32
                           const int32_t* req, const int64_t* tokens, const int32_t* bt,
                           int32_t max_requests, int32_t max_blocks);
 
+/* ---------------------------------------------------------- block manager
+ * Device-resident free list of one pool set (all stages of a plan share block
+ * ids): a stack of free block ids in HBM whose top is mirrored on the host,
+ * so capacity decisions are synchronous and deterministic.  A fresh or reset
+ * manager pops 0, 1, 2, ... (identical to the bump rule); freed blocks are
+ * pushed back and reused LIFO.  A transition given dst_blockmgr pops its new
+ * blocks from it (plan kernel) and, at commit, pushes the blocks of requests
+ * that finished meanwhile; an abort pushes every block it took.  The serving
+ * pipeline uses pop/push for its own appends and releases.  Replaces the
+ * reference's unmodelled KV memory (only parameter bytes are
+ * bound, cluster.cpp:75-96). */
+typedef struct kvx_blockmgr kvx_blockmgr;
+int kvx_bm_create(int32_t device, int32_t capacity, kvx_blockmgr** out);
+int kvx_bm_reset(kvx_blockmgr* bm);
+int kvx_bm_free_count(const kvx_blockmgr* bm, int32_t* n);
+int kvx_bm_pop(kvx_blockmgr* bm, int32_t n, int32_t* ids_out);   /* host out, LIFO order */
+int kvx_bm_push(kvx_blockmgr* bm, int32_t n, const int32_t* ids);
+int kvx_bm_snapshot(const kvx_blockmgr* bm, int32_t* stack_out, int32_t* top_out);
+int kvx_bm_destroy(kvx_blockmgr* bm);
+
 /* ------------------------------------------------------------- transition */
 typedef struct kvx_plan {
     int32_t num_stages;           /* K */
@@ -126,6 +146,7 @@ typedef struct kvx_transition_desc {
     int32_t max_sync_rounds;      /* EngineConfig::max_sync_rounds (engine.hpp:75), kvx_ctl_* */
     double kv_bytes_per_token;    /* accounting of kvx_ctl_* (engine.cpp:644); 0 = from geometry */
     void* stream;                 /* cudaStream_t to run on (not owned); NULL = a private stream */
+    void* dst_blockmgr;           /* kvx_blockmgr* of the new pools; NULL = bump rule from id 0 */
 } kvx_transition_desc;
 
 typedef struct kvx_transition kvx_transition;

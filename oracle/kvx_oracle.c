@@ -187,6 +187,18 @@ static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static int allocate_wave(const kvo_geometry* g, kvo_dst* d, int32_t n, const int32_t* req,
                          const int64_t* lo, const int64_t* hi) {
     const int64_t B = g->block_tokens;
+    /* validate the whole wave first: a rejected wave changes nothing */
+    int64_t need = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t r = req[i];
+        if (r < 0 || r >= d->max_requests || (i > 0 && req[i - 1] >= r)) return -1;
+        if (hi[i] <= lo[i]) continue;
+        if (lo[i] < 0 || lo[i] > d->synced_hi[r]) return -1;
+        if (ceil_div(hi[i], B) > d->max_blocks) return -1;
+        const int64_t add = ceil_div(hi[i], B) - ceil_div(d->synced_hi[r], B);
+        need += add > 0 ? add : 0;
+    }
+    if (d->stack ? need > d->top : d->next_block + need > d->num_blocks) return -1;
     for (int32_t i = 0; i < n; ++i) {
         const int32_t r = req[i];
         if (r < 0 || r >= d->max_requests || (i > 0 && req[i - 1] >= r)) return -1;
@@ -195,8 +207,15 @@ static int allocate_wave(const kvo_geometry* g, kvo_dst* d, int32_t n, const int
         const int64_t b0 = ceil_div(d->synced_hi[r], B), b1 = ceil_div(hi[i], B);
         if (b1 > d->max_blocks) return -1;
         for (int64_t b = b0; b < b1; ++b) {
-            if (d->next_block >= d->num_blocks) return -1;
-            d->bt[(int64_t)r * d->max_blocks + b] = d->next_block++;
+            int32_t id;
+            if (d->stack) {
+                if (d->top <= 0) return -1;
+                id = d->stack[--d->top];
+            } else {
+                if (d->next_block >= d->num_blocks) return -1;
+                id = d->next_block++;
+            }
+            d->bt[(int64_t)r * d->max_blocks + b] = id;
         }
         if (hi[i] > d->synced_hi[r]) d->synced_hi[r] = hi[i];
     }
@@ -320,7 +339,7 @@ int kvo_apply_wave_mt(const kvo_geometry* g, kvo_dst* d, int32_t old_stages, con
     return 0;
 }
 
-int64_t kvo_commit(const kvo_geometry* g, const kvo_dst* d, int32_t n, const int32_t* req,
+int64_t kvo_commit(const kvo_geometry* g, kvo_dst* d, int32_t n, const int32_t* req,
                    const int64_t* kv, int32_t* row_ptr, int32_t* blocks, int32_t* n_blocks,
                    int32_t* free_list, int32_t* n_free) {
     const int64_t B = g->block_tokens;
@@ -344,7 +363,9 @@ int64_t kvo_commit(const kvo_geometry* g, const kvo_dst* d, int32_t n, const int
         if (live[r]) continue;
         const int64_t have = ceil_div(d->synced_hi[r], B);
         for (int64_t b = 0; b < have; ++b) {
-            if (free_list) free_list[nf] = d->bt[(int64_t)r * d->max_blocks + b];
+            const int32_t id = d->bt[(int64_t)r * d->max_blocks + b];
+            if (free_list) free_list[nf] = id;
+            if (d->stack) d->stack[d->top++] = id; /* free-list update (pushed in order) */
             ++nf;
         }
     }
@@ -445,4 +466,21 @@ double kvo_warm_start_ms(int32_t n, const double* stage_bytes, const uint8_t* ca
         total += stage_bytes[k] / (cached[k] ? host_bw : storage_bw);
     }
     return total;
+}
+
+void kvo_bm_init(int32_t* stack, int32_t capacity) {
+    for (int32_t i = 0; i < capacity; ++i) stack[i] = capacity - 1 - i;
+}
+
+void kvo_abort(const kvo_geometry* g, kvo_dst* d) {
+    const int64_t B = g->block_tokens;
+    for (int32_t r = 0; r < d->max_requests; ++r) {
+        const int64_t have = ceil_div(d->synced_hi[r], B);
+        for (int64_t b = 0; b < have; ++b) {
+            if (d->stack) d->stack[d->top++] = d->bt[(int64_t)r * d->max_blocks + b];
+            d->bt[(int64_t)r * d->max_blocks + b] = -1;
+        }
+        d->synced_hi[r] = 0;
+    }
+    d->next_block = 0;
 }

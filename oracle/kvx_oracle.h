@@ -110,7 +110,15 @@ typedef struct kvo_dst {
     int32_t next_block;    /* bump pointer of the deterministic block rule */
     int32_t* bt;           /* [max_requests * max_blocks], -1 = unallocated */
     int64_t* synced_hi;    /* [max_requests] high-water mark of copied tokens */
+    int32_t* stack;        /* optional block-manager free stack (NULL: bump rule) */
+    int32_t top;           /* free ids on the stack; pops take stack[top-1] */
 } kvo_dst;
+
+/* Block manager restated: a fresh stack holds capacity-1 ... 0 (pops yield
+ * 0, 1, 2, ...); commit pushes the free list in order; abort pushes every
+ * allocated block (ascending request, ascending block). */
+void kvo_bm_init(int32_t* stack, int32_t capacity);
+void kvo_abort(const kvo_geometry* g, kvo_dst* d);
 
 /* Executes one wave: destination block allocation (new blocks in ascending
  * request order, ascending logical block, from the bump pointer; entries
@@ -137,7 +145,7 @@ int kvo_apply_wave_mt(const kvo_geometry* g, kvo_dst* d, int32_t old_stages,
  * order: row_ptr[n+1], blocks[]) and the free list of every allocated block
  * of a request that is no longer live (ascending request, ascending block).
  * Returns the violation count; *n_blocks / *n_free receive the sizes. */
-int64_t kvo_commit(const kvo_geometry* g, const kvo_dst* d, int32_t n, const int32_t* req,
+int64_t kvo_commit(const kvo_geometry* g, kvo_dst* d, int32_t n, const int32_t* req,
                    const int64_t* kv, int32_t* row_ptr, int32_t* blocks, int32_t* n_blocks,
                    int32_t* free_list, int32_t* n_free);
 

@@ -41,7 +41,8 @@ class Ctx(C.Structure):
 class Dst(C.Structure):
     _fields_ = [("max_requests", C.c_int32), ("max_blocks", C.c_int32), ("num_blocks", C.c_int32),
                 ("next_block", C.c_int32), ("bt", C.POINTER(C.c_int32)),
-                ("synced_hi", C.POINTER(C.c_int64))]
+                ("synced_hi", C.POINTER(C.c_int64)), ("stack", C.POINTER(C.c_int32)),
+                ("top", C.c_int32)]
 
 
 _lib = None
@@ -71,6 +72,8 @@ def lib() -> C.CDLL:
             "kvo_commit": (I64, [P(Geo), P(Dst), I32, P(I32), P(I64), P(I32), P(I32), P(I32), P(I32), P(I32)]),
             "kvo_verify": (I64, [P(Geo), U64, P(Dst), I32, P(I32), PP, I32, P(I32), P(I64)]),
             "kvo_activation_owner": (I32, [I32, P(I32), I32, P(I32), I32]),
+            "kvo_bm_init": (None, [P(I32), I32]),
+            "kvo_abort": (None, [P(Geo), P(Dst)]),
             "kvo_weights_plan": (None, [I32, U64, I32, P(I32), I32, P(I32), P(I32), P(U64), P(I32), P(U64)]),
             "kvo_warm_start_ms": (C.c_double, [I32, P(C.c_double), P(C.c_uint8), C.c_double, C.c_double]),
             "kvo_handoff_plan": (C.c_int, [I32, P(I32), I32, P(I32), U64, I32, P(I32), P(I32), P(U64),
@@ -166,7 +169,8 @@ class DataPlane:
     """Host pools + destination state of one transition (kvo_* data plane)."""
 
     def __init__(self, g: Geo, old_b, new_b, old_blocks: int, new_blocks: int, max_requests: int,
-                 max_blocks: int, src_bt: np.ndarray, with_pools: bool = True):
+                 max_blocks: int, src_bt: np.ndarray, with_pools: bool = True,
+                 bm: Optional["StackBM"] = None, old_pools=None, new_pools=None):
         self.g = g
         self.ob, self.nb = _i32(list(old_b)), _i32(list(new_b))
         self.old_blocks, self.new_blocks = old_blocks, new_blocks
@@ -175,14 +179,29 @@ class DataPlane:
         bb = 2 * g.block_tokens * g.num_kv_heads * g.head_dim * g.elem_bytes
         self.old_pools = self.new_pools = None
         if with_pools:
-            self.old_pools = [np.zeros(n * old_blocks * bb, np.uint8)
-                              for n in stage_layers(g.num_layers, old_b)]
-            self.new_pools = [np.zeros(n * new_blocks * bb, np.uint8)
-                              for n in stage_layers(g.num_layers, new_b)]
+            self.old_pools = old_pools if old_pools is not None else \
+                [np.zeros(n * old_blocks * bb, np.uint8) for n in stage_layers(g.num_layers, old_b)]
+            self.new_pools = new_pools if new_pools is not None else \
+                [np.zeros(n * new_blocks * bb, np.uint8) for n in stage_layers(g.num_layers, new_b)]
         self.bt = np.full((max_requests, max_blocks), -1, np.int32)
         self.synced_hi = np.zeros(max_requests, np.int64)
+        self.bm = bm  # block-manager restatement (its stack is mutated in place) or None
         self.d = Dst(max_requests, max_blocks, new_blocks, 0, _p(self.bt, C.c_int32),
-                     _p(self.synced_hi, C.c_int64))
+                     _p(self.synced_hi, C.c_int64),
+                     _p(bm.stack, C.c_int32) if bm is not None else None, 0)
+
+    def _enter(self):
+        if self.bm is not None:
+            self.d.top = self.bm.top
+
+    def _leave(self):
+        if self.bm is not None:
+            self.bm.top = int(self.d.top)
+
+    def abort(self):
+        self._enter()
+        lib().kvo_abort(C.byref(self.g), C.byref(self.d))
+        self._leave()
 
     def fill_source(self, seed: int, req, tokens):
         req, tokens = _i32(req), _i64(tokens)
@@ -196,9 +215,13 @@ class DataPlane:
                 _pp(self.old_pools), self.old_blocks, _p(self.src_bt, C.c_int32), len(self.nb) + 1,
                 _p(self.nb, C.c_int32), _pp(self.new_pools), len(req), _p(req, C.c_int32),
                 _p(lo, C.c_int64), _p(hi, C.c_int64))
-        if threads > 0:
-            return lib().kvo_apply_wave_mt(*args, threads)
-        return lib().kvo_apply_wave(*args)
+        self._enter()
+        try:
+            if threads > 0:
+                return lib().kvo_apply_wave_mt(*args, threads)
+            return lib().kvo_apply_wave(*args)
+        finally:
+            self._leave()
 
     def commit(self, req, kv):
         req, kv = _i32(req), _i64(kv)
@@ -207,9 +230,11 @@ class DataPlane:
         blocks = np.zeros(max(cap, 1), np.int32)
         free = np.zeros(max(cap, 1), np.int32)
         nb, nf = C.c_int32(), C.c_int32()
+        self._enter()
         v = lib().kvo_commit(C.byref(self.g), C.byref(self.d), len(req), _p(req, C.c_int32),
                              _p(kv, C.c_int64), _p(row_ptr, C.c_int32), _p(blocks, C.c_int32),
                              C.byref(nb), _p(free, C.c_int32), C.byref(nf))
+        self._leave()
         return int(v), row_ptr, blocks[:nb.value].copy(), free[:nf.value].copy()
 
     def verify(self, seed: int, req, kv) -> int:
@@ -254,3 +279,31 @@ def warm_start_ms(stage_bytes, cached, host_bw, storage_bw) -> float:
     b = np.ascontiguousarray(stage_bytes, dtype=np.float64)
     c = np.ascontiguousarray(cached, dtype=np.uint8)
     return float(lib().kvo_warm_start_ms(len(b), _p(b, C.c_double), _p(c, C.c_uint8), host_bw, storage_bw))
+
+
+class StackBM:
+    """Host restatement of the device block manager: a numpy free stack and
+    its top (kvo_bm_init order: pops yield 0, 1, 2, ...)."""
+
+    def __init__(self, capacity: int):
+        self.stack = np.zeros(capacity, np.int32)
+        self.capacity = capacity
+        self.reset()
+
+    def reset(self):
+        lib().kvo_bm_init(_p(self.stack, C.c_int32), self.capacity)
+        self.top = self.capacity
+
+    def pop(self, n: int) -> np.ndarray:
+        assert n <= self.top
+        out = self.stack[self.top - n:self.top][::-1].copy()
+        self.top -= n
+        return out
+
+    def push(self, ids) -> None:
+        ids = np.asarray(ids, np.int32)
+        self.stack[self.top:self.top + len(ids)] = ids
+        self.top += len(ids)
+
+    def snapshot(self) -> np.ndarray:
+        return self.stack[:self.top].copy()

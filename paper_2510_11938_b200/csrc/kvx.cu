@@ -133,6 +133,15 @@ struct kvx_pool {
     int32_t num_blocks = 0;
 };
 
+// Device-resident block manager: a free-id stack on the GPU, its top mirrored
+// on the host so every capacity decision is synchronous and deterministic.
+struct kvx_blockmgr {
+    int32_t device = -1;
+    int32_t capacity = 0;
+    int32_t top = 0;          // free blocks (host mirror of the device stack top)
+    int32_t* d_stack = nullptr;
+};
+
 struct kvx_transition {
     kvx_geometry g{};
     int32_t device = -1;
@@ -147,6 +156,7 @@ struct kvx_transition {
     std::vector<int32_t> old_b, new_b;
     std::vector<kvx_pool*> old_pools, new_pools;
     int32_t max_requests = 0, max_blocks = 0, dst_num_blocks = 0;
+    kvx_blockmgr* bm = nullptr;  // destination block manager (NULL: bump rule)
     uint64_t epoch = 0;
     enum State { kActive, kCommitPending, kCommitted, kAborted } state = kActive;
 
@@ -395,6 +405,11 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
             p->g.elem_bytes != g.elem_bytes || p->g.block_tokens != g.block_tokens)
             return fail(KVX_EINVAL, "old pool geometry mismatch");
     }
+    if (d->dst_blockmgr) {
+        const auto* bm = static_cast<const kvx_blockmgr*>(d->dst_blockmgr);
+        if (bm->device != d->device) return fail(KVX_EINVAL, "block manager lives on another device");
+        if (bm->capacity > d->dst_num_blocks) return fail(KVX_EINVAL, "block manager larger than the new pools");
+    }
     // Validate the source table against the pools it will be read through.
     const size_t cells = (size_t)d->max_requests * (size_t)d->max_blocks;
     int32_t min_old_blocks = INT32_MAX;
@@ -417,6 +432,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     t->max_requests = d->max_requests;
     t->max_blocks = d->max_blocks;
     t->dst_num_blocks = d->dst_num_blocks;
+    t->bm = static_cast<kvx_blockmgr*>(d->dst_blockmgr);
     t->epoch = d->epoch;
     t->synced_hi.assign((size_t)d->max_requests, 0);
     t->ctl.init(d->max_requests, d->max_sync_rounds,
@@ -547,7 +563,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         nseg += cdiv64(hi[i], B) - lo[i] / B;
         tokens += hi[i] - lo[i];
     }
-    if ((int64_t)t->alloc + new_blocks > t->dst_num_blocks)
+    if (t->bm ? new_blocks > t->bm->top : (int64_t)t->alloc + new_blocks > t->dst_num_blocks)
         return fail(KVX_ENOSPC, "destination pools full");
     DeviceGuard dg(t->device);
     if (n == 0 || nseg == 0) return KVX_OK;
@@ -586,7 +602,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     const int64_t* d_hi = reinterpret_cast<const int64_t*>(t->d_wave + off_hi);
     kvx::kvx_plan_kernel<<<1, kvx::kPlanThreads, 0, t->stream>>>(
         d_req, d_lo, d_hi, n, t->d_src_bt, t->d_dst_bt, t->d_synced_hi, t->max_blocks,
-        t->g.block_tokens, t->alloc, t->d_segs);
+        t->g.block_tokens, t->bm ? t->bm->top : t->alloc, t->bm ? t->bm->d_stack : nullptr, t->d_segs);
     KVX_LAUNCHED();
     if (t->n_local_layers > 0) {
         const int64_t units = nseg * t->n_local_layers;
@@ -619,6 +635,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     for (int32_t i = 0; i < n; ++i)
         if (hi[i] > t->synced_hi[(size_t)req[i]]) t->synced_hi[(size_t)req[i]] = hi[i];
     t->alloc += (int32_t)new_blocks;
+    if (t->bm) t->bm->top -= (int32_t)new_blocks;
     t->bytes_moved += (uint64_t)tokens * 2ull * token_bytes(t->g) * (uint64_t)t->n_local_layers;
     t->bytes_all_layers += (uint64_t)tokens * 2ull * token_bytes(t->g) * (uint64_t)t->g.num_layers;
     return KVX_OK;
@@ -687,6 +704,11 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
     KVX_CUDA(cudaMemcpyAsync(t->h_commit, t->d_commit_out, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, t->stream));
     KVX_CUDA(cudaMemcpyAsync(t->h_commit + 32, t->d_commit_i32, sizeof(int32_t) * (size_t)need,
                              cudaMemcpyDeviceToHost, t->stream));
+    if (t->bm && nb_free > 0) {  // free-list update: dead rows' blocks back on the stack
+        KVX_CUDA(cudaMemcpyAsync(t->bm->d_stack + t->bm->top, d_free, sizeof(int32_t) * (size_t)nb_free,
+                                 cudaMemcpyDeviceToDevice, t->stream));
+        t->bm->top += (int32_t)nb_free;
+    }
     KVX_CUDA(cudaEventRecord(t->ev_commit, t->stream));
     t->pend_n_live = n_live;
     t->pend_nb_live = nb_live;
@@ -736,6 +758,23 @@ int kvx_abort(kvx_transition* t) {
     if (t->state != kvx_transition::kActive) return fail(KVX_ESTATE, "transition is not active");
     DeviceGuard dg(t->device);
     KVX_CUDA(cudaStreamSynchronize(t->stream));  // in-flight waves land in pools we now drop
+    if (t->bm) {  // every destination block goes back on the free stack
+        const int64_t B = t->g.block_tokens;
+        int64_t nb_all = 0;
+        for (int32_t r = 0; r < t->max_requests; ++r) nb_all += cdiv64(t->synced_hi[(size_t)r], B);
+        if (nb_all > 0) {
+            int32_t* d_row_ptr = t->d_commit_i32;
+            int32_t* d_free = d_row_ptr + 1;
+            kvx::kvx_commit_kernel<<<1, kvx::kCommitThreads, 0, t->stream>>>(
+                reinterpret_cast<const int32_t*>(t->d_wave), reinterpret_cast<const int64_t*>(t->d_wave), 0,
+                t->d_dst_bt, t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens,
+                d_row_ptr, d_free, d_free, t->d_commit_out);
+            KVX_LAUNCHED();
+            KVX_CUDA(cudaMemcpyAsync(t->bm->d_stack + t->bm->top, d_free, sizeof(int32_t) * (size_t)nb_all,
+                                     cudaMemcpyDeviceToDevice, t->stream));
+            t->bm->top += (int32_t)nb_all;
+        }
+    }
     t->state = kvx_transition::kAborted;
     ++t->epoch;  // engine.cpp:769
     t->alloc = 0;
@@ -939,6 +978,86 @@ int kvx_weights_migrate(int32_t device, void* stream, int32_t num_layers, uint64
         static_cast<const kvx::Piece*>(d), (int64_t)pieces.size());
     KVX_LAUNCHED();
     KVX_CUDA(cudaLaunchHostFunc(st, release_pieces, new PieceRelease{device, d, h, bytes}));
+    return KVX_OK;
+}
+
+// ------------------------------------------------------------ block manager
+int kvx_bm_create(int32_t device, int32_t capacity, kvx_blockmgr** out) {
+    if (!out || capacity < 1) return fail(KVX_EINVAL, "bad block manager arguments");
+    *out = nullptr;
+    DeviceGuard dg(device);
+    if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed");
+    auto* bm = new kvx_blockmgr;
+    bm->device = device;
+    bm->capacity = capacity;
+    if (cudaMalloc(&bm->d_stack, sizeof(int32_t) * (size_t)capacity) != cudaSuccess) {
+        delete bm;
+        cudaGetLastError();
+        return fail(KVX_ENOSPC, "block manager allocation failed");
+    }
+    *out = bm;
+    return kvx_bm_reset(bm);
+}
+
+int kvx_bm_reset(kvx_blockmgr* bm) {
+    if (!bm) return fail(KVX_EINVAL, "block manager is null");
+    DeviceGuard dg(bm->device);
+    kvx::kvx_bm_init_kernel<<<(unsigned)std::min<int64_t>(1024, (bm->capacity + 255) / 256), 256>>>(
+        bm->d_stack, bm->capacity);
+    KVX_LAUNCHED();
+    KVX_CUDA(cudaDeviceSynchronize());
+    bm->top = bm->capacity;
+    return KVX_OK;
+}
+
+int kvx_bm_free_count(const kvx_blockmgr* bm, int32_t* n) {
+    if (!bm || !n) return fail(KVX_EINVAL, "null argument");
+    *n = bm->top;
+    return KVX_OK;
+}
+
+int kvx_bm_pop(kvx_blockmgr* bm, int32_t n, int32_t* ids_out) {
+    if (!bm || n < 0 || (n > 0 && !ids_out)) return fail(KVX_EINVAL, "bad pop arguments");
+    if (n > bm->top) return fail(KVX_ENOSPC, "block manager exhausted");
+    if (n == 0) return KVX_OK;
+    DeviceGuard dg(bm->device);
+    std::vector<int32_t> tmp((size_t)n);
+    KVX_CUDA(cudaDeviceSynchronize());  // stack pushes queued on transition streams have landed
+    KVX_CUDA(cudaMemcpy(tmp.data(), bm->d_stack + (bm->top - n), sizeof(int32_t) * (size_t)n,
+                        cudaMemcpyDeviceToHost));
+    for (int32_t i = 0; i < n; ++i) ids_out[i] = tmp[(size_t)(n - 1 - i)];  // LIFO order
+    bm->top -= n;
+    return KVX_OK;
+}
+
+int kvx_bm_push(kvx_blockmgr* bm, int32_t n, const int32_t* ids) {
+    if (!bm || n < 0 || (n > 0 && !ids)) return fail(KVX_EINVAL, "bad push arguments");
+    if (bm->top + n > bm->capacity) return fail(KVX_EINVAL, "push beyond capacity (double free?)");
+    for (int32_t i = 0; i < n; ++i)
+        if (ids[i] < 0 || ids[i] >= bm->capacity) return fail(KVX_EINVAL, "block id out of range");
+    if (n == 0) return KVX_OK;
+    DeviceGuard dg(bm->device);
+    KVX_CUDA(cudaDeviceSynchronize());
+    KVX_CUDA(cudaMemcpy(bm->d_stack + bm->top, ids, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice));
+    bm->top += n;
+    return KVX_OK;
+}
+
+int kvx_bm_snapshot(const kvx_blockmgr* bm, int32_t* stack_out, int32_t* top_out) {
+    if (!bm) return fail(KVX_EINVAL, "block manager is null");
+    DeviceGuard dg(bm->device);
+    KVX_CUDA(cudaDeviceSynchronize());
+    if (stack_out && bm->top > 0)
+        KVX_CUDA(cudaMemcpy(stack_out, bm->d_stack, sizeof(int32_t) * (size_t)bm->top, cudaMemcpyDeviceToHost));
+    if (top_out) *top_out = bm->top;
+    return KVX_OK;
+}
+
+int kvx_bm_destroy(kvx_blockmgr* bm) {
+    if (!bm) return KVX_OK;
+    DeviceGuard dg(bm->device);
+    cudaFree(bm->d_stack);
+    delete bm;
     return KVX_OK;
 }
 

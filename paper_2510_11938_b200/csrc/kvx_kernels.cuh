@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
 kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
                 const int64_t* __restrict__ hi, int32_t n, const int32_t* __restrict__ src_bt,
                 int32_t* __restrict__ dst_bt, int64_t* __restrict__ synced_hi, int32_t max_blocks,
-                int32_t block_tokens, int32_t alloc_base, Seg* __restrict__ segs) {
+                int32_t block_tokens, int32_t alloc_base, const int32_t* __restrict__ pop_stack,
+                Seg* __restrict__ segs) {
     const int64_t B = block_tokens;
     int2 carry = make_int2(0, 0);
     for (int32_t base = 0; base < n; base += kPlanThreads) {
@@ -142,7 +143,12 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
             int32_t* row = dst_bt + (int64_t)r * max_blocks;
             const int32_t* srow = src_bt + (int64_t)r * max_blocks;
             const int64_t have = cdiv(s, B);
-            for (int32_t k = 0; k < cnt.x; ++k) row[have + k] = alloc_base + carry.x + off.x + k;
+            // bump pointer, or pops off the block manager's free stack
+            // (alloc_base = its top): the j-th pop of the wave is stack[top-1-j]
+            for (int32_t k = 0; k < cnt.x; ++k) {
+                const int32_t j = carry.x + off.x + k;
+                row[have + k] = pop_stack ? pop_stack[alloc_base - 1 - j] : alloc_base + j;
+            }
             if (h > s) synced_hi[r] = h;
             const int64_t b0 = l / B;
             Seg* out = segs + carry.y + off.y;
@@ -156,6 +162,12 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
         carry.x += tot.x;
         carry.y += tot.y;
     }
+}
+
+// Block-manager helper: stack[i] = capacity - 1 - i (pops yield 0, 1, 2, ...).
+__global__ void kvx_bm_init_kernel(int32_t* __restrict__ stack, int32_t capacity) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < capacity; i += gridDim.x * blockDim.x)
+        stack[i] = capacity - 1 - i;
 }
 
 // ------------------------------------------------------------ LSU mover

@@ -78,7 +78,8 @@ class _Desc(C.Structure):
                 ("device", C.c_int32), ("max_requests", C.c_int32), ("max_blocks", C.c_int32),
                 ("dst_num_blocks", C.c_int32), ("src_block_table", C.POINTER(C.c_int32)),
                 ("epoch", C.c_uint64), ("max_sync_rounds", C.c_int32),
-                ("kv_bytes_per_token", C.c_double), ("stream", C.c_void_p)]
+                ("kv_bytes_per_token", C.c_double), ("stream", C.c_void_p),
+                ("dst_blockmgr", C.c_void_p)]
 
 
 class _CommitResult(C.Structure):
@@ -125,6 +126,13 @@ def _load() -> C.CDLL:
         "kvx_pool_read": (C.c_int, [VP, U64, U64, VP]),
         "kvx_pool_write": (C.c_int, [VP, U64, U64, VP]),
         "kvx_pool_fill_pattern": (C.c_int, [VP, U64, I32, I32, P(I32), P(I64), P(I32), I32, I32]),
+        "kvx_bm_create": (C.c_int, [I32, I32, P(VP)]),
+        "kvx_bm_reset": (C.c_int, [VP]),
+        "kvx_bm_free_count": (C.c_int, [VP, P(I32)]),
+        "kvx_bm_pop": (C.c_int, [VP, I32, P(I32)]),
+        "kvx_bm_push": (C.c_int, [VP, I32, P(I32)]),
+        "kvx_bm_snapshot": (C.c_int, [VP, P(I32), P(I32)]),
+        "kvx_bm_destroy": (C.c_int, [VP]),
         "kvx_begin": (C.c_int, [P(_Desc), P(VP)]),
         "kvx_wave": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(I64)]),
         "kvx_wait": (C.c_int, [VP, U64, P(C.c_double)]),
@@ -275,6 +283,53 @@ class Pool:
             pass
 
 
+class BlockManager:
+    """Device-resident free list of one pool set (kvx_bm_*)."""
+
+    def __init__(self, device: int, capacity: int):
+        h = C.c_void_p()
+        _check(_lib.kvx_bm_create(device, capacity, C.byref(h)))
+        self._h, self.capacity = h, capacity
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def free_count(self) -> int:
+        n = C.c_int32()
+        _check(_lib.kvx_bm_free_count(self._h, C.byref(n)))
+        return int(n.value)
+
+    def reset(self) -> None:
+        _check(_lib.kvx_bm_reset(self._h))
+
+    def pop(self, n: int) -> np.ndarray:
+        out = np.zeros(max(n, 1), np.int32)
+        _check(_lib.kvx_bm_pop(self._h, n, _p32(out)))
+        return out[:n]
+
+    def push(self, ids) -> None:
+        ids = _i32(ids)
+        _check(_lib.kvx_bm_push(self._h, len(ids), _p32(ids)))
+
+    def snapshot(self) -> np.ndarray:
+        out = np.zeros(self.capacity, np.int32)
+        top = C.c_int32()
+        _check(_lib.kvx_bm_snapshot(self._h, _p32(out), C.byref(top)))
+        return out[:top.value].copy()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _check(_lib.kvx_bm_destroy(self._h))
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 @dataclass
 class CommitResult:
     violations: int
@@ -291,7 +346,8 @@ class Transition:
                  new_boundaries: Sequence[int], new_pools: Sequence[Pool], device: int,
                  max_requests: int, max_blocks: int, dst_num_blocks: int,
                  src_block_table: np.ndarray, epoch: int = 1, max_sync_rounds: int = 8,
-                 kv_bytes_per_token: float = 0.0, stream: int = 0):
+                 kv_bytes_per_token: float = 0.0, stream: int = 0,
+                 dst_blockmgr: Optional["BlockManager"] = None):
         self.geom = geom
         self.max_requests, self.max_blocks = max_requests, max_blocks
         self._ob = _i32(list(old_boundaries))
@@ -314,6 +370,8 @@ class Transition:
         d.max_sync_rounds = max_sync_rounds
         d.kv_bytes_per_token = kv_bytes_per_token
         d.stream = stream or None
+        d.dst_blockmgr = dst_blockmgr.handle.value if dst_blockmgr is not None else None
+        self._bm = dst_blockmgr
         h = C.c_void_p()
         _check(_lib.kvx_begin(C.byref(d), C.byref(h)))
         self._h = h
