@@ -60,6 +60,22 @@ SEED = 0xB200
 METRIC = "KV-refactor GB/s (% of HBM/NVLink roofline); refactor stall ms at 1/2/4/8 B200"
 
 
+def ncu_traffic(cfg: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the wave-0 mover launch
+    from the newest committed ncu capture of this config (scripts/run_ncu.sh
+    -> profiles/*_traffic_<cfg>.csv), or None."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*bulk_traffic_{cfg}.csv")))
+    if not files:
+        return None, None
+    total = 0.0
+    for row in csv.reader(open(files[-1])):
+        if len(row) > 14 and row[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += float(row[14].replace(",", ""))
+    return (total or None), os.path.relpath(files[-1], ROOT)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -186,6 +202,68 @@ def run_step(tr, t, stall_ev=None, wait=True):
     return res
 
 
+# ------------------------------------------------------------ NCCL baseline
+def nccl_baseline(kvx, torch, dist, plan, g, old_pools, old_dev, new_dev, rank, world, dev, stream,
+                  reps=5):
+    """Wave 0 the library-call way: gather every local-source layer into a
+    local copy of the destination layout (the same kvx mover, local HBM
+    only), then ship each remote layer region with NCCL send/recv (grouped,
+    batch_isend_irecv) straight into the owner's pool.  Returns device ms
+    (gather, nccl, total), max over ranks, or None if nothing crosses GPUs."""
+    t, L = plan.t, plan.L
+    ob, nb = t.old_boundaries, t.new_boundaries
+    cross = [l for l in range(L) if old_dev[S.stage_of(ob, l)] != new_dev[S.stage_of(nb, l)]]
+    if not cross:
+        return None
+    bb = g.block_bytes
+    ranges = W.stage_ranges(L, nb)
+    bufs, pools = [], []
+    for j, (b, e) in enumerate(ranges):
+        n = (e - b) * plan.dst_blocks * bb
+        buf = torch.empty(n, dtype=torch.uint8, device=dev)
+        bufs.append(buf)
+        pools.append(kvx.Pool.wrap(dev, buf.data_ptr(), n, g, e - b, plan.dst_blocks))
+    w0 = t.waves[0]
+    alloc0 = int(((w0.hi + 15) // 16).sum())  # fresh pools: wave 0 fills blocks [0, alloc0) per layer
+    ops_spec = []
+    for l in cross:
+        src, dst = old_dev[S.stage_of(ob, l)], new_dev[S.stage_of(nb, l)]
+        j = S.stage_of(nb, l)
+        off = (l - ranges[j][0]) * plan.dst_blocks * bb
+        if rank == src:
+            ops_spec.append(("send", j, off, dst))
+        elif rank == dst:
+            ops_spec.append(("recv", j, off, src))
+    sp = stream.cuda_stream
+    res = []
+    for rep in range(reps + 1):
+        tr = kvx.Transition(g, ob, old_pools, nb, pools, dev, plan.N, plan.max_blocks, plan.dst_blocks,
+                            plan.src_bt, epoch=t.epoch, stream=sp)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            tr.wave(w0.req, w0.lo, w0.hi)
+            e1.record(stream)
+            ops = [dist.P2POp(dist.isend if k == "send" else dist.irecv,
+                              bufs[j][off:off + alloc0 * bb], peer) for k, j, off, peer in ops_spec]
+            for r in dist.batch_isend_irecv(ops) if ops else []:
+                r.wait()
+            e2.record(stream)
+        torch.cuda.synchronize(dev)
+        tr.close()
+        if rep:
+            res.append((e0.elapsed_time(e1), e1.elapsed_time(e2), e0.elapsed_time(e2)))
+    med = [statistics.median(x[i] for x in res) for i in range(3)]
+    tm = torch.tensor(med, dtype=torch.float64, device=dev)
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    for p in pools:
+        p.close()
+    del bufs
+    return [float(x) for x in tm.tolist()]
+
+
 # -------------------------------------------------------------- CPU baseline
 def cpu_sample_run(plan: Plan, steps: int, warmup: int, threads: int, target_bytes: float = 1.0e9):
     """The oracle executor (oracle/kvx_oracle.c, pthreads) on a bounded sample
@@ -269,6 +347,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-weights", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -478,6 +557,19 @@ def main():
                                "reference models this as host/storage loads (load_ready_ms)"}
             del wold, wnew
 
+    # ---- NCCL baseline of the cross-GPU path (N > 1, when bytes cross GPUs)
+    nccl = None
+    if world > 1 and not args.no_nccl:
+        nb_ms = nccl_baseline(kvx, torch, dist, plan, g, old_pools, old_dev, new_dev, rank, world, dev,
+                              stream)
+        if nb_ms is not None:
+            nccl = {"gather_ms": round(nb_ms[0], 4), "nccl_ms": round(nb_ms[1], 4),
+                    "total_ms": round(nb_ms[2], 4), "fused_p2p_ms": round(w0_avg, 4),
+                    "fused_speedup": round(nb_ms[2] / w0_avg, 3),
+                    "note": "wave 0: local gather into a copy of the destination layout + grouped "
+                            "NCCL send/recv of each remote layer region, vs the fused gather+push "
+                            "kernel over NVLink P2P (max over ranks)"}
+
     # ---- roofline of the dominant kernel
     peak, peak_kind = peaks()
     layer_bytes = plan.wave0_tokens * 2 * plan.token_bytes  # K+V bytes per layer in wave 0
@@ -488,8 +580,9 @@ def main():
                  max(i / (nvl_peak * 1e9) for i in inn))
     if n_gpus == 1:
         achieved = w0_bytes / (w0_avg * 1e-3) / 1e9
+        traffic, traffic_src = ncu_traffic(args.config)
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "kvx_move_kernel (wave 0)", "bytes_per_launch": w0_bytes,
                 "launch_ms": round(w0_avg, 4), "peak_source": peak_kind}
     else:
@@ -534,7 +627,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                 "ms_per_step": round(e2e_s * 1e3 / e2e_steps, 4)},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "handoff": handoff,
-        "weights": weights,
+        "weights": weights, "nccl_baseline": nccl,
         "move_kernel_ms_per_step": round(all_move_ms / K, 4), "move_ms_by_wave": wave_ms,
         "mover": os.environ.get("KVX_MOVE_IMPL", "bulk") + ":" + os.environ.get("KVX_BULK_CFG", "0"),
     }

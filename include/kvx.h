@@ -85,6 +85,11 @@ typedef struct kvx_pool kvx_pool;
 
 int kvx_pool_create(int32_t device, const kvx_geometry* g, int32_t num_layers,
                     int32_t num_blocks, kvx_pool** out);
+/* A pool over caller-owned device memory (e.g. the serving engine's KV cache
+ * tensor): `ptr` must hold num_layers * num_blocks * 2 * block_tokens *
+ * token_bytes bytes on `device`, 16-byte aligned.  Not freed by destroy. */
+int kvx_pool_wrap(int32_t device, void* ptr, uint64_t bytes, const kvx_geometry* g,
+                  int32_t num_layers, int32_t num_blocks, kvx_pool** out);
 /* CUDA IPC handle of a local pool, for a peer process on the same node. */
 int kvx_pool_export(const kvx_pool* p, uint8_t handle[KVX_IPC_HANDLE_BYTES]);
 /* Maps a peer's pool into `device`'s address space (NVLink P2P). */

@@ -126,6 +126,7 @@ constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]
 struct kvx_pool {
     int32_t device = -1;
     bool imported = false;
+    bool wrapped = false;  // caller-owned memory
     char* base = nullptr;
     uint64_t bytes = 0;
     kvx_geometry g{};
@@ -254,6 +255,28 @@ int kvx_pool_create(int32_t device, const kvx_geometry* g, int32_t num_layers, i
     return KVX_OK;
 }
 
+int kvx_pool_wrap(int32_t device, void* ptr, uint64_t bytes, const kvx_geometry* g, int32_t num_layers,
+                  int32_t num_blocks, kvx_pool** out) {
+    std::string why;
+    if (!out) return fail(KVX_EINVAL, "out is null");
+    *out = nullptr;
+    if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
+    if (!ptr || (reinterpret_cast<uintptr_t>(ptr) & 15)) return fail(KVX_EINVAL, "ptr must be 16-byte aligned");
+    if (num_layers < 1 || num_blocks < 1) return fail(KVX_EINVAL, "num_layers/num_blocks must be >= 1");
+    const uint64_t need = (uint64_t)num_layers * (uint64_t)num_blocks * block_bytes(*g);
+    if (bytes < need) return fail(KVX_EINVAL, "wrapped buffer smaller than the pool");
+    auto* p = new kvx_pool;
+    p->device = device;
+    p->wrapped = true;
+    p->base = static_cast<char*>(ptr);
+    p->g = *g;
+    p->num_layers = num_layers;
+    p->num_blocks = num_blocks;
+    p->bytes = need;
+    *out = p;
+    return KVX_OK;
+}
+
 int kvx_pool_export(const kvx_pool* p, uint8_t handle[KVX_IPC_HANDLE_BYTES]) {
     if (!p || !handle || p->imported) return fail(KVX_EINVAL, "export needs a local pool");
     static_assert(sizeof(cudaIpcMemHandle_t) == KVX_IPC_HANDLE_BYTES, "ipc handle size");
@@ -300,7 +323,7 @@ int kvx_pool_info(const kvx_pool* p, void** dptr, uint64_t* bytes, int32_t* devi
 int kvx_pool_destroy(kvx_pool* p) {
     if (!p) return KVX_OK;
     DeviceGuard dg(p->device);
-    cudaError_t e = p->imported ? cudaIpcCloseMemHandle(p->base) : cudaFree(p->base);
+    cudaError_t e = p->wrapped ? cudaSuccess : p->imported ? cudaIpcCloseMemHandle(p->base) : cudaFree(p->base);
     delete p;
     if (e != cudaSuccess) return fail(KVX_ECUDA, std::string("pool free: ") + cudaGetErrorString(e));
     return KVX_OK;
@@ -888,12 +911,9 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
     KVX_CUDA(cudaEventRecord(t->pieces_free, t->stream));
     constexpr int kStages = 4;
     constexpr uint32_t kChunk = 32768;
-    static bool attr_set = false;
-    if (!attr_set) {
-        KVX_CUDA(cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kStages, kChunk>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * (int)kChunk));
-        attr_set = true;
-    }
+    // per-device attribute: set on every call (cheap; the handle's device may differ)
+    KVX_CUDA(cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kStages, kChunk>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * (int)kChunk));
     const unsigned grid = (unsigned)std::min<int64_t>(2 * (int64_t)t->num_sms, (int64_t)pieces.size());
     kvx::kvx_copy_list_kernel<kStages, kChunk><<<grid, kvx::kBulkThreads, kStages * kChunk, t->stream>>>(
         t->d_pieces, (int64_t)pieces.size());

@@ -118,6 +118,7 @@ def _load() -> C.CDLL:
         "kvx_launch_count": (U64, []),
         "kvx_device_count": (C.c_int, [P(I32)]),
         "kvx_pool_create": (C.c_int, [I32, P(Geometry), I32, I32, P(VP)]),
+        "kvx_pool_wrap": (C.c_int, [I32, VP, U64, P(Geometry), I32, I32, P(VP)]),
         "kvx_pool_export": (C.c_int, [VP, C.c_char_p]),
         "kvx_pool_import": (C.c_int, [I32, C.c_char_p, P(Geometry), I32, I32, P(VP)]),
         "kvx_pool_info": (C.c_int, [VP, P(VP), P(U64), P(I32), P(I32)]),
@@ -238,6 +239,14 @@ class Pool:
         _check(_lib.kvx_pool_import(device, handle, C.byref(geom), num_layers, num_blocks,
                                     C.byref(h)))
         return cls(device, geom, num_layers, num_blocks, _handle=h.value, imported=True)
+
+    @classmethod
+    def wrap(cls, device: int, ptr: int, nbytes: int, geom: Geometry, num_layers: int,
+             num_blocks: int) -> "Pool":
+        """A pool over caller-owned device memory (e.g. a torch tensor's data_ptr())."""
+        h = C.c_void_p()
+        _check(_lib.kvx_pool_wrap(device, ptr, nbytes, C.byref(geom), num_layers, num_blocks, C.byref(h)))
+        return cls(device, geom, num_layers, num_blocks, _handle=h.value)
 
     def export_ipc(self) -> bytes:
         buf = C.create_string_buffer(IPC_HANDLE_BYTES)
