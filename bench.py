@@ -335,6 +335,103 @@ def run_reference(args):
     return 0
 
 
+# ---------------------------------------------------- repeated refactors (C5)
+def run_chain(args):
+    """BASELINE config 5: the reference's bursty, mixed-length trace
+    (tests/golden/bursty_repeated.jsonl: gamma arrivals CV=4) drives two
+    consecutive inflight refactors, 8->4 then 4->8, at the Llama-2-13B shape.
+    The second reads the first one's destination pools through its block
+    table; destination blocks come from device block managers; the serving
+    pipeline's decode appends between the two are emulated (untimed).  One
+    step = both transitions; value = their reference-accounted KV bytes / the
+    transitions' device time."""
+    import torch
+    from paper_2510_11938_b200 import kvx
+    dev = 0
+    torch.cuda.set_device(dev)
+    scn = W.load_golden("bursty_repeated")
+    t1, t2 = [t for t in scn.transitions if t.outcome == "commit"][:2]
+    N = scn.num_requests
+    L, H, D = W.SHAPES["llama2-13b"]
+    g = kvx.geometry(L, H, D)
+    tok1, tok2 = t1.max_tokens(N), t2.max_tokens(N)
+    max_blocks = int((max(tok1.max(), tok2.max()) + 15) // 16)
+    need2 = int(((tok2 + 15) // 16).sum())
+    src_bt1, capA = W.fragmented_block_table(tok1, max_blocks, 16, seed=7)
+    capA = max(capA, need2 + 16)
+    capB = int(((np.maximum(tok1, tok2) + 15) // 16).sum()) + 16
+    live1 = np.nonzero(tok1)[0].astype(np.int32)
+    poolsA = [kvx.Pool(dev, g, e - b, capA) for b, e in W.stage_ranges(L, t1.old_boundaries)]
+    poolsB = [kvx.Pool(dev, g, e - b, capB) for b, e in W.stage_ranges(L, t1.new_boundaries)]
+    bmA, bmB = kvx.BlockManager(dev, capA), kvx.BlockManager(dev, capB)
+    stream = torch.cuda.Stream(device=dev)
+    sp = stream.cuda_stream
+    bytes1 = sum(int((w.hi - w.lo).clip(min=0).sum()) for w in t1.waves) * scn.kv_bytes_per_token
+    bytes2 = sum(int((w.hi - w.lo).clip(min=0).sum()) for w in t2.waves) * scn.kv_bytes_per_token
+    times, stalls, bad = [], [], 0
+    for s in range(args.warmup + args.steps):
+        for k, (b, e) in enumerate(W.stage_ranges(L, t1.old_boundaries)):
+            poolsA[k].fill_pattern(SEED, b, live1, tok1[live1], src_bt1)
+        bmA.reset()
+        bmB.reset()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        st1 = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), stream)
+        st2 = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), stream)
+        tr1 = kvx.Transition(g, t1.old_boundaries, poolsA, t1.new_boundaries, poolsB, dev, N, max_blocks, capB,
+                             src_bt1, epoch=t1.epoch, max_sync_rounds=scn.max_sync_rounds,
+                             kv_bytes_per_token=scn.kv_bytes_per_token, stream=sp, dst_blockmgr=bmB)
+        torch.cuda.synchronize(dev)
+        ev[0].record(stream)
+        run_step(tr1, t1, st1)
+        ev[1].record(stream)
+        torch.cuda.synchronize(dev)
+        table = tr1.dst_block_table()
+        tr1.close()
+        # serving between the refactors: decode appends into the 4-stage pools
+        grown = W.serving_append(bmB.pop, table, t1.live_kv_map(N), tok2)
+        if len(grown):
+            for k, (b, e) in enumerate(W.stage_ranges(L, t1.new_boundaries)):
+                poolsB[k].fill_pattern(SEED, b, grown, tok2[grown], table)
+        tr2 = kvx.Transition(g, t2.old_boundaries, poolsB, t2.new_boundaries, poolsA, dev, N, max_blocks, capA,
+                             table, epoch=t2.epoch, max_sync_rounds=scn.max_sync_rounds,
+                             kv_bytes_per_token=scn.kv_bytes_per_token, stream=sp, dst_blockmgr=bmA)
+        torch.cuda.synchronize(dev)
+        ev[2].record(stream)
+        run_step(tr2, t2, st2)
+        ev[3].record(stream)
+        torch.cuda.synchronize(dev)
+        if s == args.warmup + args.steps - 1:
+            bad = tr2.verify_pattern(SEED, t2.live_req, t2.live_kv)
+        tr2.close()
+        if s >= args.warmup:
+            times.append((ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])))
+            stalls.append((st1[0].elapsed_time(st1[1]), st2[0].elapsed_time(st2[1])))
+    if bad:
+        raise SystemExit(f"bench c5: final KV differs from the payload ({bad} words)")
+    ms1 = statistics.median(x[0] for x in times)
+    ms2 = statistics.median(x[1] for x in times)
+    value = (bytes1 + bytes2) / ((ms1 + ms2) * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms1 + ms2, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp16 (u16 words)", "data": "synthetic",
+        "config": {"workload": "BASELINE C5: bursty gamma trace (CV=4), mixed lengths, repeated inflight "
+                               "refactors 8->4->8 at the Llama-2-13B shape, chained through device block "
+                               "managers", "golden_wave_plan": "bursty_repeated",
+                   "transitions": [{"stages": f"{t1.old_stages}->{t1.new_stages}", "bytes": bytes1,
+                                    "ms": round(ms1, 4), "stall_ms": round(statistics.median(x[0] for x in stalls), 4)},
+                                   {"stages": f"{t2.old_stages}->{t2.new_stages}", "bytes": bytes2,
+                                    "ms": round(ms2, 4), "stall_ms": round(statistics.median(x[1] for x in stalls), 4)}]},
+        "verified_words_mismatched": int(bad),
+    }
+    print(json.dumps(line), flush=True)
+    for p in poolsA + poolsB:
+        p.close()
+    bmA.close()
+    bmB.close()
+    return 0
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -342,7 +439,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kvx", choices=["kvx", "reference"])
-    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + ["c5"])
     ap.add_argument("--placement", default="affinity", choices=["affinity", "disjoint"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -352,6 +449,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "c5":
+        return run_chain(args)
     if args.warmup < 3:
         args.warmup = 3
 

@@ -85,6 +85,13 @@ class TransitionSpec:
     violations: Optional[int] = None
     kv_synced_bytes_total: Optional[float] = None
 
+    def live_kv_map(self, max_requests: int) -> np.ndarray:
+        """kv_tokens at commit per request id (0 for requests not live)."""
+        t = np.zeros(max_requests, np.int64)
+        if self.live_req is not None:
+            t[self.live_req] = self.live_kv
+        return t
+
     def max_tokens(self, max_requests: int) -> np.ndarray:
         """Per-request token count the source must hold (max over waves/commit)."""
         t = np.zeros(max_requests, np.int64)
@@ -195,3 +202,19 @@ def stage_ranges(num_layers: int, boundaries) -> List[Tuple[int, int]]:
 
 def synthetic_lengths(n: int, lo: int, hi: int, seed: int) -> np.ndarray:
     return np.random.default_rng(seed).integers(lo, hi + 1, size=n).astype(np.int64)
+
+
+def serving_append(pop, table: np.ndarray, have: np.ndarray, want: np.ndarray,
+                   block_tokens: int = 16) -> np.ndarray:
+    """Emulates the serving pipeline's decode appends between two refactors:
+    every request growing from have[r] to want[r] tokens gets the extra
+    logical blocks popped from its pool set's block manager (`pop(n) -> ids`)
+    and written into `table` (in place).  Returns the grown request ids."""
+    grown = []
+    for r in np.nonzero(want > have)[0]:
+        b0 = int((have[r] + block_tokens - 1) // block_tokens)
+        b1 = int((want[r] + block_tokens - 1) // block_tokens)
+        if b1 > b0:
+            table[r, b0:b1] = pop(b1 - b0)
+        grown.append(int(r))
+    return np.array(grown, np.int32)
