@@ -47,6 +47,7 @@
 #undef private
 
 #include "kvx.h"
+#include "scenarios.hpp"  // oracle/scenarios.hpp: the golden scenarios, shared with the extractor
 
 using namespace pipesim;
 using json = nlohmann::json;
@@ -81,6 +82,7 @@ struct Xfer {  // one transition's data-plane state
     int64_t tokens = 0;
     Live commit_live;
     bool have_commit_live = false;
+    json wave_times = json::array();
 };
 
 struct Observer {
@@ -169,7 +171,20 @@ struct Observer {
             x.tokens += std::max<int64_t>(0, target - lo.back());
         }
         fill_source(x, req, hi);  // decode appends of the serving pipeline
+        int64_t tok = 0;
+        for (size_t i = 0; i < req.size(); ++i) tok += std::max<int64_t>(0, hi[i] - lo[i]);
         CHECK_KVX(kvx_wave(x.t, x.epoch, (int32_t)req.size(), req.data(), lo.data(), hi.data()));
+        // measured-time mode: the B200 time of this wave beside the reference's
+        // modelled sync_ms = tokens * kv_bytes_per_token / kv_bw() (engine.cpp:644,670,683)
+        double ms = 0.0;
+        CHECK_KVX(kvx_wait(x.t, x.epoch, &ms));
+        const double bw = e->cfg_.kv_sync_bw_bytes_per_ms > 0.0 ? e->cfg_.kv_sync_bw_bytes_per_ms
+                                                                : e->cfg_.inter_stage_bw_bytes_per_ms;
+        json w;
+        w["tokens"] = tok;
+        w["modelled_ms"] = (double)tok * e->cfg_.exec.kv_bytes_per_token / bw;
+        w["measured_ms"] = ms;
+        x.wave_times.push_back(w);
         ++x.waves;
     }
 
@@ -181,6 +196,7 @@ struct Observer {
         j["tokens"] = x.tokens;
         j["old_stages"] = x.old_pools.size();
         j["new_stages"] = x.new_pools.size();
+        j["wave_times"] = x.wave_times;
         if (committed) {
             if (!x.have_commit_live) {
                 std::fprintf(stderr, "commit without a captured live set\n");
@@ -295,72 +311,40 @@ std::vector<Request> steady(int n, double gap, int prompt, int output) {
 }  // namespace
 
 int main(int argc, char** argv) {
-    const std::string name = argc > 1 ? argv[1] : "criterion12";
-    const int heads = argc > 2 ? std::atoi(argv[2]) : 2;
-    const int dim = argc > 3 ? std::atoi(argv[3]) : 64;
-
-    // Fixtures of test_engine.cpp:23-55 / acceptance_main.cpp:631-689.
-    CompGraph g = make_uniform_chain(32, 1.0, 0.5e9, 2.0e6, 2);
-    PartitionParams pp;
-    pp.bandwidth_bytes_per_ms = 1.0e7;
-    pp.gpu_memory_bytes = 16.0e9;
-    EngineConfig ec;
-    ec.graph = g;
-    ec.exec.batch_exponent = 0.8;
-    ec.exec.kv_bytes_per_token = 1.0e5;
-    ec.exec.batch_scaling = {0.1, 1};
-    ec.inter_stage_bw_bytes_per_ms = 1.0e7;
-    ec.policy.adaptive = false;
-    ec.policy.initial_instances = 1;
-    ec.default_slo_ms = 1.0e9;
-    SyntheticClusterSpec cs;
-    cs.racks = 2;
-    cs.gpus_per_server = 4;
-    cs.gpu_memory_bytes = 16.0e9;
-    std::vector<Request> reqs;
-    std::vector<std::pair<double, int>> forced;
-    std::vector<double> revoke;
-    if (name == "criterion12") {  // acceptance_main.cpp:631-689
-        ec.granularities = enumerate_granularities(g, {4, 16}, pp, 8);
-        ec.exec.batch_max_wait_ms = 5.0;
-        ec.policy.static_stages = 4;
-        cs.servers_per_rack = 8;
-        for (int i = 0; i < 100; ++i) {
-            Request r;
-            r.id = i;
-            r.arrival_ms = 1.0 + 0.05 * i;
-            r.prompt_tokens = 120;
-            r.output_tokens = 24;
-            r.model_id = "m0";
-            r.slo_deadline_ms = 1.0e9;
-            reqs.push_back(r);
-        }
-        forced = {{400.0, 16}, {8000.0, 4}};
-    } else if (name == "consolidate" || name == "revoke") {  // test_engine.cpp:240-263
-        const bool rv = name == "revoke";
-        ec.granularities = enumerate_granularities(g, {4, 16}, pp, 32);
-        ec.exec.batch_max_wait_ms = 0.0;
-        ec.policy.static_stages = rv ? 4 : 16;
-        cs.servers_per_rack = 4;
-        cs.storage_bw_bytes_per_ms = 1.0e6;
-        cs.host_bw_bytes_per_ms = 1.0e7;
-        reqs = steady(40, 4.0, 100, 10);
-        forced = {{rv ? 100.0 : 150.0, rv ? 16 : 4}};
-        if (rv) revoke = {110.0};
-    } else {
+    std::string name = argc > 1 ? argv[1] : "criterion12";
+    if (name == "consolidate") name = "engine_consolidate";  // test_engine.cpp:240-249
+    if (name == "revoke") name = "engine_revoke";            // test_engine.cpp:251-263
+    const scen::Scenario* sp = nullptr;
+    const auto all = scen::scenarios();
+    for (const auto& sc : all)
+        if (sc.name == name) sp = &sc;
+    if (!sp) {
         std::fprintf(stderr, "unknown scenario %s\n", name.c_str());
         return 1;
     }
-    Hrg cluster = make_synthetic_cluster(cs);
-    ec.storage_bw_bytes_per_ms = cs.storage_bw_bytes_per_ms;
-
-    Engine engine(ec, cluster, reqs);
-    for (auto [t, k] : forced) engine.force_refactor_at(t, "m0", k);
-    for (double t : revoke) engine.revoke_grant_at(t, "m0");
+    const scen::Scenario& sc = *sp;
+    // KV geometry: "auto" = the model shape whose bytes/token equals the
+    // scenario's kv_bytes_per_token (Llama presets); else heads x dim given.
+    int heads = 2, dim = 64;
+    if (argc > 2 && std::string(argv[2]) == "auto") {
+        const double per = sc.kv_bytes_per_token / (2.0 * sc.num_ops * 128 * 2);
+        if (per == (double)(int)per && per >= 1.0) {
+            heads = (int)per;
+            dim = 128;
+        }
+    } else if (argc > 3) {
+        heads = std::atoi(argv[2]);
+        dim = std::atoi(argv[3]);
+    }
+    scen::Built built = scen::build(sc);
+    const std::vector<Request>& reqs = sc.reqs;
+    Engine engine(built.ec, built.cluster, reqs);
+    for (auto [t, k] : sc.forced) engine.force_refactor_at(t, "m0", k);
+    for (double t : sc.revocations) engine.revoke_grant_at(t, "m0");
 
     Observer obs;
     obs.e = &engine;
-    obs.g = kvx_geometry{32, heads, dim, 2, 16};
+    obs.g = kvx_geometry{sc.num_ops, heads, dim, 2, 16};
     obs.max_requests = (int32_t)reqs.size();
     int32_t total = 0;
     for (const auto& r : reqs) {
@@ -397,6 +381,7 @@ int main(int argc, char** argv) {
     sum["transitions"] = obs.transitions;
     sum["kv_synced_bytes_reference"] = res.kv_synced_bytes;
     sum["kvx_launches"] = kvx_launch_count();
+    sum["geometry"] = {sc.num_ops, heads, dim};
     std::printf("%s\n", sum.dump().c_str());
     return (obs.mismatched_words == 0 && obs.dev_violations == res.kv_violations) ? 0 : 5;
 }

@@ -32,3 +32,20 @@ def test_reference_engine_drives_kvx(gpu_count, scenario, commits, aborts):
     for l in lines[:-1]:
         if l["kind"] == "commit":
             assert l["live"] > 0 and l["blocks"] > 0
+
+
+@pytest.mark.parametrize("scenario", ["llama13b_8to4", "llama7b_4to2"])
+def test_measured_time_mode_real_geometry(gpu_count, scenario):
+    """The same harness at the scenario's real KV geometry (geometry 'auto':
+    40x128 for 13B, 32x128 for 7B): every wave reports the reference's modelled
+    sync time (tokens * kv_bytes_per_token / kv_bw) beside the B200-measured one."""
+    out = subprocess.run([BIN, scenario, "auto"], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout + out.stderr
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    summary = lines[-1]
+    assert summary["geometry"][2] == 128 and summary["mismatched_words"] == 0
+    assert summary["kv_violations_device"] == summary["kv_violations_reference"] == 0
+    waves = [w for l in lines[:-1] for w in l["wave_times"]]
+    assert waves and all(w["measured_ms"] >= 0 for w in waves)
+    big = max(waves, key=lambda w: w["tokens"])
+    assert big["measured_ms"] < big["modelled_ms"]  # B200 HBM/NVLink beats the modelled 900 GB/s link
