@@ -728,7 +728,7 @@ def main():
         "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "handoff": handoff,
         "weights": weights, "nccl_baseline": nccl,
         "move_kernel_ms_per_step": round(all_move_ms / K, 4), "move_ms_by_wave": wave_ms,
-        "mover": os.environ.get("KVX_MOVE_IMPL", "bulk") + ":" + os.environ.get("KVX_BULK_CFG", "0"),
+        "mover": os.environ.get("KVX_MOVE_IMPL", "bulk") + ":" + os.environ.get("KVX_BULK_CFG", "auto"),
     }
     if n_gpus == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1

@@ -150,8 +150,8 @@ struct kvx_transition {
     bool own_stream = true;
     int num_sms = 0;
     int move_ctas_per_sm = 1;
-    int bulk_ctas_per_sm = 1;
-    int bulk_variant = 0;
+    int bulk_ctas[16] = {};  // resident CTAs per SM of each bulk variant
+    int bulk_variant = -1;   // -1: chosen per wave from the average run size
     bool use_bulk = false;   // TMA bulk mover for local destinations
     bool peer_bulk = false;  // ... and for peer (NVLink) destinations
     std::vector<int32_t> old_b, new_b;
@@ -474,14 +474,19 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         return bail(fail(KVX_ECUDA, "occupancy query"));
     t->move_ctas_per_sm = std::max(1, occ);
     {
+        // -1 = per wave: 3 x 64 KiB ring for slab-sized runs (>= 64 KiB on
+        // average, e.g. full 320 KiB 13B blocks), 6 x 32 KiB otherwise
+        // (token-sized delta / final waves).  KVX_BULK_CFG pins one variant.
         const char* cfg = getenv("KVX_BULK_CFG");
-        t->bulk_variant = cfg ? std::max(0, std::min(kNumBulkVariants - 1, atoi(cfg))) : 0;
-        const BulkVariant& bv = kBulkVariants[t->bulk_variant];
-        const int smem = bv.stages * (int)bv.chunk;
-        if (cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bv.fn, kvx::kBulkThreads, smem) != cudaSuccess)
-            return bail(fail(KVX_ECUDA, "bulk kernel attributes"));
-        t->bulk_ctas_per_sm = std::max(1, occ);
+        t->bulk_variant = cfg ? std::max(0, std::min(kNumBulkVariants - 1, atoi(cfg))) : -1;
+        for (int v = 0; v < kNumBulkVariants; ++v) {
+            const BulkVariant& bv = kBulkVariants[v];
+            const int smem = bv.stages * (int)bv.chunk;
+            if (cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bv.fn, kvx::kBulkThreads, smem) != cudaSuccess)
+                return bail(fail(KVX_ECUDA, "bulk kernel attributes"));
+            t->bulk_ctas[v] = std::max(1, occ);
+        }
         // Bulk (TMA engine) mover by default, for local and peer (NVLink)
         // destinations alike; KVX_PEER_BULK=0 keeps the LSU mover for peer
         // pushes, KVX_MOVE_IMPL=lsu everywhere.
@@ -639,8 +644,10 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                                 (uint64_t)t->n_local_layers);
         KVX_CUDA(cudaEventRecord(ev.first, t->stream));
         if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
-            const BulkVariant& bv = kBulkVariants[t->bulk_variant];
-            const int64_t full_b = (int64_t)t->num_sms * t->bulk_ctas_per_sm;
+            const uint64_t run_bytes = nseg > 0 ? (uint64_t)tokens * 2ull * token_bytes(t->g) / (uint64_t)nseg : 0;
+            const int vi = t->bulk_variant >= 0 ? t->bulk_variant : (run_bytes >= 65536 ? 2 : 0);
+            const BulkVariant& bv = kBulkVariants[vi];
+            const int64_t full_b = (int64_t)t->num_sms * t->bulk_ctas[vi];
             const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
             bv.fn<<<grid_b, kvx::kBulkThreads, (size_t)bv.stages * bv.chunk, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
