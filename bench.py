@@ -445,6 +445,8 @@ def main():
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-weights", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--pull", action="store_true",
+                    help="cross-GPU moves pulled by the destination GPU instead of pushed")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -484,7 +486,7 @@ def main():
     old_pools, new_pools = S.setup_rank_pools(
         kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, dev, plan.old_blocks,
         plan.dst_blocks, all_gather=gather if world > 1 else None,
-        fill=(SEED, plan.live, plan.tokens[plan.live], plan.src_bt))
+        fill=(SEED, plan.live, plan.tokens[plan.live], plan.src_bt), pull=args.pull)
     if world > 1:
         dist.barrier()
 
@@ -495,7 +497,7 @@ def main():
         return kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, dev,
                               plan.N, plan.max_blocks, plan.dst_blocks, plan.src_bt, epoch=t.epoch,
                               max_sync_rounds=plan.scn.max_sync_rounds,
-                              kv_bytes_per_token=plan.kv_bytes_per_token, stream=sp)
+                              kv_bytes_per_token=plan.kv_bytes_per_token, stream=sp, pull=args.pull)
 
     K, Wm = args.steps, args.warmup
     trs = [make() for _ in range(Wm + K)]

@@ -152,6 +152,9 @@ typedef struct kvx_transition_desc {
     double kv_bytes_per_token;    /* accounting of kvx_ctl_* (engine.cpp:644); 0 = from geometry */
     void* stream;                 /* cudaStream_t to run on (not owned); NULL = a private stream */
     void* dst_blockmgr;           /* kvx_blockmgr* of the new pools; NULL = bump rule from id 0 */
+    int32_t pull;                 /* 0: move the layers whose OLD pool is local (push to peers);
+                                     1: move the layers whose NEW pool is local, reading peers'
+                                     (imported) old pools over NVLink (pull) */
 } kvx_transition_desc;
 
 typedef struct kvx_transition kvx_transition;

@@ -407,7 +407,10 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     if (!d->src_block_table) return fail(KVX_EINVAL, "src_block_table is null");
     for (int k = 0; k < d->new_plan.num_stages; ++k) {
         const kvx_pool* p = d->new_plan.pools[k];
-        if (!p) return fail(KVX_EINVAL, "every new-stage pool is required");
+        if (!p) {
+            if (d->pull) continue;  // pull: only the local new pools are written here
+            return fail(KVX_EINVAL, "every new-stage pool is required");
+        }
         const int32_t layers = (k + 1 < d->new_plan.num_stages ? nb[(size_t)k] : g.num_layers) -
                                stage_begin(nb, k);
         if (p->num_layers != layers) return fail(KVX_EINVAL, "new pool layer count != stage layer range");
@@ -547,8 +550,13 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     for (int32_t l = 0; l < g.num_layers; ++l) {
         const int so = stage_of_layer(ob, l), sn = stage_of_layer(nb, l);
         kvx_pool* src = t->old_pools[(size_t)so];
-        if (!src || src->imported || src->device != d->device) continue;
         kvx_pool* dst = t->new_pools[(size_t)sn];
+        if (d->pull) {  // this GPU owns the layer's destination; the source may be a peer's
+            if (!dst || dst->imported || dst->device != d->device || !src) continue;
+            if (src->imported) t->has_peer_dst = true;  // peer traffic on this handle
+        } else if (!src || src->imported || src->device != d->device) {
+            continue;
+        }
         const uint64_t ls = (uint64_t)(l - stage_begin(ob, so)) * (uint64_t)src->num_blocks * bb;
         const uint64_t ld = (uint64_t)(l - stage_begin(nb, sn)) * (uint64_t)dst->num_blocks * bb;
         layers.push_back({src->base + ls, dst->base + ld});
@@ -1158,7 +1166,7 @@ int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_
     dim3 grid((unsigned)n, (unsigned)cdiv64(max_tok, t->g.block_tokens));
     for (size_t k = 0; k < t->new_pools.size(); ++k) {
         const kvx_pool* p = t->new_pools[k];
-        if (p->imported) continue;  // the owning rank verifies it
+        if (!p || p->imported) continue;  // the owning rank verifies it
         kvx::kvx_verify_kernel<<<grid, 256, 0, t->stream>>>(
             p->base, p->num_blocks, stage_begin(t->new_b, (int)k), p->num_layers, d_req, d_kv,
             t->d_dst_bt, t->max_blocks, t->g.block_tokens, token_bytes(t->g), seed, d_bad);

@@ -79,7 +79,7 @@ class _Desc(C.Structure):
                 ("dst_num_blocks", C.c_int32), ("src_block_table", C.POINTER(C.c_int32)),
                 ("epoch", C.c_uint64), ("max_sync_rounds", C.c_int32),
                 ("kv_bytes_per_token", C.c_double), ("stream", C.c_void_p),
-                ("dst_blockmgr", C.c_void_p)]
+                ("dst_blockmgr", C.c_void_p), ("pull", C.c_int32)]
 
 
 class _CommitResult(C.Structure):
@@ -356,7 +356,7 @@ class Transition:
                  max_requests: int, max_blocks: int, dst_num_blocks: int,
                  src_block_table: np.ndarray, epoch: int = 1, max_sync_rounds: int = 8,
                  kv_bytes_per_token: float = 0.0, stream: int = 0,
-                 dst_blockmgr: Optional["BlockManager"] = None):
+                 dst_blockmgr: Optional["BlockManager"] = None, pull: bool = False):
         self.geom = geom
         self.max_requests, self.max_blocks = max_requests, max_blocks
         self._ob = _i32(list(old_boundaries))
@@ -364,7 +364,7 @@ class Transition:
         self._old = list(old_pools)
         self._new = list(new_pools)
         self._op = (C.c_void_p * len(self._old))(*[p.handle.value if p else None for p in self._old])
-        self._np = (C.c_void_p * len(self._new))(*[p.handle.value for p in self._new])
+        self._np = (C.c_void_p * len(self._new))(*[p.handle.value if p else None for p in self._new])
         src = _i32(src_block_table)
         if src.shape != (max_requests, max_blocks):
             raise ValueError("src_block_table must be [max_requests, max_blocks]")
@@ -381,6 +381,7 @@ class Transition:
         d.stream = stream or None
         d.dst_blockmgr = dst_blockmgr.handle.value if dst_blockmgr is not None else None
         self._bm = dst_blockmgr
+        d.pull = 1 if pull else 0
         h = C.c_void_p()
         _check(_lib.kvx_begin(C.byref(d), C.byref(h)))
         self._h = h

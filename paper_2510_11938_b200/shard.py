@@ -72,16 +72,20 @@ def link_bytes(L: int, ob, nb, old_dev, new_dev, layer_bytes: int, n_gpus: int):
 
 def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, old_blocks: int,
                      dst_blocks: int, all_gather: Optional[Callable] = None,
-                     fill: Optional[tuple] = None, zero_new: bool = True):
+                     fill: Optional[tuple] = None, zero_new: bool = True, pull: bool = False):
     """Creates this rank's pools and maps every peer's new-stage pool.
 
     fill = (seed, live_req, tokens, src_bt) writes the synthetic payload into
     the local old pools.  all_gather(obj) -> list of every rank's obj (e.g.
     torch.distributed.all_gather_object); None for a single process.
+    pull=False maps peers' NEW pools (this rank pushes its old layers into
+    them); pull=True maps peers' OLD pools (this rank pulls the layers of its
+    new stages out of them).
     Returns (old_pools, new_pools) indexed by stage (None where remote/absent).
     """
     L = g.num_layers
     old_pools: List = [None] * (len(ob) + 1)
+    mine = {}
     for k, (b, e) in enumerate(W.stage_ranges(L, ob)):
         if old_dev[k] == rank:
             p = kvx.Pool(device, g, e - b, old_blocks)
@@ -90,21 +94,24 @@ def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, o
                 p.zero()
                 p.fill_pattern(seed, b, live, tokens, src_bt)
             old_pools[k] = p
+            if pull and all_gather is not None:
+                mine[k] = p.export_ipc()
     new_pools: List = [None] * (len(nb) + 1)
-    mine = {}
     for j, (b, e) in enumerate(W.stage_ranges(L, nb)):
         if new_dev[j] == rank:
             p = kvx.Pool(device, g, e - b, dst_blocks)
             if zero_new:
                 p.zero()
             new_pools[j] = p
-            if all_gather is not None:
+            if not pull and all_gather is not None:
                 mine[j] = p.export_ipc()
     if all_gather is not None:
+        target, ranges, blocks = (old_pools, W.stage_ranges(L, ob), old_blocks) if pull else \
+            (new_pools, W.stage_ranges(L, nb), dst_blocks)
         for r, handles in enumerate(all_gather(mine)):
             if r == rank:
                 continue
             for j, h in handles.items():
-                b, e = W.stage_ranges(L, nb)[int(j)]
-                new_pools[int(j)] = kvx.Pool.import_ipc(device, h, g, e - b, dst_blocks)
+                b, e = ranges[int(j)]
+                target[int(j)] = kvx.Pool.import_ipc(device, h, g, e - b, blocks)
     return old_pools, new_pools

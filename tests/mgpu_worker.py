@@ -47,7 +47,7 @@ def cpu_worker(rank, world, port, out):
         out.put((rank, "err", traceback.format_exc()))
 
 
-def gpu_worker(rank, world, port, name, heads, dim, mode, out):
+def gpu_worker(rank, world, port, name, heads, dim, mode, pull, out):
     try:
         dist = _init(rank, world, port)
         import numpy as np
@@ -76,12 +76,12 @@ def gpu_worker(rank, world, port, name, heads, dim, mode, out):
 
         old_pools, new_pools = S.setup_rank_pools(
             kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, rank, old_blocks,
-            dst_blocks, all_gather=gather, fill=(SEED, live, tokens[live], src_bt))
+            dst_blocks, all_gather=gather, fill=(SEED, live, tokens[live], src_bt), pull=pull)
         dist.barrier()
         tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, rank, N,
                             max_blocks, dst_blocks, src_bt, epoch=t.epoch,
                             max_sync_rounds=scn.max_sync_rounds,
-                            kv_bytes_per_token=scn.kv_bytes_per_token)
+                            kv_bytes_per_token=scn.kv_bytes_per_token, pull=pull)
         octx = O.ControlCtx(N, scn.max_sync_rounds, scn.kv_bytes_per_token)
         dp = O.DataPlane(O.geo(L, heads, dim), t.old_boundaries, t.new_boundaries, old_blocks,
                          dst_blocks, N, max_blocks, src_bt)

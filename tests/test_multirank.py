@@ -42,10 +42,11 @@ def test_two_ranks_shard_every_layer_once_cpu():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("pull", [False, True], ids=["push", "pull"])
 @pytest.mark.parametrize("mode", ["affinity", "disjoint"])
 @pytest.mark.parametrize("name,heads,dim", [("criterion12", 2, 64), ("engine_consolidate", 2, 64)])
-def test_two_gpu_transition_bit_exact(gpu_count, mode, name, heads, dim):
+def test_two_gpu_transition_bit_exact(gpu_count, mode, name, heads, dim, pull):
     if gpu_count < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
-    res = _run(mgpu_worker.gpu_worker, 2, name, heads, dim, mode)
+    res = _run(mgpu_worker.gpu_worker, 2, name, heads, dim, mode, pull)
     assert sum(r["checked"] for r in res.values()) >= 2
