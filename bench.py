@@ -55,6 +55,9 @@ CONFIGS = {
            "Llama-2-7B shape, 2->8 split, 1024 live requests"),
     "c4": ("llama70b_8to2to8", "llama2-70b",
            "Llama-2-70B GQA shape (80 layers, 8 KV heads), 8->2 and 2->8"),
+    "c4r": ("llama70b_8to2to8", "llama2-70b",
+            "Llama-2-70B GQA shape (80 layers, 8 KV heads), same-K re-placement of all 8 stages "
+            "(10 layers each), ~64k live tokens = 21 GB; wave plan of the reference's 2->8 transition"),
 }
 SEED = 0xB200
 METRIC = "KV-refactor GB/s (% of HBM/NVLink roofline); refactor stall ms at 1/2/4/8 B200"
@@ -150,8 +153,15 @@ class Plan:
         golden, shape, self.desc = CONFIGS[cfg]
         self.golden = golden
         self.scn = W.load_golden(golden)
-        self.t = [t for t in self.scn.transitions if t.outcome == "commit"][-1] if cfg == "c4" \
+        self.t = [t for t in self.scn.transitions if t.outcome == "commit"][-1] if cfg in ("c4", "c4r") \
             else self.scn.transitions[0]
+        if cfg == "c4r":
+            # BASELINE C4: same-K re-placement.  The reference drops same-plan
+            # directives (engine.cpp:562) -- parity unpinned; its last wave
+            # plan is reused with the old 8-stage cut on both sides.
+            import copy
+            self.t = copy.copy(self.t)
+            self.t.old_boundaries = list(self.t.new_boundaries)
         self.L, self.H, self.D = W.SHAPES[shape]
         self.N = self.scn.num_requests
         self.tokens = self.t.max_tokens(self.N)

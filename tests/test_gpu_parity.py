@@ -78,3 +78,24 @@ def test_full_size_properties(gpu_count, name):
             assert case.tr.bytes_moved() == moved * 2 * case.g.token_bytes * L
         finally:
             case.close()
+
+
+def test_c4_same_k_replacement_full_size(gpu_count):
+    """BASELINE config 4: every 10-layer stage of the 80-layer 70B-GQA model
+    re-placed (same boundaries on both sides) -- no reference path
+    (engine.cpp:562), so the oracle restatement is the only pin: block table
+    identical to the oracle's, every live word equal to the payload."""
+    import copy
+    scn = W.load_golden("llama70b_8to2to8")
+    t = copy.copy([x for x in scn.transitions if x.outcome == "commit"][-1])
+    t.old_boundaries = list(t.new_boundaries)
+    assert len(t.old_boundaries) == 7
+    case = GpuCase(scn, t, 8, 128, oracle_pools=False)
+    try:
+        case.run_ctl()
+        case.compare_tables()
+        res = _commit_and_compare(case)
+        assert res.violations == 0
+        assert case.tr.verify_pattern(SEED, t.live_req, t.live_kv) == 0
+    finally:
+        case.close()
