@@ -202,6 +202,7 @@ struct kvx_transition {
 
     // host mirror of the destination rule (capacity checks are synchronous)
     std::vector<int64_t> synced_hi;
+    std::vector<int32_t> src_bt;  // host copy: every wave's source blocks must be backed
     int32_t alloc = 0;
     uint64_t bytes_moved = 0;       // by this handle (local-source layers)
     uint64_t bytes_all_layers = 0;  // reference-accounted, all layers
@@ -370,25 +371,31 @@ int kvx_pool_fill_pattern(kvx_pool* p, uint64_t seed, int32_t first_layer, int32
     }
     if (max_tok == 0) return KVX_OK;
     DeviceGuard dg(p->device);
-    int32_t* d_req = nullptr;
-    int64_t* d_tok = nullptr;
-    int32_t* d_bt = nullptr;
+    kvx::Arena& A = kvx::Arena::of(p->device);
     const size_t bt_bytes = sizeof(int32_t) * (size_t)max_requests * (size_t)max_blocks;
-    KVX_CUDA(cudaMalloc(&d_req, sizeof(int32_t) * n));
-    KVX_CUDA(cudaMalloc(&d_tok, sizeof(int64_t) * n));
-    KVX_CUDA(cudaMalloc(&d_bt, bt_bytes));
-    KVX_CUDA(cudaMemcpy(d_req, req, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
-    KVX_CUDA(cudaMemcpy(d_tok, tokens, sizeof(int64_t) * n, cudaMemcpyHostToDevice));
-    KVX_CUDA(cudaMemcpy(d_bt, bt, bt_bytes, cudaMemcpyHostToDevice));
+    struct Scratch {  // released on every return path
+        kvx::Arena& a;
+        void *req = nullptr, *tok = nullptr, *bt = nullptr;
+        size_t nreq, ntok, nbt;
+        ~Scratch() {
+            a.dev_free(req, nreq);
+            a.dev_free(tok, ntok);
+            a.dev_free(bt, nbt);
+        }
+    } sc{A, nullptr, nullptr, nullptr, sizeof(int32_t) * n, sizeof(int64_t) * n, bt_bytes};
+    KVX_CUDA(A.dev_alloc(&sc.req, sc.nreq));
+    KVX_CUDA(A.dev_alloc(&sc.tok, sc.ntok));
+    KVX_CUDA(A.dev_alloc(&sc.bt, sc.nbt));
+    KVX_CUDA(cudaMemcpy(sc.req, req, sc.nreq, cudaMemcpyHostToDevice));
+    KVX_CUDA(cudaMemcpy(sc.tok, tokens, sc.ntok, cudaMemcpyHostToDevice));
+    KVX_CUDA(cudaMemcpy(sc.bt, bt, sc.nbt, cudaMemcpyHostToDevice));
     dim3 grid((unsigned)n, (unsigned)cdiv64(max_tok, p->g.block_tokens));
-    kvx::kvx_fill_kernel<<<grid, 256>>>(p->base, p->num_blocks, first_layer, p->num_layers, d_req,
-                                        d_tok, d_bt, max_blocks, p->g.block_tokens,
+    kvx::kvx_fill_kernel<<<grid, 256>>>(p->base, p->num_blocks, first_layer, p->num_layers,
+                                        static_cast<const int32_t*>(sc.req), static_cast<const int64_t*>(sc.tok),
+                                        static_cast<const int32_t*>(sc.bt), max_blocks, p->g.block_tokens,
                                         token_bytes(p->g), seed);
     KVX_LAUNCHED();
     KVX_CUDA(cudaDeviceSynchronize());
-    cudaFree(d_req);
-    cudaFree(d_tok);
-    cudaFree(d_bt);
     return KVX_OK;
 }
 
@@ -461,6 +468,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     t->bm = static_cast<kvx_blockmgr*>(d->dst_blockmgr);
     t->epoch = d->epoch;
     t->synced_hi.assign((size_t)d->max_requests, 0);
+    t->src_bt.assign(d->src_block_table, d->src_block_table + cells);
     t->ctl.init(d->max_requests, d->max_sync_rounds,
                 d->kv_bytes_per_token > 0.0 ? d->kv_bytes_per_token
                                             : (double)g.num_layers * (double)block_bytes(g) /
@@ -552,7 +560,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         kvx_pool* src = t->old_pools[(size_t)so];
         kvx_pool* dst = t->new_pools[(size_t)sn];
         if (d->pull) {  // this GPU owns the layer's destination; the source may be a peer's
-            if (!dst || dst->imported || dst->device != d->device || !src) continue;
+            if (!dst || dst->imported || dst->device != d->device) continue;
+            if (!src) return bail(fail(KVX_EINVAL, "pull: a local destination layer has no mapped source pool"));
             if (src->imported) t->has_peer_dst = true;  // peer traffic on this handle
         } else if (!src || src->imported || src->device != d->device) {
             continue;
@@ -595,6 +604,9 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         const int64_t s = t->synced_hi[(size_t)r];
         if (lo[i] < 0 || lo[i] > s) return fail(KVX_EINVAL, "wave interval leaves a gap (lo > synced)");
         if (cdiv64(hi[i], B) > t->max_blocks) return fail(KVX_ENOSPC, "request exceeds max_blocks");
+        const int32_t* srow = t->src_bt.data() + (size_t)r * (size_t)t->max_blocks;
+        for (int64_t b = lo[i] / B; b < cdiv64(hi[i], B); ++b)
+            if (srow[b] < 0) return fail(KVX_EINVAL, "wave reads a source block the source table does not back");
         new_blocks += std::max<int64_t>(0, cdiv64(hi[i], B) - cdiv64(s, B));
         nseg += cdiv64(hi[i], B) - lo[i] / B;
         tokens += hi[i] - lo[i];

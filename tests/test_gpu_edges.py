@@ -107,6 +107,9 @@ def test_errors(gpu_count):
             m.tr.wave([0], [0], [49])                            # 4 blocks > max_blocks 3
         with pytest.raises(kvx.StaleEpoch):
             m.tr.wave([0], [0], [1], epoch=4)
+        with pytest.raises(kvx.KvxError) as e:
+            m.tr.wave([2], [0], [5])                             # request 2 has no source blocks
+        assert e.value.code == kvx.KVX_EINVAL
         m.wave([0], [0], [40])
         res = m.tr.commit([0, 1], [40, 20])
         assert res.violations == 1                               # request 1 never synced
