@@ -321,6 +321,23 @@ def cpu_sample_run(plan: Plan, steps: int, warmup: int, threads: int, target_byt
     return gbs, desc, step_bytes
 
 
+def reference_control_plane(golden: str):
+    """The reference's OWN transition handlers (oracle/_ref/extract_waves, the
+    unmodified reference library) timed on this host for the same scenario:
+    refactor_begin / kv_sync_complete / refactor_commit wall us (median).  The
+    reference moves no bytes, so this is its whole CPU path for the
+    transition; None when the prebuilt binary is absent."""
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "extract_waves")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe, "--time", golden, "5"], capture_output=True, text=True, timeout=120)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # report, never fail the bench on it
+        return {"error": str(e)}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -336,7 +353,8 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16 (u16 words)",
         "data": "synthetic", "config": {"workload": plan.desc, "golden_wave_plan": plan.golden},
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": desc},
+                         "sample": desc,
+                         "reference_control_plane": reference_control_plane(plan.golden)},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference (pipesim) is a simulator that moves no bytes; its CPU path for this "
                 "metric is the oracle restatement executing the identical byte plan",
@@ -746,7 +764,8 @@ def main():
         threads = os.cpu_count() or 1
         gbs, desc, _ = cpu_sample_run(plan, 3, 1, threads)
         line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                                "sample": desc}
+                                "sample": desc,
+                                "reference_control_plane": reference_control_plane(plan.golden)}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

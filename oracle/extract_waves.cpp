@@ -24,7 +24,9 @@
 // reference produced.
 //
 // Usage: extract_waves <out_dir>   (writes <scenario>.jsonl per scenario)
+#include <algorithm>
 #include <any>
+#include <chrono>
 #include <cstdio>
 #include <deque>
 #include <fstream>
@@ -331,7 +333,54 @@ void run(const Scenario& s, const std::string& dir) {
 
 }  // namespace
 
+// --time <scenario> <reps>: wall time of the reference's own transition
+// handlers (SURVEY App. A probe 3), attributed by trace-sink deltas: the sink
+// runs right before each handler (engine.cpp:243-245), so a handler's cost is
+// the time to the next dispatch.  Medians over reps; JSON on stdout.
+int time_handlers(const std::string& name, int reps) {
+    std::map<std::string, std::vector<double>> us;
+    std::vector<double> run_ms;
+    for (const auto& s : scenarios()) {
+        if (s.name != name) continue;
+        for (int rep = 0; rep < reps; ++rep) {
+            scen::Built b = scen::build(s);
+            Engine engine(b.ec, b.cluster, s.reqs);
+            for (const auto& [t, k] : s.forced) engine.force_refactor_at(t, "m0", k);
+            for (double t : s.revocations) engine.revoke_grant_at(t, "m0");
+            std::string pending;
+            auto t_prev = std::chrono::steady_clock::now();
+            engine.set_trace_sink([&](const SimEvent& ev) {
+                const auto now = std::chrono::steady_clock::now();
+                if (!pending.empty())
+                    us[pending].push_back(std::chrono::duration<double, std::micro>(now - t_prev).count());
+                pending.clear();
+                if (ev.kind == EventKind::RefactorBegin || ev.kind == EventKind::KvSyncComplete ||
+                    ev.kind == EventKind::RefactorCommit)
+                    pending = to_string(ev.kind);
+                t_prev = std::chrono::steady_clock::now();
+            });
+            const auto t0 = std::chrono::steady_clock::now();
+            engine.run();
+            run_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        }
+    }
+    auto med = [](std::vector<double> v) {
+        if (v.empty()) return 0.0;
+        std::sort(v.begin(), v.end());
+        return v[v.size() / 2];
+    };
+    json j;
+    j["scenario"] = name;
+    j["reps"] = reps;
+    for (const auto& [k, v] : us) j[k + "_us"] = med(v);
+    j["engine_run_ms"] = med(run_ms);
+    std::printf("%s\n", j.dump().c_str());
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 2 && std::string(argv[1]) == "--time")
+        return time_handlers(argv[2], argc > 3 ? std::atoi(argv[3]) : 5);
     const std::string dir = argc > 1 ? argv[1] : ".";
     const std::string only = argc > 2 ? argv[2] : "";
     for (const auto& s : scenarios()) {
