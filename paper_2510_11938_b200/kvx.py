@@ -261,6 +261,13 @@ class Pool:
     def nbytes(self) -> int:
         return self.num_layers * self.num_blocks * self.geom.block_bytes
 
+    @property
+    def ptr(self) -> int:
+        """Device address of the pool (local, or this process's peer mapping)."""
+        d = C.c_void_p()
+        _check(_lib.kvx_pool_info(self._h, C.byref(d), None, None, None))
+        return int(d.value or 0)
+
     def zero(self) -> None:
         _check(_lib.kvx_pool_zero(self._h))
 

@@ -132,3 +132,98 @@ def gpu_worker(rank, world, port, name, heads, dim, mode, pull, out):
                               "new_dev": new_dev}))
     except Exception:
         out.put((rank, "err", traceback.format_exc()))
+
+
+def handoff_worker(rank, world, port, out):
+    """Cross-GPU activation handoff: criterion12's second transition (16 -> 4)
+    with the old stages split over 2 GPUs and the new stages shifted ('disjoint'
+    placement), so every in-flight micro-batch crosses NVLink into an arena
+    mapped from the peer through CUDA IPC."""
+    try:
+        dist = _init(rank, world, port)
+        import numpy as np
+        import torch
+        from oracle import pyoracle as O
+        from paper_2510_11938_b200 import kvx
+        from paper_2510_11938_b200 import shard as S
+        from paper_2510_11938_b200 import workload as W
+
+        torch.cuda.set_device(rank)
+        scn = W.load_golden("engine_consolidate")   # 16 -> 4, 19 in-flight micro-batches at the barrier
+        t = scn.transitions[0]
+        bar = next(e for e in t.events if isinstance(e, W.Barrier))
+        L, N = scn.num_layers, scn.num_requests
+        g = kvx.geometry(L, 1, 8)
+        old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, world, "disjoint")
+        tokens = t.max_tokens(N)
+        max_blocks = int(max(1, (tokens.max() + 15) // 16))
+        src_bt, cap0 = W.fragmented_block_table(tokens, max_blocks, 16, seed=7)
+        dst = max(1, int(((tokens + 15) // 16).sum()))
+
+        def gather(obj):
+            o = [None] * world
+            dist.all_gather_object(o, obj)
+            return o
+
+        old_pools, new_pools = S.setup_rank_pools(kvx, g, t.old_boundaries, t.new_boundaries, old_dev,
+                                                  new_dev, rank, rank, cap0, dst, all_gather=gather)
+        row = 512
+        cap = sum(m.tokens * row + 256 for m in bar.microbatches) + 256
+        # activation arenas of the new stages: raw pools, exported to the peer
+        ablocks = cap // g.block_bytes + 1
+        arenas, mine = [None] * len(new_dev), {}
+        for j, d in enumerate(new_dev):
+            if d == rank:
+                arenas[j] = kvx.Pool(rank, g, 1, ablocks)
+                arenas[j].zero()
+                mine[j] = arenas[j].export_ipc()
+        for r, hs in enumerate(gather(mine)):
+            for j, h in hs.items():
+                if r != rank:
+                    arenas[int(j)] = kvx.Pool.import_ipc(rank, h, g, 1, ablocks)
+
+        def payload(m):
+            gen = torch.Generator(device="cpu").manual_seed(int(m.batch))
+            return torch.randint(0, 256, (max(m.tokens, 1) * row,), dtype=torch.uint8, generator=gen)
+
+        srcs = []
+        for m in bar.microbatches:
+            local = m.after >= 0 and m.after + 1 < len(old_dev) and old_dev[m.after] == rank
+            srcs.append(payload(m).cuda() if local else torch.empty(16, dtype=torch.uint8, device="cuda"))
+        torch.cuda.synchronize()
+        tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, rank, N,
+                            max_blocks, dst, src_bt, epoch=t.epoch)
+        slots = tr.handoff(row, [(m.batch, m.after, m.tokens, s.data_ptr())
+                                 for m, s in zip(bar.microbatches, srcs)],
+                           [a.ptr for a in arenas], [cap] * len(arenas))
+        tr.wait()
+        rc, ns, rl, off, by = O.handoff_plan(t.old_boundaries, t.new_boundaries, row,
+                                             [m.after for m in bar.microbatches],
+                                             [m.tokens for m in bar.microbatches], [cap] * len(arenas))
+        assert rc == 0
+        for i, sl in enumerate(slots):
+            assert tuple(sl) == (bar.microbatches[i].batch, ns[i], rl[i], off[i], by[i])
+        dist.barrier()   # every rank's pushes have landed
+        checked = crossed = 0
+        for i, m in enumerate(bar.microbatches):
+            k, nbytes = int(ns[i]), int(by[i])
+            if nbytes == 0 or new_dev[k] != rank:
+                continue
+            got = arenas[k].read(int(off[i]), nbytes)
+            assert np.array_equal(got, payload(m)[:nbytes].numpy()), f"batch {m.batch}"
+            checked += 1
+            crossed += old_dev[m.after] != rank
+        tr.close()
+        dist.barrier()
+        for p in arenas + old_pools + new_pools:
+            if p is not None and p.imported:
+                p.close()
+        dist.barrier()
+        for p in arenas + old_pools + new_pools:
+            if p is not None and not p.imported:
+                p.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        out.put((rank, "ok", {"checked": checked, "crossed": crossed}))
+    except Exception:
+        out.put((rank, "err", traceback.format_exc()))

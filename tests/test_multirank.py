@@ -50,3 +50,12 @@ def test_two_gpu_transition_bit_exact(gpu_count, mode, name, heads, dim, pull):
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
     res = _run(mgpu_worker.gpu_worker, 2, name, heads, dim, mode, pull)
     assert sum(r["checked"] for r in res.values()) >= 2
+
+
+@pytest.mark.gpu
+def test_two_gpu_activation_handoff(gpu_count):
+    if gpu_count < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    res = _run(mgpu_worker.handoff_worker, 2)
+    assert sum(r["checked"] for r in res.values()) >= 10
+    assert sum(r["crossed"] for r in res.values()) >= 10
