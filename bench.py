@@ -468,7 +468,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kvx", choices=["kvx", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + ["c5"])
-    ap.add_argument("--placement", default="affinity", choices=["affinity", "disjoint"])
+    ap.add_argument("--placement", default="affinity", choices=["affinity", "disjoint", "spread"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-weights", action="store_true")

@@ -33,9 +33,14 @@ def placement(L: int, ob: Sequence[int], nb: Sequence[int], n_gpus: int,
     already holds most of its layers (warm-start affinity, cluster.cpp:525-536
     and AffinityHistory::covers, cluster.cpp:158-199), ties to the lowest id.
     mode='disjoint' shifts each new stage by N/2 GPUs so all of its KV crosses
-    NVLink, the physical analogue of the reference's disjoint grant."""
+    NVLink, the physical analogue of the reference's disjoint grant.
+    mode='spread' puts new stage j on GPU floor(j * N / K_new): a split fans
+    its new stages out over every GPU (what a split is for)."""
     k_old = len(ob) + 1
     old_dev = [k * n_gpus // k_old for k in range(k_old)]
+    if mode == "spread":
+        k_new = len(nb) + 1
+        return old_dev, [j * n_gpus // k_new for j in range(k_new)]
     new_dev = []
     for b, e in W.stage_ranges(L, nb):
         share: Dict[int, int] = {}
