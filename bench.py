@@ -535,7 +535,10 @@ def main():
         run_step(trs[s], t)
     torch.cuda.synchronize(dev)
 
-    # ---- correctness gate on the warm-up output (device-side payload check)
+    # ---- correctness gate on the warm-up output (device-side payload check);
+    #      peers push into our pools, so every rank must be done first
+    if world > 1:
+        dist.barrier()
     bad = 0
     if not args.no_verify:
         bad = trs[Wm - 1].verify_pattern(SEED, t.live_req, t.live_kv)
