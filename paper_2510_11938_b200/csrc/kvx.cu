@@ -667,7 +667,8 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             const uint64_t run_bytes = nseg > 0 ? (uint64_t)tokens * 2ull * token_bytes(t->g) / (uint64_t)nseg : 0;
             const int vi = t->bulk_variant >= 0 ? t->bulk_variant : (run_bytes >= 65536 ? 2 : 0);
             const BulkVariant& bv = kBulkVariants[vi];
-            const int64_t full_b = (int64_t)t->num_sms * t->bulk_ctas[vi];
+            int64_t full_b = (int64_t)t->num_sms * t->bulk_ctas[vi];
+            if (const char* cap = getenv("KVX_BULK_GRID")) full_b = std::max<int64_t>(1, std::min<int64_t>(full_b, atoll(cap)));
             const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
             bv.fn<<<grid_b, kvx::kBulkThreads, (size_t)bv.stages * bv.chunk, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
