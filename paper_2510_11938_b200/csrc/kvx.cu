@@ -107,7 +107,8 @@ bool plan_ok(const kvx_plan& p, int32_t L, std::string* why, std::vector<int32_t
 // (ring depth, chunk bytes) of the TMA bulk mover; selectable with
 // KVX_BULK_CFG=<index> for tuning, index 0 is the default.
 namespace {
-using BulkFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, uint64_t, int32_t);
+using BulkFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, uint64_t, int32_t,
+                        int32_t, int32_t);
 struct BulkVariant {
     int stages;
     uint32_t chunk;
@@ -167,6 +168,7 @@ struct kvx_transition {
     int64_t* d_synced_hi = nullptr;
     kvx::LayerPtr* d_layers = nullptr;
     int32_t n_local_layers = 0;
+    int32_t n_peer_layers = 0;  // layers [0, n_peer_layers) of d_layers push to a peer
     bool has_peer_dst = false;
     // wave staging: pinned host ring of 2 + device buffer
     char* h_wave[2] = {nullptr, nullptr};
@@ -554,6 +556,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
 
     // Per-layer slab bases for the layers this GPU sources.
     std::vector<kvx::LayerPtr> layers;
+    std::vector<uint8_t> layer_is_peer;
     const uint64_t bb = block_bytes(g);
     for (int32_t l = 0; l < g.num_layers; ++l) {
         const int so = stage_of_layer(ob, l), sn = stage_of_layer(nb, l);
@@ -569,7 +572,16 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         const uint64_t ls = (uint64_t)(l - stage_begin(ob, so)) * (uint64_t)src->num_blocks * bb;
         const uint64_t ld = (uint64_t)(l - stage_begin(nb, sn)) * (uint64_t)dst->num_blocks * bb;
         layers.push_back({src->base + ls, dst->base + ld});
+        layer_is_peer.push_back(dst->imported || src->imported ? 1 : 0);
         if (dst->imported) t->has_peer_dst = true;
+    }
+    // peer-destination layers first (see kvx_bulk_kernel's CTA split)
+    {
+        std::vector<kvx::LayerPtr> peer, local;
+        for (size_t i = 0; i < layers.size(); ++i) (layer_is_peer[i] ? peer : local).push_back(layers[i]);
+        t->n_peer_layers = (int32_t)peer.size();
+        layers = peer;
+        layers.insert(layers.end(), local.begin(), local.end());
     }
     t->n_local_layers = (int32_t)layers.size();
     if (!layers.empty()) {
@@ -667,12 +679,21 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             const uint64_t run_bytes = nseg > 0 ? (uint64_t)tokens * 2ull * token_bytes(t->g) / (uint64_t)nseg : 0;
             const int vi = t->bulk_variant >= 0 ? t->bulk_variant : (run_bytes >= 65536 ? 2 : 0);
             const BulkVariant& bv = kBulkVariants[vi];
-            int64_t full_b = (int64_t)t->num_sms * t->bulk_ctas[vi];
+            // Grid: measured on B200 (profiles/r01_grid_sweep.jsonl), 128 one-CTA-per-SM
+            // streams beat all 148 SMs for HBM-bound waves (1.034 vs 0.98 of the copy
+            // peak); NVLink pushes saturate with ~16 CTAs, so mixed waves give the
+            // peer layers kPeerCtas of them and the local layers the rest.
+            constexpr int64_t kLocalGrid = 128, kPeerCtas = 32;
+            int64_t full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid);
+            if (t->n_peer_layers > 0 && t->n_peer_layers < t->n_local_layers)
+                full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid + kPeerCtas);
             if (const char* cap = getenv("KVX_BULK_GRID")) full_b = std::max<int64_t>(1, std::min<int64_t>(full_b, atoll(cap)));
+            int32_t peer_ctas = (int32_t)kPeerCtas;
+            if (const char* pc = getenv("KVX_PEER_CTAS")) peer_ctas = std::max(0, atoi(pc));
             const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
             bv.fn<<<grid_b, kvx::kBulkThreads, (size_t)bv.stages * bv.chunk, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
-                token_bytes(t->g), t->g.block_tokens);
+                token_bytes(t->g), t->g.block_tokens, t->n_peer_layers, peer_ctas);
         } else {
             kvx::kvx_move_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),

@@ -394,10 +394,15 @@ __device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint6
     bulk_wait_all();
 }
 
+// The first n_peer layers of `layers` have a peer (NVLink) destination.  When
+// a wave mixes them with local layers, CTAs [0, peer_ctas) stream only the
+// peer units and the rest only the local ones, so the NVLink-bound and the
+// HBM-bound traffic overlap instead of running layer after layer.
 template <int kStages, uint32_t kChunk>
 __global__ void __launch_bounds__(kBulkThreads)
 kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
-                int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens) {
+                int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
+                int32_t n_peer, int32_t peer_ctas) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[kStages];
     if (threadIdx.x != 0) return;
@@ -405,9 +410,22 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     it.segs = segs;
     it.layers = layers;
     it.nseg = nseg;
-    it.units = (int64_t)nseg * nlayers;
-    it.u = blockIdx.x;
-    it.ustep = gridDim.x;
+    const int64_t split = (int64_t)nseg * n_peer;
+    if (peer_ctas > 0 && n_peer > 0 && n_peer < nlayers && (int)gridDim.x > peer_ctas) {
+        if ((int)blockIdx.x < peer_ctas) {
+            it.u = blockIdx.x;
+            it.ustep = peer_ctas;
+            it.units = split;
+        } else {
+            it.u = split + (blockIdx.x - peer_ctas);
+            it.ustep = gridDim.x - peer_ctas;
+            it.units = (int64_t)nseg * nlayers;
+        }
+    } else {
+        it.u = blockIdx.x;
+        it.ustep = gridDim.x;
+        it.units = (int64_t)nseg * nlayers;
+    }
     it.block_bytes = block_bytes;
     it.token_bytes = token_bytes;
     it.block_tokens = block_tokens;
