@@ -687,7 +687,8 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             int64_t full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid);
             if (t->n_peer_layers > 0 && t->n_peer_layers < t->n_local_layers)
                 full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid + kPeerCtas);
-            if (const char* cap = getenv("KVX_BULK_GRID")) full_b = std::max<int64_t>(1, std::min<int64_t>(full_b, atoll(cap)));
+            if (const char* cap = getenv("KVX_BULK_GRID"))
+                full_b = std::max<int64_t>(1, std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], atoll(cap)));
             int32_t peer_ctas = (int32_t)kPeerCtas;
             if (const char* pc = getenv("KVX_PEER_CTAS")) peer_ctas = std::max(0, atoi(pc));
             const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
