@@ -131,6 +131,14 @@ int kvx_bm_push(kvx_blockmgr* bm, int32_t n, const int32_t* ids);
 int kvx_bm_snapshot(const kvx_blockmgr* bm, int32_t* stack_out, int32_t* top_out);
 int kvx_bm_destroy(kvx_blockmgr* bm);
 
+/* The serving pipeline's decode appends, as test / bench emulation: the
+ * payload for tokens [from[i], to[i]) of each request, stream-ordered on
+ * `stream` (NULL = legacy default), so it can run concurrently with a wave
+ * reading the same pool (KV is append-only, engine.cpp:494-499). */
+int kvx_pool_append_pattern(kvx_pool* p, void* stream, uint64_t seed, int32_t first_layer, int32_t n,
+                            const int32_t* req, const int64_t* from, const int64_t* to, const int32_t* bt,
+                            int32_t max_requests, int32_t max_blocks);
+
 /* ------------------------------------------------------------- transition */
 typedef struct kvx_plan {
     int32_t num_stages;           /* K */

@@ -103,6 +103,22 @@ bool plan_ok(const kvx_plan& p, int32_t L, std::string* why, std::vector<int32_t
 
 }  // namespace
 
+namespace {
+struct PieceRelease {  // returns a call's descriptor buffers to the arena once the stream passed them
+    int device;
+    void* d;
+    void* h;
+    size_t bytes;
+};
+void CUDART_CB release_pieces(void* arg) {
+    auto* r = static_cast<PieceRelease*>(arg);
+    kvx::Arena& A = kvx::Arena::of(r->device);
+    A.dev_free(r->d, r->bytes);
+    A.host_free(r->h, r->bytes);
+    delete r;
+}
+}  // namespace
+
 // ---------------------------------------------------------- bulk variants
 // (ring depth, chunk bytes) of the TMA bulk mover; selectable with
 // KVX_BULK_CFG=<index> for tuning, index 0 is the default.
@@ -398,6 +414,53 @@ int kvx_pool_fill_pattern(kvx_pool* p, uint64_t seed, int32_t first_layer, int32
                                         token_bytes(p->g), seed);
     KVX_LAUNCHED();
     KVX_CUDA(cudaDeviceSynchronize());
+    return KVX_OK;
+}
+
+int kvx_pool_append_pattern(kvx_pool* p, void* stream, uint64_t seed, int32_t first_layer, int32_t n,
+                            const int32_t* req, const int64_t* from, const int64_t* to, const int32_t* bt,
+                            int32_t max_requests, int32_t max_blocks) {
+    if (!p || p->imported) return fail(KVX_EINVAL, "append needs a local pool");
+    if (n < 0 || (n > 0 && (!req || !from || !to || !bt))) return fail(KVX_EINVAL, "null arrays");
+    int64_t max_tok = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (req[i] < 0 || req[i] >= max_requests || from[i] < 0 || to[i] < from[i])
+            return fail(KVX_EINVAL, "bad append entry");
+        if (cdiv64(to[i], p->g.block_tokens) > max_blocks) return fail(KVX_EINVAL, "tokens exceed max_blocks");
+        for (int64_t b = from[i] / p->g.block_tokens; b < cdiv64(to[i], p->g.block_tokens); ++b) {
+            const int32_t id = bt[(int64_t)req[i] * max_blocks + b];
+            if (id < 0 || id >= p->num_blocks) return fail(KVX_EINVAL, "block id out of pool range");
+        }
+        max_tok = std::max(max_tok, to[i]);
+    }
+    if (n == 0 || max_tok == 0) return KVX_OK;
+    DeviceGuard dg(p->device);
+    kvx::Arena& A = kvx::Arena::of(p->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // one scratch region [req | from | to | bt], freed after the stream passes it
+    const size_t o_from = ((sizeof(int32_t) * (size_t)n) + 15) & ~size_t(15);
+    const size_t o_to = o_from + sizeof(int64_t) * (size_t)n;
+    const size_t o_bt = o_to + sizeof(int64_t) * (size_t)n;
+    const size_t bytes = o_bt + sizeof(int32_t) * (size_t)max_requests * (size_t)max_blocks;
+    void *d = nullptr, *h = nullptr;
+    KVX_CUDA(A.dev_alloc(&d, bytes));
+    KVX_CUDA(A.host_alloc(&h, bytes));
+    char* hc = static_cast<char*>(h);
+    std::memcpy(hc, req, sizeof(int32_t) * (size_t)n);
+    std::memcpy(hc + o_from, from, sizeof(int64_t) * (size_t)n);
+    std::memcpy(hc + o_to, to, sizeof(int64_t) * (size_t)n);
+    std::memcpy(hc + o_bt, bt, bytes - o_bt);
+    KVX_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+    char* dc = static_cast<char*>(d);
+    dim3 grid((unsigned)n, (unsigned)cdiv64(max_tok, p->g.block_tokens));
+    kvx::kvx_fill_kernel<<<grid, 256, 0, st>>>(p->base, p->num_blocks, first_layer, p->num_layers,
+                                               reinterpret_cast<const int32_t*>(dc),
+                                               reinterpret_cast<const int64_t*>(dc + o_to),
+                                               reinterpret_cast<const int32_t*>(dc + o_bt), max_blocks,
+                                               p->g.block_tokens, token_bytes(p->g), seed,
+                                               reinterpret_cast<const int64_t*>(dc + o_from));
+    KVX_LAUNCHED();
+    KVX_CUDA(cudaLaunchHostFunc(st, release_pieces, new PieceRelease{p->device, d, h, bytes}));
     return KVX_OK;
 }
 
@@ -971,21 +1034,6 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
     return KVX_OK;
 }
 
-namespace {
-struct PieceRelease {  // returns a call's descriptor buffers to the arena once the stream passed them
-    int device;
-    void* d;
-    void* h;
-    size_t bytes;
-};
-void CUDART_CB release_pieces(void* arg) {
-    auto* r = static_cast<PieceRelease*>(arg);
-    kvx::Arena& A = kvx::Arena::of(r->device);
-    A.dev_free(r->d, r->bytes);
-    A.host_free(r->h, r->bytes);
-    delete r;
-}
-}  // namespace
 
 int kvx_weights_migrate(int32_t device, void* stream, int32_t num_layers, uint64_t layer_bytes,
                         int32_t old_stages, const int32_t* old_boundaries, void* const* old_ptrs,

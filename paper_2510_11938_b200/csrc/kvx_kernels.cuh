@@ -560,26 +560,33 @@ kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ k
 // ---------------------------------------------------- payload kernels
 // grid = (entries, max logical blocks); one CTA per (request, logical block),
 // looping over the pool's layers and the block's K/V token rows.
+// from == nullptr: tokens [0, tokens[i]); else [from[i], tokens[i]) (decode appends).
 __global__ void __launch_bounds__(256)
 kvx_fill_kernel(char* __restrict__ pool, int32_t pool_blocks, int32_t first_layer,
                 int32_t num_layers, const int32_t* __restrict__ req,
                 const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
-                int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed) {
+                int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed,
+                const int64_t* __restrict__ from = nullptr) {
     const int32_t i = blockIdx.x, b = blockIdx.y;
     const int32_t r = req[i];
-    const int64_t t_begin = (int64_t)b * block_tokens;
+    int64_t t_begin = (int64_t)b * block_tokens;
     if (t_begin >= tokens[i]) return;
     const int64_t t_end = min(tokens[i], t_begin + block_tokens);
+    if (from) {
+        if (t_end <= from[i]) return;
+        t_begin = max(t_begin, from[i]);
+    }
     const int32_t blk = bt[(int64_t)r * max_blocks + b];
     const uint64_t block_bytes = 2ull * block_tokens * token_bytes;
     const uint32_t vecs = (uint32_t)(token_bytes >> 4);
     const int32_t rows = (int32_t)(t_end - t_begin);
+    const int32_t row0 = (int32_t)(t_begin - (int64_t)b * block_tokens);  // first row inside the block
     for (int32_t l = 0; l < num_layers; ++l) {
         char* slab = pool + ((uint64_t)l * pool_blocks + blk) * block_bytes;
         for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
             const int32_t kvi = kvr / rows, t = kvr % rows;
             const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
-            uint4* row = reinterpret_cast<uint4*>(slab + ((uint64_t)kvi * block_tokens + t) * token_bytes);
+            uint4* row = reinterpret_cast<uint4*>(slab + ((uint64_t)kvi * block_tokens + row0 + t) * token_bytes);
             for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) row[v] = pattern_vec(th, v);
         }
     }

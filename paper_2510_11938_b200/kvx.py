@@ -127,6 +127,7 @@ def _load() -> C.CDLL:
         "kvx_pool_read": (C.c_int, [VP, U64, U64, VP]),
         "kvx_pool_write": (C.c_int, [VP, U64, U64, VP]),
         "kvx_pool_fill_pattern": (C.c_int, [VP, U64, I32, I32, P(I32), P(I64), P(I32), I32, I32]),
+        "kvx_pool_append_pattern": (C.c_int, [VP, VP, U64, I32, I32, P(I32), P(I64), P(I64), P(I32), I32, I32]),
         "kvx_bm_create": (C.c_int, [I32, I32, P(VP)]),
         "kvx_bm_reset": (C.c_int, [VP]),
         "kvx_bm_free_count": (C.c_int, [VP, P(I32)]),
@@ -286,6 +287,14 @@ class Pool:
         bt = _i32(block_table)
         _check(_lib.kvx_pool_fill_pattern(self._h, seed, first_layer, len(req), _p32(req),
                                           _p64(tokens), _p32(bt), bt.shape[0], bt.shape[1]))
+
+    def append_pattern(self, seed: int, first_layer: int, req, frm, to, block_table: np.ndarray,
+                       stream: int = 0) -> None:
+        """Decode appends [frm, to) per request, asynchronous on `stream`."""
+        req, frm, to = _i32(req), _i64(frm), _i64(to)
+        bt = _i32(block_table)
+        _check(_lib.kvx_pool_append_pattern(self._h, stream or None, seed, first_layer, len(req), _p32(req),
+                                            _p64(frm), _p64(to), _p32(bt), bt.shape[0], bt.shape[1]))
 
     def close(self) -> None:
         if self._h is not None and self._h.value:
