@@ -30,7 +30,7 @@ def cpu_worker(rank, world, port, out):
         t = scn.transitions[0]
         L = scn.num_layers
         res = {}
-        for mode in ("affinity", "disjoint"):
+        for mode in ("affinity", "disjoint", "spread"):
             old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, world, mode)
             mine = S.layers_of_rank(L, t.old_boundaries, old_dev, rank)
             every = [None] * world

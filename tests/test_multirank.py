@@ -26,19 +26,24 @@ def _run(target, world, *args, timeout=600):
     return {r: p for r, (_, p) in res.items()}
 
 
-def test_two_ranks_shard_every_layer_once_cpu():
-    res = _run(mgpu_worker.cpu_worker, 2)
-    for mode in ("affinity", "disjoint"):
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_ranks_shard_every_layer_once_cpu(world):
+    res = _run(mgpu_worker.cpu_worker, world)
+    for mode in ("affinity", "disjoint", "spread"):
         every, handles, old_dev, new_dev = res[0][mode]
-        assert res[1][mode][0] == every  # both ranks agree on the sharding
+        for r in range(1, world):
+            assert res[r][mode][0] == every  # every rank agrees on the sharding
         flat = sorted(l for layers in every for l in layers)
         assert flat == list(range(40))   # each layer moved by exactly one rank
         owners = {j for hs in handles for j in hs}
         assert owners == set(range(4))   # every new stage exported by its owner
+        assert all(0 <= d < world for d in old_dev + new_dev)
     _, _, old_dev, new_dev = res[0]["affinity"]
-    assert old_dev == [0, 0, 0, 0, 1, 1, 1, 1] and new_dev == [0, 0, 1, 1]
-    _, _, old_dev, new_dev = res[0]["disjoint"]
-    assert new_dev == [1, 1, 0, 0]
+    if world == 2:
+        assert old_dev == [0, 0, 0, 0, 1, 1, 1, 1] and new_dev == [0, 0, 1, 1]
+        assert res[0]["disjoint"][3] == [1, 1, 0, 0]
+    if world == 8:
+        assert old_dev == list(range(8)) and new_dev == [0, 2, 4, 6]   # half of each stage crosses NVLink
 
 
 @pytest.mark.gpu
