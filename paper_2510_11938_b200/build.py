@@ -16,8 +16,8 @@ PKG = os.path.join(ROOT, "paper_2510_11938_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libkvx.so")
-SOURCES = ["kvx.cu", "kvx_ctl.cpp"]
-HEADERS = ["kvx_kernels.cuh", "kvx_internal.h", "kvx_arena.h"]
+SOURCES = ["kvx_common.cu", "kvx_pool.cu", "kvx_transition.cu", "kvx_extras.cu", "kvx_ctl.cpp"]
+HEADERS = ["kvx_kernels.cuh", "kvx_internal.h", "kvx_arena.h", "kvx_common.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall",

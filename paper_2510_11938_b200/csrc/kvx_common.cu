@@ -1,0 +1,45 @@
+// kvx_common.cu -- library-wide state: the thread-local error message, the
+// launch counter, version / device queries and the hooks kvx_ctl.cpp uses.
+#include "kvx_common.h"
+
+namespace kvx_host {
+std::string& last_error() {
+    thread_local std::string msg;
+    return msg;
+}
+std::atomic<uint64_t>& launches() {
+    static std::atomic<uint64_t> n{0};
+    return n;
+}
+}  // namespace kvx_host
+
+using namespace kvx_host;
+
+extern "C" {
+
+const char* kvx_last_error(void) { return last_error().c_str(); }
+int kvx_abi_version(void) { return KVX_ABI_VERSION; }
+uint64_t kvx_launch_count(void) { return launches().load(); }
+
+int kvx_device_count(int32_t* out) {
+    if (!out) return fail(KVX_EINVAL, "out is null");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = 0;
+        return fail(KVX_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    *out = n;
+    return KVX_OK;
+}
+
+}  // extern "C"
+
+// ----------------------------------------------- hooks for kvx_ctl.cpp
+namespace kvx {
+CtlState& ctl_of(kvx_transition* t) { return t->ctl; }
+const CtlState& ctl_of(const kvx_transition* t) { return t->ctl; }
+uint64_t epoch_of(const kvx_transition* t) { return t->epoch; }
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace kvx

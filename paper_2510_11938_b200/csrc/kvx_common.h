@@ -1,0 +1,221 @@
+// kvx_common.h -- internal to the kvx library: the opaque handle types of
+// include/kvx.h, error/launch bookkeeping and the small host helpers shared by
+// the translation units (kvx_pool.cu, kvx_transition.cu, kvx_extras.cu,
+// kvx_common.cu).  Device code lives in kvx_kernels.cuh.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kvx.h"
+#include "kvx_arena.h"
+#include "kvx_internal.h"
+#include "kvx_kernels.cuh"
+
+namespace kvx_host {
+
+std::string& last_error();          // thread-local message (kvx_common.cu)
+std::atomic<uint64_t>& launches();   // process-wide launch counter
+
+inline int fail(int code, const std::string& msg) {
+    last_error() = msg;
+    return code;
+}
+
+#define KVX_CUDA(call)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return kvx_host::fail(KVX_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+    } while (0)
+
+#define KVX_LAUNCHED()                                                                    \
+    do {                                                                                  \
+        kvx_host::launches().fetch_add(1, std::memory_order_relaxed);                               \
+        cudaError_t e_ = cudaGetLastError();                                              \
+        if (e_ != cudaSuccess)                                                            \
+            return kvx_host::fail(KVX_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Restores the caller's current device (torch keeps its own notion of it).
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+inline bool geometry_ok(const kvx_geometry* g, std::string* why) {
+    if (!g) return *why = "geometry is null", false;
+    if (g->num_layers < 1 || g->num_kv_heads < 1 || g->head_dim < 1 || g->elem_bytes < 1 ||
+        g->block_tokens < 1)
+        return *why = "geometry fields must be positive", false;
+    const uint64_t tb = (uint64_t)g->num_kv_heads * g->head_dim * g->elem_bytes;
+    if (tb % 16 != 0) return *why = "token_bytes must be a multiple of 16", false;
+    return true;
+}
+
+inline uint64_t token_bytes(const kvx_geometry& g) {
+    return (uint64_t)g.num_kv_heads * (uint64_t)g.head_dim * (uint64_t)g.elem_bytes;
+}
+inline uint64_t block_bytes(const kvx_geometry& g) { return 2ull * (uint64_t)g.block_tokens * token_bytes(g); }
+
+inline int64_t cdiv64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline int stage_of_layer(const std::vector<int32_t>& b, int32_t layer) {  // modelgraph.cpp:55-62
+    int s = 0;
+    for (int32_t cut : b) {
+        if (layer < cut) break;
+        ++s;
+    }
+    return s;
+}
+inline int stage_begin(const std::vector<int32_t>& b, int s) { return s == 0 ? 0 : b[(size_t)s - 1]; }
+
+inline bool plan_ok(const kvx_plan& p, int32_t L, std::string* why, std::vector<int32_t>* out) {
+    if (p.num_stages < 1 || p.num_stages > L) return *why = "num_stages out of range", false;
+    out->assign(p.boundaries, p.boundaries + (p.num_stages - 1));
+    int32_t prev = 0;
+    for (int32_t b : *out) {
+        if (b <= prev || b >= L) return *why = "boundaries must be strictly increasing in (0, L)", false;
+        prev = b;
+    }
+    if (!p.pools) return *why = "plan pools array is null", false;
+    return true;
+}
+
+
+struct PieceRelease {  // returns a call's descriptor buffers to the arena once the stream passed them
+    int device;
+    void* d;
+    void* h;
+    size_t bytes;
+};
+inline void CUDART_CB release_pieces(void* arg) {
+    auto* r = static_cast<PieceRelease*>(arg);
+    kvx::Arena& A = kvx::Arena::of(r->device);
+    A.dev_free(r->d, r->bytes);
+    A.host_free(r->h, r->bytes);
+    delete r;
+}
+
+// (ring depth, chunk bytes) of the TMA bulk mover; KVX_BULK_CFG=<index> pins one.
+using BulkFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, uint64_t, int32_t,
+                        int32_t, int32_t);
+struct BulkVariant {
+    int stages;
+    uint32_t chunk;
+    BulkFn fn;
+};
+inline const BulkVariant kBulkVariants[] = {
+    {6, 32768, kvx::kvx_bulk_kernel<6, 32768>},  {4, 49152, kvx::kvx_bulk_kernel<4, 49152>},
+    {3, 65536, kvx::kvx_bulk_kernel<3, 65536>},  {12, 16384, kvx::kvx_bulk_kernel<12, 16384>},
+    {3, 32768, kvx::kvx_bulk_kernel<3, 32768>},  {8, 16384, kvx::kvx_bulk_kernel<8, 16384>},
+    {2, 65536, kvx::kvx_bulk_kernel<2, 65536>},  {4, 16384, kvx::kvx_bulk_kernel<4, 16384>},
+};
+constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
+
+}  // namespace kvx_host
+
+// ------------------------------------------------- opaque handle types
+struct kvx_pool {
+    int32_t device = -1;
+    bool imported = false;
+    bool wrapped = false;  // caller-owned memory
+    char* base = nullptr;
+    uint64_t bytes = 0;
+    kvx_geometry g{};
+    int32_t num_layers = 0;
+    int32_t num_blocks = 0;
+};
+
+// Device-resident block manager: a free-id stack on the GPU, its top mirrored
+// on the host so every capacity decision is synchronous and deterministic.
+struct kvx_blockmgr {
+    int32_t device = -1;
+    int32_t capacity = 0;
+    int32_t top = 0;          // free blocks (host mirror of the device stack top)
+    int32_t* d_stack = nullptr;
+};
+
+struct kvx_transition {
+    kvx_geometry g{};
+    int32_t device = -1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    int num_sms = 0;
+    int move_ctas_per_sm = 1;
+    int bulk_ctas[16] = {};  // resident CTAs per SM of each bulk variant
+    int bulk_variant = -1;   // -1: chosen per wave from the average run size
+    bool use_bulk = false;   // TMA bulk mover for local destinations
+    bool peer_bulk = false;  // ... and for peer (NVLink) destinations
+    std::vector<int32_t> old_b, new_b;
+    std::vector<kvx_pool*> old_pools, new_pools;
+    int32_t max_requests = 0, max_blocks = 0, dst_num_blocks = 0;
+    kvx_blockmgr* bm = nullptr;  // destination block manager (NULL: bump rule)
+    uint64_t epoch = 0;
+    enum State { kActive, kCommitPending, kCommitted, kAborted } state = kActive;
+
+    // device state
+    int32_t* d_src_bt = nullptr;
+    int32_t* d_dst_bt = nullptr;
+    int64_t* d_synced_hi = nullptr;
+    kvx::LayerPtr* d_layers = nullptr;
+    int32_t n_local_layers = 0;
+    int32_t n_peer_layers = 0;  // layers [0, n_peer_layers) of d_layers push to a peer
+    bool has_peer_dst = false;
+    // wave staging: pinned host ring of 2 + device buffer
+    char* h_wave[2] = {nullptr, nullptr};
+    cudaEvent_t h_wave_free[2] = {nullptr, nullptr};
+    int wave_slot = 0;
+    char* d_wave = nullptr;
+    kvx::Seg* d_segs = nullptr;
+    int64_t seg_cap = 0;
+    // commit scratch
+    uint8_t* d_live = nullptr;
+    int32_t* d_commit_i32 = nullptr;  // row_ptr | blocks | free_list
+    int64_t commit_i32_cap = 0;
+    size_t bt_bytes = 0, wave_bytes = 0, layers_bytes = 0;
+    int64_t* d_commit_out = nullptr;
+    // pinned landing zone of an async commit: [int64 x4 | row_ptr | blocks | free]
+    char* h_commit = nullptr;
+    size_t h_commit_bytes = 0;
+    cudaEvent_t ev_commit = nullptr;
+    int32_t pend_n_live = 0;
+    int64_t pend_nb_live = 0, pend_nb_free = 0;
+    // timing
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+    bool timing_open = false;
+    // one (start, end) event pair per move-kernel launch of this handle
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> move_ev;
+    std::vector<uint64_t> move_bytes;
+
+    // activation handoff pieces (grown on demand, freed at destroy)
+    kvx::Piece* d_pieces = nullptr;
+    kvx::Piece* h_pieces = nullptr;
+    int64_t piece_cap = 0;
+    cudaEvent_t pieces_free = nullptr;
+
+    // host mirror of the destination rule (capacity checks are synchronous)
+    std::vector<int64_t> synced_hi;
+    std::vector<int32_t> src_bt;  // host copy: every wave's source blocks must be backed
+    int32_t alloc = 0;
+    uint64_t bytes_moved = 0;       // by this handle (local-source layers)
+    uint64_t bytes_all_layers = 0;  // reference-accounted, all layers
+
+    kvx::CtlState ctl;  // control-plane mirror (kvx_ctl.cpp)
+};
+

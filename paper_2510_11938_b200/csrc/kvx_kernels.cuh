@@ -21,6 +21,8 @@
 //                      rows that are no longer live (ballot + prefix scan).
 //   kvx_fill_kernel / kvx_verify_kernel   synthetic payload (test + bench).
 #pragma once
+// Included by several translation units: non-template kernels have internal
+// linkage (static), templates are instantiated where used.
 
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -113,7 +115,7 @@ constexpr int kPlanThreads = 1024;
 // so rows never collide.  Destination rule: the new blocks of a request are
 // logical blocks [ceil(synced_hi/B), ceil(hi/B)); their ids are the bump
 // pointer plus the exclusive scan of the per-entry counts, in entry order.
-__global__ void __launch_bounds__(kPlanThreads, 1)
+static __global__ void __launch_bounds__(kPlanThreads, 1)
 kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
                 const int64_t* __restrict__ hi, int32_t n, const int32_t* __restrict__ src_bt,
                 int32_t* __restrict__ dst_bt, int64_t* __restrict__ synced_hi, int32_t max_blocks,
@@ -165,7 +167,7 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
 }
 
 // Block-manager helper: stack[i] = capacity - 1 - i (pops yield 0, 1, 2, ...).
-__global__ void kvx_bm_init_kernel(int32_t* __restrict__ stack, int32_t capacity) {
+static __global__ void kvx_bm_init_kernel(int32_t* __restrict__ stack, int32_t capacity) {
     for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < capacity; i += gridDim.x * blockDim.x)
         stack[i] = capacity - 1 - i;
 }
@@ -205,7 +207,7 @@ __device__ __forceinline__ void cta_copy(uint4* __restrict__ dst, const uint4* _
 // Work unit u -> (layer = u / nseg, segment = u % nseg): consecutive CTAs walk
 // consecutive destination blocks of one layer (the dense rule makes them
 // contiguous), sources are wherever the old block table points.
-__global__ void __launch_bounds__(kMoveThreads)
+static __global__ void __launch_bounds__(kMoveThreads)
 kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
                 int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
                 int32_t fence_system) {
@@ -493,7 +495,7 @@ constexpr int kCommitThreads = 1024;
 // Phase A (this kernel, one CTA): live flags, Eq. 10 violations, CSR row
 // pointers and free-list offsets; phase B writes the blocks (same kernel,
 // after the scans).  live_flag is a scratch [max_requests] array.
-__global__ void __launch_bounds__(kCommitThreads, 1)
+static __global__ void __launch_bounds__(kCommitThreads, 1)
 kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ kv, int32_t n,
                   const int32_t* __restrict__ dst_bt, const int64_t* __restrict__ synced_hi,
                   uint8_t* __restrict__ live_flag, int32_t max_requests, int32_t max_blocks,
@@ -561,7 +563,7 @@ kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ k
 // grid = (entries, max logical blocks); one CTA per (request, logical block),
 // looping over the pool's layers and the block's K/V token rows.
 // from == nullptr: tokens [0, tokens[i]); else [from[i], tokens[i]) (decode appends).
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
 kvx_fill_kernel(char* __restrict__ pool, int32_t pool_blocks, int32_t first_layer,
                 int32_t num_layers, const int32_t* __restrict__ req,
                 const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
@@ -592,7 +594,7 @@ kvx_fill_kernel(char* __restrict__ pool, int32_t pool_blocks, int32_t first_laye
     }
 }
 
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
 kvx_verify_kernel(const char* __restrict__ pool, int32_t pool_blocks, int32_t first_layer,
                   int32_t num_layers, const int32_t* __restrict__ req,
                   const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
