@@ -715,14 +715,14 @@ def main():
         traffic, traffic_src = ncu_traffic(args.config)
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": "kvx_move_kernel (wave 0)", "bytes_per_launch": w0_bytes,
+                "kernel": "kvx_bulk_kernel<3,64K> (wave 0, TMA bulk mover)", "bytes_per_launch": w0_bytes,
                 "launch_ms": round(w0_avg, 4), "peak_source": peak_kind}
     else:
         frac = t_roof * 1e3 / w0_avg
         bound = "nvlink" if max(out + inn) / nvl_peak > max(hbm) / peak else "hbm"
         roof = {"bound": bound, "achieved": round(frac * (peak if bound == "hbm" else nvl_peak), 1),
                 "peak": peak if bound == "hbm" else nvl_peak, "unit": "GB/s", "frac": round(frac, 4),
-                "traffic": None, "kernel": "kvx_move_kernel (wave 0, slowest rank)",
+                "traffic": None, "kernel": "kvx_bulk_kernel (wave 0, slowest rank)",
                 "t_roof_ms": round(t_roof * 1e3, 4), "launch_ms": round(w0_avg, 4),
                 "peak_source": f"hbm {peak_kind}; nvlink 770 GB/s measured peer copy"}
 

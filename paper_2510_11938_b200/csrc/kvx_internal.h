@@ -1,4 +1,4 @@
-// kvx_internal.h -- shared between kvx.cu (data plane) and kvx_ctl.cpp
+// kvx_internal.h -- shared between the data plane (kvx_*.cu) and kvx_ctl.cpp
 // (control-plane mirror).  Not part of the public ABI.
 #pragma once
 
