@@ -763,11 +763,14 @@ def main():
         "move_kernel_ms_per_step": round(all_move_ms / K, 4), "move_ms_by_wave": wave_ms,
         "mover": os.environ.get("KVX_MOVE_IMPL", "bulk") + ":" + os.environ.get("KVX_BULK_CFG", "auto"),
     }
+    sim = plan.t.simulated_stall_ms()
+    line["stall_reference_simulated_ms"] = round(sim, 3) if sim is not None else None
     if n_gpus == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         gbs, desc, _ = cpu_sample_run(plan, 3, 1, threads)
+        gbs1, desc1, _ = cpu_sample_run(plan, 2, 1, 1, target_bytes=0.25e9)
         line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                                "sample": desc,
+                                "sample": desc, "value_1_thread": round(gbs1, 3), "sample_1_thread": desc1,
                                 "reference_control_plane": reference_control_plane(plan.golden)}
     print(json.dumps(line), flush=True)
     if world > 1:

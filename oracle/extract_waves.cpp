@@ -214,6 +214,7 @@ struct Observer {
                 j["kind"] = "barrier";
                 j["instance"] = inst.id;
                 j["t_ms"] = t_ms;
+                j["barrier_ms"] = prev_dispatch_ms;  // time of the handler that set it
                 j["epoch"] = inst.epoch;
                 j["rounds"] = ctx.rounds;
                 j["inflight_batches"] = inst.inflight_batches;
@@ -252,9 +253,11 @@ struct Observer {
     }
 
     std::map<std::int64_t, double> begin_ms;  // time of the last RefactorBegin per instance
+    double prev_dispatch_ms = 0.0;            // event time of the handler that just ran
 
     void before(const SimEvent& ev) {
         observe(ev.time_ms);
+        prev_dispatch_ms = ev.time_ms;
         if (ev.kind == EventKind::RefactorBegin) begin_ms[ev.instance_id] = ev.time_ms;
         if (ev.kind == EventKind::RefactorCommit) {
             auto& inst = *e->instances_[static_cast<std::size_t>(ev.instance_id)];

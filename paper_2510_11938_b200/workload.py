@@ -61,6 +61,7 @@ class Barrier:
     req: np.ndarray
     kv: np.ndarray
     microbatches: list = field(default_factory=list)
+    barrier_ms: float = 0.0
 
 
 @dataclass
@@ -84,6 +85,15 @@ class TransitionSpec:
     live_kv: Optional[np.ndarray] = None
     violations: Optional[int] = None
     kv_synced_bytes_total: Optional[float] = None
+    commit_ms: Optional[float] = None
+
+    def simulated_stall_ms(self) -> Optional[float]:
+        """The reference's own stall for this transition: barrier -> commit in
+        simulated time (engine.cpp:676 -> 686), drain and load waits included."""
+        bars = [e for e in self.events if isinstance(e, Barrier)]
+        if not bars or self.commit_ms is None:
+            return None
+        return self.commit_ms - bars[0].barrier_ms
 
     def live_kv_map(self, max_requests: int) -> np.ndarray:
         """kv_tokens at commit per request id (0 for requests not live)."""
@@ -143,11 +153,13 @@ def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
             mbs = [MicroBatchRec(m["batch"], m["where"], m["after"], int(sum(u[2] for u in m["units"])),
                                  m["act_bytes"]) for m in r.get("microbatches", [])]
             cur[r["instance"]].events.append(Barrier(r["rounds"], r["inflight_batches"],
-                                                     e[:, 0].astype(np.int32), e[:, 1].copy(), mbs))
+                                                     e[:, 0].astype(np.int32), e[:, 1].copy(), mbs,
+                                                     r.get("barrier_ms", r["t_ms"])))
         elif k == "commit_state":
             e = np.array(r["live"], dtype=np.int64).reshape(-1, 2)
             t = cur[r["instance"]]
             t.live_req, t.live_kv = e[:, 0].astype(np.int32), e[:, 1].copy()
+            t.commit_ms = r["t_ms"]  # RefactorCommit dispatch time
         elif k in ("commit", "abort", "end_unknown"):
             t = cur.pop(r["instance"])
             t.outcome = k
