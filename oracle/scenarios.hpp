@@ -228,6 +228,27 @@ inline std::vector<Scenario> scenarios() {
         s.forced = {{300.0, 4}, {1500.0, 8}, {3000.0, 4}};
         out.push_back(s);
     }
+    {  // delta-wave rounds: a slow KV link (kv_sync_bw, engine.cpp:87-90) keeps
+       // decode ahead of every wave, so delta waves repeat (engine.cpp:665-674)
+       // until the max_sync_rounds cap (engine.hpp:75) forces the barrier.
+        Scenario s = engine_fixture({4, 8}, 4);
+        s.name = "delta_rounds_cap";
+        s.note = "slow KV link: 5 delta waves until max_sync_rounds=5 forces the barrier";
+        s.kv_sync_bw = 2.0e4;  // bytes per ms
+        s.max_sync_rounds = 5;
+        s.reqs = steady(24, 2.0, 40, 200);
+        s.forced = {{150.0, 8}};
+        out.push_back(s);
+    }
+    {
+        Scenario s = engine_fixture({4, 8}, 4);
+        s.name = "delta_rounds_converge";
+        s.note = "moderate KV link: delta waves shrink (990, 34, 1 tokens) until one finds nothing new";
+        s.kv_sync_bw = 5.0e5;
+        s.reqs = steady(24, 2.0, 40, 60);
+        s.forced = {{600.0, 8}};
+        out.push_back(s);
+    }
     return out;
 }
 

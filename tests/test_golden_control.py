@@ -99,3 +99,14 @@ def test_delta_rounds_capped():
     assert acts == [O.ACT_DELTA, O.ACT_DELTA, O.ACT_BARRIER_WAIT, O.ACT_BARRIER_WAIT]
     act, tok, lo, hi = ctx.on_sync_complete(np.array([0]), np.array([kv]), 0)
     assert act == O.ACT_FINAL and tok == kv - 12 and lo[0] == 12 and hi[0] == kv
+
+
+def test_delta_round_cap_and_convergence_pinned():
+    """engine.cpp:665-676: delta waves repeat while delta > 0 and rounds <
+    max_sync_rounds; the cap (5 here) or an empty delta drops the barrier."""
+    cap = W.load_golden("delta_rounds_cap").transitions[0]
+    assert [w.rounds for w in cap.waves] == [0, 1, 2, 3, 4, 5, 5] and cap.waves[-1].final
+    assert [e.rounds for e in cap.events if isinstance(e, W.Barrier)] == [5]
+    conv = W.load_golden("delta_rounds_converge").transitions[0]
+    assert [w.tokens for w in conv.waves][:3] == [990, 34, 1]
+    assert [e.rounds for e in conv.events if isinstance(e, W.Barrier)] == [2]

@@ -11,7 +11,8 @@ from tests.gpu_harness import SEED, GpuCase
 pytestmark = pytest.mark.gpu
 
 SMALL = [("engine_mid_decode", 2, 64), ("engine_consolidate", 2, 64), ("criterion12", 2, 64),
-         ("engine_zero_inflight", 2, 64), ("bursty_repeated", 1, 8)]
+         ("engine_zero_inflight", 2, 64), ("bursty_repeated", 1, 8), ("delta_rounds_cap", 2, 64),
+         ("delta_rounds_converge", 2, 64)]
 
 
 def _commit_and_compare(case):

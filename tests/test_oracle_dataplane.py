@@ -70,7 +70,7 @@ def test_mt_executor_matches_per_token():
 
 
 @pytest.mark.parametrize("name", ["engine_mid_decode", "engine_consolidate", "criterion12",
-                                  "bursty_repeated"])
+                                  "bursty_repeated", "delta_rounds_cap", "delta_rounds_converge"])
 def test_golden_transitions_bytes(name):
     """Every golden transition, replayed through the oracle control plane and
     executed by the oracle data plane: destination bytes equal the pattern of
