@@ -626,8 +626,10 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = float(te.item())
 
-    # ---- stage-boundary activation handoff of the barrier's in-flight
-    #      micro-batches (alternative to the drain; hidden 5120 x fp16 rows)
+    # ---- drain-free stall: at the reference's barrier the
+    #      in-flight micro-batches are handed to their new owners (hidden x
+    #      fp16 rows) instead of drained, the final wave goes out at once over
+    #      the barrier's live set, then commit.  Device time barrier -> commit.
     handoff = None
     bar = next((e for e in t.events if isinstance(e, W.Barrier) and e.microbatches), None)
     if bar is not None:
@@ -636,28 +638,46 @@ def main():
                 for m in bar.microbatches]
         cap = sum(m.tokens * row + 256 for m in bar.microbatches) + 256
         arenas = [torch.zeros(cap, dtype=torch.uint8, device=dev) for _ in range(len(t.new_boundaries) + 1)]
-        htimes = []
+        htimes, stimes = [], []
         for rep in range(6):
             tr = make()
-            tr.begin_refactor((t.waves[0].req, t.waves[0].hi))
+            tr.set_handoff(True)
+            w0 = t.waves[0]
+            tr.begin_refactor((w0.req, w0.hi))
+            for e in t.events[1:]:  # delta waves before the barrier, as the reference ran them
+                if isinstance(e, W.Barrier):
+                    break
+                tr.on_kv_sync_complete((e.req, e.hi), 1)
+            if world > 1:
+                dist.barrier()
             torch.cuda.synchronize(dev)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            slots = tr.handoff(row, [(m.batch, m.after, m.tokens, s.data_ptr())
-                                     for m, s in zip(bar.microbatches, srcs)],
+            a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a0.record(stream)
+            act, _ = tr.on_kv_sync_complete((bar.req, bar.kv), bar.inflight_batches)
+            assert act == kvx.ACT_FINAL, act
+            slots = tr.handoff(row, [(m.batch, m.after, m.tokens, s_.data_ptr())
+                                     for m, s_ in zip(bar.microbatches, srcs)],
                                [x.data_ptr() for x in arenas], [cap] * len(arenas))
-            b.record(stream)
+            a1.record(stream)
+            res = tr.on_refactor_commit((bar.req, bar.kv))
+            a2.record(stream)
             torch.cuda.synchronize(dev)
+            assert res.violations == 0
             if rep > 0:
-                htimes.append(a.elapsed_time(b))
-            tr.abort()
+                htimes.append(a0.elapsed_time(a1))
+                stimes.append(a0.elapsed_time(a2))
             tr.close()
         hbytes = sum(sl[4] for sl in slots)
-        hms = statistics.median(htimes)
-        handoff = {"batches": len(bar.microbatches), "bytes": int(hbytes), "ms": round(hms, 4),
-                   "GB_s": round(hbytes / (hms * 1e-3) / 1e9, 1),
-                   "note": "in-flight micro-batches of the reference's barrier moved to their new "
-                           "owners instead of drained (hidden x fp16 rows)"}
+        hms, sms = statistics.median(htimes), statistics.median(stimes)
+        if world > 1:
+            tt = torch.tensor([hms, sms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            hms, sms = [float(x) for x in tt.tolist()]
+        handoff = {"batches": len(bar.microbatches), "bytes": int(hbytes),
+                   "final_wave_plus_handoff_ms": round(hms, 4), "stall_handoff_ms": round(sms, 4),
+                   "note": "drain-free mode: in-flight micro-batches of the reference's barrier moved "
+                           "to their new owners (hidden x fp16 rows), final wave over the barrier's "
+                           "live set, commit; device time barrier -> commit result on host"}
 
     # ---- stage weight migration: the new stages' parameters
     #      gathered by layer range on the device (N=1; fp16 weights of the shape)

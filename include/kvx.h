@@ -310,6 +310,12 @@ int kvx_ctl_commit_async(kvx_transition* t, uint64_t epoch, int32_t n, const int
                          const int64_t* kv);
 int kvx_ctl_commit_collect(kvx_transition* t, kvx_commit_result* out);
 int kvx_ctl_state_get(const kvx_transition* t, kvx_ctl_state* out);
+/* Handoff mode: at the barrier the caller hands the in-flight micro-batches
+ * to the new pipeline (kvx_handoff) instead of draining them, so the final
+ * wave is issued at once -- the wait on inflight_batches (engine.cpp:678) is
+ * dropped and the drain leaves the stall.  Off by default (reference
+ * semantics). */
+int kvx_ctl_set_handoff(kvx_transition* t, int32_t enable);
 
 #ifdef __cplusplus
 }

@@ -107,7 +107,9 @@ int kvx_ctl_sync_complete(kvx_transition* t, uint64_t epoch, int32_t n, const in
         }
         c.barrier = true;  // engine.cpp:676
     }
-    if (c.commit_scheduled || inflight_batches > 0) {  // engine.cpp:678
+    // engine.cpp:678 -- unless the in-flight micro-batches are handed off to
+    // the new pipeline (kvx_handoff) instead of drained on the old one
+    if (c.commit_scheduled || (inflight_batches > 0 && !c.handoff)) {
         if (action_out) *action_out = KVX_ACT_BARRIER_WAIT;
         return KVX_OK;
     }
@@ -156,6 +158,12 @@ int kvx_ctl_commit(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* 
     const int rc = kvx_ctl_commit_async(t, epoch, n, req, kv);
     if (rc != KVX_OK) return rc;
     return kvx_ctl_commit_collect(t, out);
+}
+
+int kvx_ctl_set_handoff(kvx_transition* t, int32_t enable) {
+    if (!t) return kvx::set_error(KVX_EINVAL, "transition is null");
+    kvx::ctl_of(t).handoff = enable != 0;
+    return KVX_OK;
 }
 
 int kvx_ctl_state_get(const kvx_transition* t, kvx_ctl_state* out) {

@@ -27,6 +27,7 @@ struct CtlState {
     double kv_synced_bytes = 0.0;
     int64_t last_wave_tokens = 0;
     int64_t host_violations = 0;    // Eq. 10 on the mirror, checked against the device at collect
+    bool handoff = false;           // in-flight batches are handed off, not drained
 
     void init(int32_t max_requests, int32_t max_rounds, double bpt) {
         synced.assign((size_t)max_requests, 0);

@@ -158,6 +158,7 @@ def _load() -> C.CDLL:
         "kvx_commit_async": (C.c_int, [VP, U64, I32, P(I32), P(I64)]),
         "kvx_commit_collect": (C.c_int, [VP, P(_CommitResult)]),
         "kvx_ctl_state_get": (C.c_int, [VP, P(_CtlState)]),
+        "kvx_ctl_set_handoff": (C.c_int, [VP, I32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -521,6 +522,10 @@ class Transition:
     def abort_refactor(self) -> None:
         """engine.cpp:759-772."""
         self.abort()
+
+    def set_handoff(self, enable: bool = True) -> None:
+        """Hand in-flight micro-batches off at the barrier instead of draining."""
+        _check(_lib.kvx_ctl_set_handoff(self._h, 1 if enable else 0))
 
     def ctl_state(self) -> dict:
         s = _CtlState()

@@ -16,7 +16,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("scenario,commits,aborts", [("criterion12", 2, 0), ("consolidate", 1, 0),
-                                                     ("revoke", 0, 1)])
+                                                     ("revoke", 0, 1), ("delta_rounds_cap", 1, 0),
+                                                     ("bursty_repeated", 2, 0)])
 def test_reference_engine_drives_kvx(gpu_count, scenario, commits, aborts):
     assert os.path.exists(BIN), "build it with __graft_entry__.build() (needs the reference sources)"
     out = subprocess.run([BIN, scenario], capture_output=True, text=True, timeout=600)

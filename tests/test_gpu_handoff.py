@@ -6,7 +6,8 @@ import pytest
 
 from oracle import pyoracle as O
 from paper_2510_11938_b200 import workload as W
-from tests.gpu_harness import GpuCase
+from paper_2510_11938_b200 import kvx
+from tests.gpu_harness import SEED, GpuCase
 from tests.test_handoff_oracle import CASES
 
 pytestmark = pytest.mark.gpu
@@ -41,5 +42,46 @@ def test_handoff_bit_exact(gpu_count, name, ti, t, b):
                 got = arenas[k][o:o + nbytes].cpu().numpy()
                 want = srcs[i][:nbytes].cpu().numpy()
                 assert np.array_equal(got, want), f"batch {bid} differs"
+    finally:
+        case.close()
+
+
+@pytest.mark.parametrize("name", ["llama13b_8to4", "engine_consolidate", "delta_rounds_cap"])
+def test_handoff_mode_commits_at_the_barrier(gpu_count, name):
+    """kvx_ctl_set_handoff: the barrier decision issues the final wave at once
+    (no drain); the data plane over the barrier's live set is the oracle's
+    (control replayed with inflight = 0) and the payload checks out."""
+    scn = W.load_golden(name)
+    t = scn.transitions[0]
+    L, H, D = W.shape_for(scn)
+    case = GpuCase(scn, t, H if name.startswith("llama") else 2, D if name.startswith("llama") else 64,
+                   oracle_pools=False)
+    try:
+        octx = O.ControlCtx(case.N, scn.max_sync_rounds, scn.kv_bytes_per_token)
+        tr = case.tr
+        tr.set_handoff(True)
+        w0 = t.waves[0]
+        tr.begin_refactor((w0.req, w0.hi))
+        r = octx.begin(w0.req, w0.hi)
+        assert case.dp.wave(w0.req, r[1], r[2]) == 0
+        for e in t.events[1:]:
+            if isinstance(e, W.Barrier):
+                bar = e
+                break
+            act, _ = tr.on_kv_sync_complete((e.req, e.hi), 1)
+            r = octx.on_sync_complete(e.req, e.hi, 1)
+            assert act == r[0] == kvx.ACT_DELTA
+            assert case.dp.wave(e.req, r[2], r[3]) == 0
+        assert bar.inflight_batches > 0
+        act, tok = tr.on_kv_sync_complete((bar.req, bar.kv), bar.inflight_batches)
+        r = octx.on_sync_complete(bar.req, bar.kv, 0)      # handed off == nothing left in flight
+        assert act == r[0] == kvx.ACT_FINAL and tok == r[1]
+        assert case.dp.wave(bar.req, r[2], r[3]) == 0
+        res = tr.on_refactor_commit((bar.req, bar.kv))
+        v, row_ptr, blocks, free = case.dp.commit(bar.req, bar.kv)
+        assert res.violations == v == 0
+        np.testing.assert_array_equal(res.blocks, blocks)
+        np.testing.assert_array_equal(tr.dst_block_table(), case.dp.bt)
+        assert tr.verify_pattern(SEED, bar.req, bar.kv) == 0
     finally:
         case.close()
