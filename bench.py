@@ -560,7 +560,7 @@ def main():
     torch.cuda.synchronize(dev)
     launches0 = kvx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    w0 = time.time()
+    wall0 = time.time()
     ev0.record(stream)
     for s in range(K):
         # commit without a host sync: the next transition's waves queue right
@@ -568,7 +568,7 @@ def main():
         run_step(trs[Wm + s], t, stall_pairs[s], wait=False)
     ev1.record(stream)
     torch.cuda.synchronize(dev)
-    w1 = time.time()
+    wall1 = time.time()
     launches = kvx.launch_count() - launches0
     for s in range(K):
         res = trs[Wm + s].collect_commit()
@@ -642,8 +642,8 @@ def main():
         for rep in range(6):
             tr = make()
             tr.set_handoff(True)
-            w0 = t.waves[0]
-            tr.begin_refactor((w0.req, w0.hi))
+            wave0 = t.waves[0]
+            tr.begin_refactor((wave0.req, wave0.hi))
             for e in t.events[1:]:  # delta waves before the barrier, as the reference ran them
                 if isinstance(e, W.Barrier):
                     break
@@ -765,7 +765,7 @@ def main():
 
     value = plan.step_bytes * K / (dev_ms * 1e-3) / 1e9
     e2e_value = plan.step_bytes * e2e_steps / e2e_s / 1e9
-    clocks = sampler.summary(w0, w1)
+    clocks = sampler.summary(wall0, wall1)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": n_gpus, "steps": K,
         "warmup": Wm, "ms_per_step": round(dev_ms / K, 4), "higher_is_better": True,
