@@ -722,6 +722,24 @@ def main():
                             "NCCL send/recv of each remote layer region, vs the fused gather+push "
                             "kernel over NVLink P2P (max over ranks)"}
 
+    # ---- the roofline denominator re-measured live on this GPU: the same
+    #      torch copy MEASURED_PEAKS.json uses (b.copy_(a), 1 Gi bf16, read+write)
+    copy_ref = None
+    if world == 1:
+        a_t = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+        b_t = torch.empty_like(a_t)
+        best = float("inf")
+        for _ in range(10):
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record()
+            b_t.copy_(a_t)
+            c1.record()
+            torch.cuda.synchronize(dev)
+            best = min(best, c0.elapsed_time(c1))
+        copy_ref = {"torch_copy_GBps": round(2 * a_t.numel() * 2 / (best * 1e-3) / 1e9, 1),
+                    "note": "b.copy_(a) over 1 Gi bf16 (read+write), best of 10, this run"}
+        del a_t, b_t
+
     # ---- roofline of the dominant kernel
     peak, peak_kind = peaks()
     layer_bytes = plan.wave0_tokens * 2 * plan.token_bytes  # K+V bytes per layer in wave 0
@@ -734,6 +752,7 @@ def main():
         achieved = w0_bytes / (w0_avg * 1e-3) / 1e9
         traffic, traffic_src = ncu_traffic(args.config)
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "live_copy_reference": copy_ref,
                 "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "kvx_bulk_kernel<3,64K> (wave 0, TMA bulk mover)", "bytes_per_launch": w0_bytes,
                 "launch_ms": round(w0_avg, 4), "peak_source": peak_kind}
