@@ -211,6 +211,9 @@ static __global__ void __launch_bounds__(kMoveThreads)
 kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
                 int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
                 int32_t fence_system) {
+    // launched with programmatic dependent launch behind the plan kernel:
+    // wait until its segment list is complete and visible (no-op otherwise)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t units = (int64_t)nseg * nlayers;
     const uint64_t half = block_bytes >> 1;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -408,6 +411,7 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[kStages];
     if (threadIdx.x != 0) return;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the plan kernel's segments
     ChunkIter it;
     it.segs = segs;
     it.layers = layers;
@@ -501,7 +505,8 @@ kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ k
                   uint8_t* __restrict__ live_flag, int32_t max_requests, int32_t max_blocks,
                   int32_t block_tokens, int32_t* __restrict__ row_ptr,
                   int32_t* __restrict__ blocks, int32_t* __restrict__ free_list,
-                  int64_t* __restrict__ out /* [0]=violations [1]=n_blocks [2]=n_free */) {
+                  int64_t* __restrict__ out /* [0]=violations [1]=n_blocks [2]=n_free */,
+                  int32_t* __restrict__ free_list_dev /* optional device copy (block-manager push) */) {
     __shared__ unsigned long long s_viol;
     if (threadIdx.x == 0) s_viol = 0;
     for (int32_t r = threadIdx.x; r < max_requests; r += kCommitThreads) live_flag[r] = 0;
@@ -546,9 +551,12 @@ kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ k
         if (r < max_requests && !live_flag[r]) nb = (int32_t)cdiv(synced_hi[r], B);
         int2 tot;
         const int2 off = block_exclusive_scan2<kCommitThreads>(make_int2(nb, 0), &tot);
-        if (nb > 0 && free_list)
-            for (int32_t k = 0; k < nb; ++k)
-                free_list[carry.x + off.x + k] = dst_bt[(int64_t)r * max_blocks + k];
+        if (nb > 0 && (free_list || free_list_dev))
+            for (int32_t k = 0; k < nb; ++k) {
+                const int32_t id = dst_bt[(int64_t)r * max_blocks + k];
+                if (free_list) free_list[carry.x + off.x + k] = id;
+                if (free_list_dev) free_list_dev[carry.x + off.x + k] = id;
+            }
         carry.x += tot.x;
     }
     __syncthreads();

@@ -267,16 +267,17 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         KVX_CUDA(cudaEventRecord(t->ev_begin, t->stream));
         t->timing_open = true;
     }
-    // One H2D copy covering the three arrays at their fixed offsets.
-    KVX_CUDA(cudaMemcpyAsync(t->d_wave, h, off_hi + sizeof(int64_t) * n, cudaMemcpyHostToDevice, t->stream));
-    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
-    const int32_t* d_req = reinterpret_cast<const int32_t*>(t->d_wave);
-    const int64_t* d_lo = reinterpret_cast<const int64_t*>(t->d_wave + off_lo);
-    const int64_t* d_hi = reinterpret_cast<const int64_t*>(t->d_wave + off_hi);
+    // The plan kernel reads the entries straight from the pinned (UVA-mapped)
+    // staging slot: no separate H2D copy on the stream.  The slot is free
+    // again once the plan kernel has run.
+    const int32_t* h_req = reinterpret_cast<const int32_t*>(h);
+    const int64_t* h_lo = reinterpret_cast<const int64_t*>(h + off_lo);
+    const int64_t* h_hi = reinterpret_cast<const int64_t*>(h + off_hi);
     kvx::kvx_plan_kernel<<<1, kvx::kPlanThreads, 0, t->stream>>>(
-        d_req, d_lo, d_hi, n, t->d_src_bt, t->d_dst_bt, t->d_synced_hi, t->max_blocks,
+        h_req, h_lo, h_hi, n, t->d_src_bt, t->d_dst_bt, t->d_synced_hi, t->max_blocks,
         t->g.block_tokens, t->bm ? t->bm->top : t->alloc, t->bm ? t->bm->d_stack : nullptr, t->d_segs);
     KVX_LAUNCHED();
+    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     if (t->n_local_layers > 0) {
         const int64_t units = nseg * t->n_local_layers;
         const int64_t full = (int64_t)t->num_sms * t->move_ctas_per_sm;
@@ -305,9 +306,22 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             int32_t peer_ctas = (int32_t)kPeerCtas;
             if (const char* pc = getenv("KVX_PEER_CTAS")) peer_ctas = std::max(0, atoi(pc));
             const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
-            bv.fn<<<grid_b, kvx::kBulkThreads, (size_t)bv.stages * bv.chunk, t->stream>>>(
-                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
-                token_bytes(t->g), t->g.block_tokens, t->n_peer_layers, peer_ctas);
+            // programmatic dependent launch: the mover's launch overlaps the
+            // plan kernel; it waits (griddepcontrol.wait) for its segments
+            cudaLaunchAttribute attr{};
+            attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr.val.programmaticStreamSerializationAllowed = 1;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(grid_b);
+            cfg.blockDim = dim3(kvx::kBulkThreads);
+            cfg.dynamicSmemBytes = (size_t)bv.stages * bv.chunk;
+            cfg.stream = t->stream;
+            cfg.attrs = &attr;
+            cfg.numAttrs = 1;
+            KVX_CUDA(cudaLaunchKernelEx(&cfg, bv.fn, (const kvx::Seg*)t->d_segs, (int32_t)nseg,
+                                        (const kvx::LayerPtr*)t->d_layers, t->n_local_layers,
+                                        block_bytes(t->g), token_bytes(t->g), t->g.block_tokens,
+                                        t->n_peer_layers, peer_ctas));
         } else {
             kvx::kvx_move_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
@@ -377,19 +391,20 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
     if (n_live > 0) {
         std::memcpy(h, req, sizeof(int32_t) * n_live);
         std::memcpy(h + off_kv, kv_tokens, sizeof(int64_t) * n_live);
-        KVX_CUDA(cudaMemcpyAsync(t->d_wave, h, off_kv + sizeof(int64_t) * n_live, cudaMemcpyHostToDevice,
-                                 t->stream));
     }
-    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
+    // The commit kernel reads the live set from the pinned (UVA-mapped)
+    // staging slot and writes its results straight into the pinned landing
+    // zone h_commit = [int64 x4 | row_ptr | blocks | free]: no copies on the
+    // stream.  A device copy of the free list feeds the block-manager push.
+    int32_t* h32 = reinterpret_cast<int32_t*>(t->h_commit + 32);
     kvx::kvx_commit_kernel<<<1, kvx::kCommitThreads, 0, t->stream>>>(
-        reinterpret_cast<const int32_t*>(t->d_wave), reinterpret_cast<const int64_t*>(t->d_wave + off_kv),
-        n_live, t->d_dst_bt, t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens,
-        d_row_ptr, d_blocks, d_free, t->d_commit_out);
+        reinterpret_cast<const int32_t*>(h), reinterpret_cast<const int64_t*>(h + off_kv), n_live, t->d_dst_bt,
+        t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens, h32, h32 + (n_live + 1),
+        h32 + (n_live + 1) + nb_live, reinterpret_cast<int64_t*>(t->h_commit), t->bm ? d_free : nullptr);
     KVX_LAUNCHED();
-    // results land in pinned memory; kvx_commit_collect reads them
-    KVX_CUDA(cudaMemcpyAsync(t->h_commit, t->d_commit_out, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, t->stream));
-    KVX_CUDA(cudaMemcpyAsync(t->h_commit + 32, t->d_commit_i32, sizeof(int32_t) * (size_t)need,
-                             cudaMemcpyDeviceToHost, t->stream));
+    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
+    (void)d_row_ptr;
+    (void)d_blocks;
     if (t->bm && nb_free > 0) {  // free-list update: dead rows' blocks back on the stack
         KVX_CUDA(cudaMemcpyAsync(t->bm->d_stack + t->bm->top, d_free, sizeof(int32_t) * (size_t)nb_free,
                                  cudaMemcpyDeviceToDevice, t->stream));
@@ -454,7 +469,7 @@ int kvx_abort(kvx_transition* t) {
             kvx::kvx_commit_kernel<<<1, kvx::kCommitThreads, 0, t->stream>>>(
                 reinterpret_cast<const int32_t*>(t->d_wave), reinterpret_cast<const int64_t*>(t->d_wave), 0,
                 t->d_dst_bt, t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens,
-                d_row_ptr, nullptr, d_free, t->d_commit_out);
+                d_row_ptr, nullptr, d_free, t->d_commit_out, nullptr);
             KVX_LAUNCHED();
             KVX_CUDA(cudaMemcpyAsync(t->bm->d_stack + t->bm->top, d_free, sizeof(int32_t) * (size_t)nb_all,
                                      cudaMemcpyDeviceToDevice, t->stream));
