@@ -591,7 +591,13 @@ def main():
 
     tm = torch.tensor([dev_ms, stall_med, float(launches), w0_avg, float(w0_bytes)], dtype=torch.float64,
                       device=dev)
+    rank_ms = [round(dev_ms / K, 4)]
+    rank_w0 = [round(w0_avg, 4)]
     if world > 1:
+        allv = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(world)]
+        dist.all_gather(allv, torch.tensor([dev_ms / K, w0_avg], dtype=torch.float64, device=dev))
+        rank_ms = [round(float(v[0]), 4) for v in allv]
+        rank_w0 = [round(float(v[1]), 4) for v in allv]
         mx = tm.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = tm.clone()
@@ -800,6 +806,7 @@ def main():
         "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "handoff": handoff,
         "weights": weights, "nccl_baseline": nccl,
         "move_kernel_ms_per_step": round(all_move_ms / K, 4), "move_ms_by_wave": wave_ms,
+        "rank_ms_per_step": rank_ms, "rank_wave0_move_ms": rank_w0,
         "mover": os.environ.get("KVX_MOVE_IMPL", "bulk") + ":" + os.environ.get("KVX_BULK_CFG", "auto"),
     }
     sim = plan.t.simulated_stall_ms()
