@@ -227,3 +227,93 @@ def handoff_worker(rank, world, port, out):
         out.put((rank, "ok", {"checked": checked, "crossed": crossed}))
     except Exception:
         out.put((rank, "err", traceback.format_exc()))
+
+
+def random_worker(rank, world, port, seed, out):
+    """Random plans, geometries, lengths, waves and a random stage->GPU map
+    over the ranks (push or pull, bump rule or block manager): every rank's
+    local destination pools must equal the oracle's, byte for byte."""
+    try:
+        dist = _init(rank, world, port)
+        import numpy as np
+        from oracle import pyoracle as O
+        from paper_2510_11938_b200 import kvx
+        from paper_2510_11938_b200 import shard as S
+        from paper_2510_11938_b200 import workload as W
+
+        rng = np.random.default_rng(seed)
+        L = int(rng.integers(2, 20))
+        heads, dim = int(rng.choice([1, 2, 4])), int(rng.choice([8, 64, 128]))
+
+        def plan():
+            k = int(rng.integers(1, min(L, 8) + 1))
+            return sorted(rng.choice(np.arange(1, L), size=k - 1, replace=False).tolist()) if k > 1 else []
+        ob, nb = plan(), plan()
+        old_dev = rng.integers(0, world, len(ob) + 1).tolist()
+        new_dev = rng.integers(0, world, len(nb) + 1).tolist()
+        pull = bool(rng.random() < 0.5)
+        use_bm = bool(rng.random() < 0.5)
+        N = int(rng.integers(1, 40))
+        final = rng.integers(0, 150, N).astype(np.int64)
+        max_blocks = int(max(1, (final.max() + 15) // 16))
+        src_bt, cap0 = W.fragmented_block_table(final, max_blocks, 16, seed=seed)
+        cap1 = max(1, int(((final + 15) // 16).sum()))
+        live = np.nonzero(final)[0].astype(np.int32)
+        g, og = kvx.geometry(L, heads, dim), O.geo(L, heads, dim)
+
+        def gather(obj):
+            o = [None] * world
+            dist.all_gather_object(o, obj)
+            return o
+
+        old_pools, new_pools = S.setup_rank_pools(
+            kvx, g, ob, nb, old_dev, new_dev, rank, rank, cap0, cap1, all_gather=gather,
+            fill=(seed, live, final[live], src_bt) if len(live) else None, pull=pull)
+        for k, p in enumerate(old_pools):   # zero-filled sources where nothing is live
+            if p is not None and not p.imported and not len(live):
+                p.zero()
+        bm = kvx.BlockManager(rank, cap1) if use_bm else None
+        ref_bm = O.StackBM(cap1) if use_bm else None
+        dist.barrier()
+        tr = kvx.Transition(g, ob, old_pools, nb, new_pools, rank, N, max_blocks, cap1, src_bt, epoch=1,
+                            dst_blockmgr=bm, pull=pull)
+        dp = O.DataPlane(og, ob, nb, cap0, cap1, N, max_blocks, src_bt, bm=ref_bm)
+        if len(live):
+            dp.fill_source(seed, live, final[live])
+        synced = np.zeros(N, np.int64)
+        for w in range(int(rng.integers(1, 4))):
+            target = final if w == 2 else np.minimum(final, synced + rng.integers(0, 80, N))
+            req = np.arange(N, dtype=np.int32)
+            hi = np.maximum(target, synced)
+            tr.wave(req, synced, hi)
+            assert dp.wave(req, synced, hi) == 0
+            synced = hi
+        req = np.arange(N, dtype=np.int32)
+        tr.wave(req, synced, final)          # make sure everything landed
+        assert dp.wave(req, synced, final) == 0
+        tr.wait()
+        dist.barrier()                       # peers' pushes have landed
+        checked = 0
+        for j, d in enumerate(new_dev):
+            if d == rank:
+                assert np.array_equal(new_pools[j].read(), dp.new_pools[j]), f"stage {j} rank {rank}"
+                checked += 1
+        assert np.array_equal(tr.dst_block_table(), dp.bt)
+        res = tr.commit(live, final[live])
+        assert res.violations == 0
+        tr.close()
+        dist.barrier()
+        for p in old_pools + new_pools:
+            if p is not None and p.imported:
+                p.close()
+        dist.barrier()
+        for p in old_pools + new_pools:
+            if p is not None and not p.imported:
+                p.close()
+        if bm is not None:
+            bm.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        out.put((rank, "ok", {"checked": checked, "pull": pull, "bm": use_bm}))
+    except Exception:
+        out.put((rank, "err", traceback.format_exc()))

@@ -64,3 +64,11 @@ def test_two_gpu_activation_handoff(gpu_count):
     res = _run(mgpu_worker.handoff_worker, 2)
     assert sum(r["checked"] for r in res.values()) >= 10
     assert sum(r["crossed"] for r in res.values()) >= 10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_two_gpu_random_bit_exact(gpu_count, seed):
+    if gpu_count < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    _run(mgpu_worker.random_worker, 2, seed)
