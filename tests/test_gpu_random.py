@@ -24,24 +24,25 @@ def random_plan(rng, L):
 def one_case(seed):
     rng = np.random.default_rng(seed)
     L = int(rng.integers(2, 24))
+    elem = int(rng.choice([1, 2, 4]))            # fp8 / fp16 / fp32 KV
     heads = int(rng.choice([1, 2, 4, 8]))
-    dim = int(rng.choice([8, 16, 64, 128]))
+    dim = int(rng.choice([16, 64, 128])) if elem == 1 else int(rng.choice([8, 16, 64, 128]))
+    B = int(rng.choice([8, 16, 32]))             # paged-KV block size
     ob, nb = random_plan(rng, L), random_plan(rng, L)
     N = int(rng.integers(1, 80))
-    B = 16
     final = rng.integers(0, 200, N).astype(np.int64)
     final[rng.random(N) < 0.15] = 0
     max_blocks = int(max(1, (final.max() + B - 1) // B))
     use_bm = bool(rng.random() < 0.5)
-    return rng, L, heads, dim, ob, nb, N, final, max_blocks, use_bm
+    return rng, L, heads, dim, elem, B, ob, nb, N, final, max_blocks, use_bm
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(40))
 def test_random_transition_bit_exact(gpu_count, seed):
-    rng, L, heads, dim, ob, nb, N, final, max_blocks, use_bm = one_case(seed)
-    g, og = kvx.geometry(L, heads, dim), O.geo(L, heads, dim)
-    src_bt, cap0 = W.fragmented_block_table(final, max_blocks, 16, seed=seed, slack=float(rng.random()))
-    need = int(((final + 15) // 16).sum())
+    rng, L, heads, dim, elem, B, ob, nb, N, final, max_blocks, use_bm = one_case(seed)
+    g, og = kvx.geometry(L, heads, dim, elem, B), O.geo(L, heads, dim, elem, B)
+    src_bt, cap0 = W.fragmented_block_table(final, max_blocks, B, seed=seed, slack=float(rng.random()))
+    need = int(((final + B - 1) // B).sum())
     cap1 = max(1, need + int(rng.integers(0, 8)))
     live = np.nonzero(final)[0].astype(np.int32)
     old = []
