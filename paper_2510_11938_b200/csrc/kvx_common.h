@@ -162,6 +162,7 @@ struct kvx_transition {
     int bulk_variant = -1;   // -1: chosen per wave from the average run size
     bool use_bulk = false;   // TMA bulk mover for local destinations
     bool peer_bulk = false;  // ... and for peer (NVLink) destinations
+    bool lsu256 = false;     // LSU mover with 256-bit accesses (KVX_MOVE_IMPL=lsu256)
     std::vector<int32_t> old_b, new_b;
     std::vector<kvx_pool*> old_pools, new_pools;
     int32_t max_requests = 0, max_blocks = 0, dst_num_blocks = 0;

@@ -204,6 +204,63 @@ __device__ __forceinline__ void cta_copy(uint4* __restrict__ dst, const uint4* _
     for (; i < nvec; i += kMoveThreads) st_stream(dst + i, ld_stream(src + i));
 }
 
+// 256-bit variant (sm_100: LDG/STG.256): half the memory instructions per
+// byte; needs 32-byte-aligned runs (token_bytes % 32 == 0, checked on host).
+struct alignas(32) V8 {
+    uint32_t w[8];
+};
+__device__ __forceinline__ V8 ld_stream256(const V8* p) {
+    V8 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]),
+                   "=r"(v.w[6]), "=r"(v.w[7])
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream256(V8* p, const V8& v) {
+    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+                 "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                 : "memory");
+}
+__device__ __forceinline__ void cta_copy256(V8* __restrict__ dst, const V8* __restrict__ src, uint32_t n) {
+    constexpr int kU = 4;
+    uint32_t i = threadIdx.x;
+    const uint32_t step = kMoveThreads * kU;
+    for (; i + (kU - 1) * kMoveThreads < n; i += step) {
+        V8 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = ld_stream256(src + i + u * kMoveThreads);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) st_stream256(dst + i + u * kMoveThreads, v[u]);
+    }
+    for (; i < n; i += kMoveThreads) st_stream256(dst + i, ld_stream256(src + i));
+}
+
+static __global__ void __launch_bounds__(kMoveThreads)
+kvx_move256_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
+                   int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
+                   int32_t fence_system) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int64_t units = (int64_t)nseg * nlayers;
+    const uint64_t half = block_bytes >> 1;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t layer = (int32_t)(u / nseg);
+        const Seg sg = segs[u - (int64_t)layer * nseg];
+        const LayerPtr lp = layers[layer];
+        const char* src = lp.src + (uint64_t)sg.src_blk * block_bytes;
+        char* dst = lp.dst + (uint64_t)sg.dst_blk * block_bytes;
+        if (sg.t0 == 0 && sg.t1 == block_tokens) {
+            cta_copy256(reinterpret_cast<V8*>(dst), reinterpret_cast<const V8*>(src), (uint32_t)(block_bytes >> 5));
+        } else {
+            const uint64_t off = (uint64_t)sg.t0 * token_bytes;
+            const uint32_t n = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * token_bytes) >> 5);
+            cta_copy256(reinterpret_cast<V8*>(dst + off), reinterpret_cast<const V8*>(src + off), n);
+            cta_copy256(reinterpret_cast<V8*>(dst + half + off), reinterpret_cast<const V8*>(src + half + off), n);
+        }
+    }
+    if (fence_system) __threadfence_system();
+}
+
 // Work unit u -> (layer = u / nseg, segment = u % nseg): consecutive CTAs walk
 // consecutive destination blocks of one layer (the dense rule makes them
 // contiguous), sources are wherever the old block table points.

@@ -117,7 +117,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         // destinations alike; KVX_PEER_BULK=0 keeps the LSU mover for peer
         // pushes, KVX_MOVE_IMPL=lsu everywhere.
         const char* impl = getenv("KVX_MOVE_IMPL");
-        t->use_bulk = !(impl && std::string(impl) == "lsu");
+        t->use_bulk = !(impl && (std::string(impl) == "lsu" || std::string(impl) == "lsu256"));
+        t->lsu256 = impl && std::string(impl) == "lsu256";
         const char* pb = getenv("KVX_PEER_BULK");
         t->peer_bulk = t->use_bulk && !(pb && std::string(pb) == "0");
     }
@@ -322,6 +323,10 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                                         (const kvx::LayerPtr*)t->d_layers, t->n_local_layers,
                                         block_bytes(t->g), token_bytes(t->g), t->g.block_tokens,
                                         t->n_peer_layers, peer_ctas));
+        } else if (t->lsu256 && token_bytes(t->g) % 32 == 0) {
+            kvx::kvx_move256_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
+                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
+                token_bytes(t->g), t->g.block_tokens, t->has_peer_dst ? 1 : 0);
         } else {
             kvx::kvx_move_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
