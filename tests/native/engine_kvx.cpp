@@ -93,6 +93,7 @@ struct Observer {
     std::map<int64_t, Xfer> active;
     int64_t commits = 0, aborts = 0, violations_ref = 0;
     int64_t dev_violations = 0, mismatched_words = 0, transitions = 0;
+    double measured_ms = 0.0, measured_bytes = 0.0;  // KV waves on the GPU (reference-accounted bytes)
     std::vector<json> lines;
 
     std::vector<int32_t> bounds(int plan) {
@@ -180,6 +181,10 @@ struct Observer {
         CHECK_KVX(kvx_wait(x.t, x.epoch, &ms));
         const double bw = e->cfg_.kv_sync_bw_bytes_per_ms > 0.0 ? e->cfg_.kv_sync_bw_bytes_per_ms
                                                                 : e->cfg_.inter_stage_bw_bytes_per_ms;
+        if (tok > 0) {
+            measured_ms += ms;
+            measured_bytes += (double)tok * e->cfg_.exec.kv_bytes_per_token;
+        }
         json w;
         w["tokens"] = tok;
         w["modelled_ms"] = (double)tok * e->cfg_.exec.kv_bytes_per_token / bw;
@@ -293,6 +298,53 @@ struct Observer {
     }
 };
 
+// Barrier -> commit stall per transition of a plain engine run (no data
+// plane), read through the same trace hook: the barrier is the handler that
+// sets RefactorCtx::barrier (engine.cpp:676), the commit the RefactorCommit
+// dispatch that ends the ctx (engine.cpp:690-757).
+struct StallProbe {
+    Engine* e = nullptr;
+    std::map<int64_t, double> barrier_at;
+    std::map<int64_t, bool> had_ctx;
+    std::vector<double> stalls;
+    double prev_ms = 0.0, commit_ev_ms = -1.0;
+    void before(const SimEvent& ev) {
+        for (const auto& ip : e->instances_) {
+            auto& inst = *ip;
+            if (inst.refactor && inst.refactor->barrier && !barrier_at.count(inst.id)) barrier_at[inst.id] = prev_ms;
+            if (!inst.refactor && had_ctx[inst.id] && barrier_at.count(inst.id)) {
+                if (commit_ev_ms >= 0) stalls.push_back(commit_ev_ms - barrier_at[inst.id]);
+                barrier_at.erase(inst.id);
+            }
+            had_ctx[inst.id] = (bool)inst.refactor;
+        }
+        if (ev.kind == EventKind::RefactorCommit) commit_ev_ms = ev.time_ms;
+        prev_ms = ev.time_ms;
+    }
+};
+
+json plain_run(const scen::Scenario& sc, double kv_bw) {
+    scen::Built b = scen::build(sc);
+    b.ec.kv_sync_bw_bytes_per_ms = kv_bw;
+    Engine engine(b.ec, b.cluster, sc.reqs);
+    for (auto [t, k] : sc.forced) engine.force_refactor_at(t, "m0", k);
+    for (double t : sc.revocations) engine.revoke_grant_at(t, "m0");
+    StallProbe pr;
+    pr.e = &engine;
+    engine.set_trace_sink([&pr](const SimEvent& ev) { pr.before(ev); });
+    EngineResult r = engine.run();
+    pr.before(SimEvent{engine.now_ms_, 0, EventKind::Arrival, -1, -1, -1, -1});
+    double lat = 0.0;
+    for (const auto& rec : r.records) lat += rec.finish_ms - rec.arrival_ms;
+    json j;
+    j["kv_sync_bw_bytes_per_ms"] = kv_bw;
+    j["stall_ms"] = pr.stalls;
+    j["mean_latency_ms"] = r.records.empty() ? 0.0 : lat / (double)r.records.size();
+    j["duration_ms"] = r.duration_ms;
+    j["refactor_commits"] = r.refactor_commits;
+    return j;
+}
+
 std::vector<Request> steady(int n, double gap, int prompt, int output) {
     std::vector<Request> v;
     for (int i = 0; i < n; ++i) {
@@ -382,6 +434,18 @@ int main(int argc, char** argv) {
     sum["kv_synced_bytes_reference"] = res.kv_synced_bytes;
     sum["kvx_launches"] = kvx_launch_count();
     sum["geometry"] = {sc.num_ops, heads, dim};
+    // measured-time mode: feed the B200-measured KV wave
+    // bandwidth back into the unmodified engine through its own knob
+    // (EngineConfig::kv_sync_bw_bytes_per_ms, engine.cpp:87-90) and report
+    // the simulated stall / latency under the modelled and measured speeds.
+    if (obs.measured_ms > 0.0 && obs.measured_bytes > 0.0) {
+        const double modelled_bw = built.ec.kv_sync_bw_bytes_per_ms > 0.0 ? built.ec.kv_sync_bw_bytes_per_ms
+                                                                         : built.ec.inter_stage_bw_bytes_per_ms;
+        json cal;
+        cal["modelled"] = plain_run(sc, modelled_bw);
+        cal["measured"] = plain_run(sc, obs.measured_bytes / obs.measured_ms);
+        sum["measured_time_mode"] = cal;
+    }
     std::printf("%s\n", sum.dump().c_str());
     return (obs.mismatched_words == 0 && obs.dev_violations == res.kv_violations) ? 0 : 5;
 }

@@ -50,3 +50,8 @@ def test_measured_time_mode_real_geometry(gpu_count, scenario):
     assert waves and all(w["measured_ms"] >= 0 for w in waves)
     big = max(waves, key=lambda w: w["tokens"])
     assert big["measured_ms"] < big["modelled_ms"]  # B200 HBM/NVLink beats the modelled 900 GB/s link
+    # measured-time mode: the engine re-run at the measured KV bandwidth
+    mt = summary["measured_time_mode"]
+    assert mt["measured"]["kv_sync_bw_bytes_per_ms"] > mt["modelled"]["kv_sync_bw_bytes_per_ms"]
+    assert mt["measured"]["refactor_commits"] == mt["modelled"]["refactor_commits"]
+    assert len(mt["measured"]["stall_ms"]) == len(mt["modelled"]["stall_ms"]) >= 1
