@@ -120,7 +120,7 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
                 const int64_t* __restrict__ hi, int32_t n, const int32_t* __restrict__ src_bt,
                 int32_t* __restrict__ dst_bt, int64_t* __restrict__ synced_hi, int32_t max_blocks,
                 int32_t block_tokens, int32_t alloc_base, const int32_t* __restrict__ pop_stack,
-                Seg* __restrict__ segs) {
+                Seg* __restrict__ segs, int32_t src_cap, int32_t dst_cap, int32_t* __restrict__ err) {
     const int64_t B = block_tokens;
     int2 carry = make_int2(0, 0);
     for (int32_t base = 0; base < n; base += kPlanThreads) {
@@ -158,7 +158,15 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
                 const int64_t b = b0 + k;
                 const int64_t t0 = l > b * B ? l - b * B : 0;
                 const int64_t t1 = h < (b + 1) * B ? h - b * B : B;
-                out[k] = Seg{srow[b], row[b], (int32_t)t0, (int32_t)t1};
+                Seg sg{srow[b], row[b], (int32_t)t0, (int32_t)t1};
+                // bounds check on every segment (defence in depth behind the host
+                // validation): an id outside its pool becomes an empty run, so the
+                // mover never touches memory out of range; the error word reports it
+                if (sg.src_blk < 0 || sg.src_blk >= src_cap || sg.dst_blk < 0 || sg.dst_blk >= dst_cap) {
+                    atomicOr(err, 1);
+                    sg.t0 = sg.t1 = 0;
+                }
+                out[k] = sg;
             }
         }
         carry.x += tot.x;
@@ -563,7 +571,8 @@ kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ k
                   int32_t block_tokens, int32_t* __restrict__ row_ptr,
                   int32_t* __restrict__ blocks, int32_t* __restrict__ free_list,
                   int64_t* __restrict__ out /* [0]=violations [1]=n_blocks [2]=n_free */,
-                  int32_t* __restrict__ free_list_dev /* optional device copy (block-manager push) */) {
+                  int32_t* __restrict__ free_list_dev /* optional device copy (block-manager push) */,
+                  const int32_t* __restrict__ err = nullptr /* plan-kernel error word -> out[3] */) {
     __shared__ unsigned long long s_viol;
     if (threadIdx.x == 0) s_viol = 0;
     for (int32_t r = threadIdx.x; r < max_requests; r += kCommitThreads) live_flag[r] = 0;
@@ -621,6 +630,7 @@ kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ k
         out[0] = (int64_t)s_viol;
         out[1] = n_blocks;
         out[2] = carry.x;
+        out[3] = err ? (int64_t)*err : 0;
     }
 }
 

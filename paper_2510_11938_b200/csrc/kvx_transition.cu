@@ -141,8 +141,10 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         A.dev_alloc((void**)&t->d_synced_hi, sizeof(int64_t) * (size_t)d->max_requests) != cudaSuccess ||
         A.dev_alloc((void**)&t->d_wave, wave_bytes) != cudaSuccess ||
         A.dev_alloc((void**)&t->d_live, (size_t)d->max_requests) != cudaSuccess ||
-        A.dev_alloc((void**)&t->d_commit_out, 4 * sizeof(int64_t)) != cudaSuccess)
+        A.dev_alloc((void**)&t->d_commit_out, 4 * sizeof(int64_t)) != cudaSuccess ||
+        A.dev_alloc((void**)&t->d_err, sizeof(int32_t)) != cudaSuccess)
         return bail(fail(KVX_ENOSPC, "transition state allocation failed"));
+    t->src_cap = min_old_blocks;  // INT32_MAX when no old pool is visible here (no local sources)
     for (int s = 0; s < 2; ++s)
         if (A.host_alloc((void**)&t->h_wave[s], wave_bytes) != cudaSuccess ||
             A.event(&t->h_wave_free[s], false) != cudaSuccess)
@@ -151,7 +153,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
             cudaSuccess ||
         cudaMemsetAsync(t->d_dst_bt, 0xff, bt_bytes, t->stream) != cudaSuccess ||
         cudaMemsetAsync(t->d_synced_hi, 0, sizeof(int64_t) * (size_t)d->max_requests, t->stream) !=
-            cudaSuccess)
+            cudaSuccess ||
+        cudaMemsetAsync(t->d_err, 0, sizeof(int32_t), t->stream) != cudaSuccess)
         return bail(fail(KVX_ECUDA, "transition state init"));
 
     // Worst-case wave and commit buffers up front, so no allocation happens
@@ -276,7 +279,8 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     const int64_t* h_hi = reinterpret_cast<const int64_t*>(h + off_hi);
     kvx::kvx_plan_kernel<<<1, kvx::kPlanThreads, 0, t->stream>>>(
         h_req, h_lo, h_hi, n, t->d_src_bt, t->d_dst_bt, t->d_synced_hi, t->max_blocks,
-        t->g.block_tokens, t->bm ? t->bm->top : t->alloc, t->bm ? t->bm->d_stack : nullptr, t->d_segs);
+        t->g.block_tokens, t->bm ? t->bm->top : t->alloc, t->bm ? t->bm->d_stack : nullptr, t->d_segs,
+        t->src_cap, t->dst_num_blocks, t->d_err);
     KVX_LAUNCHED();
     KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     if (t->n_local_layers > 0) {
@@ -351,6 +355,9 @@ int kvx_wait(kvx_transition* t, uint64_t epoch, double* measured_ms) {
     if (epoch != t->epoch) return fail(KVX_ESTALE, "stale epoch");
     DeviceGuard dg(t->device);
     KVX_CUDA(cudaStreamSynchronize(t->stream));
+    int32_t err = 0;
+    KVX_CUDA(cudaMemcpy(&err, t->d_err, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err) return fail(KVX_ECUDA, "device bounds check failed: a wave referenced a block outside its pool");
     float ms = 0.f;
     if (t->timing_open) {
         KVX_CUDA(cudaEventElapsedTime(&ms, t->ev_begin, t->ev_end));
@@ -405,7 +412,8 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
     kvx::kvx_commit_kernel<<<1, kvx::kCommitThreads, 0, t->stream>>>(
         reinterpret_cast<const int32_t*>(h), reinterpret_cast<const int64_t*>(h + off_kv), n_live, t->d_dst_bt,
         t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens, h32, h32 + (n_live + 1),
-        h32 + (n_live + 1) + nb_live, reinterpret_cast<int64_t*>(t->h_commit), t->bm ? d_free : nullptr);
+        h32 + (n_live + 1) + nb_live, reinterpret_cast<int64_t*>(t->h_commit), t->bm ? d_free : nullptr,
+        t->d_err);
     KVX_LAUNCHED();
     KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     (void)d_row_ptr;
@@ -430,8 +438,9 @@ int kvx_commit_collect(kvx_transition* t, kvx_commit_result* out) {
     if (t->state != kvx_transition::kCommitPending) return fail(KVX_ESTATE, "no commit pending");
     DeviceGuard dg(t->device);
     KVX_CUDA(cudaEventSynchronize(t->ev_commit));
-    int64_t res[3];
+    int64_t res[4];
     std::memcpy(res, t->h_commit, sizeof(res));
+    if (res[3]) return fail(KVX_ECUDA, "device bounds check failed: a wave referenced a block outside its pool");
     if (res[1] != t->pend_nb_live || res[2] != t->pend_nb_free)
         return fail(KVX_ECUDA, "device compaction disagrees with the host mirror");
     const int32_t* h32 = reinterpret_cast<const int32_t*>(t->h_commit + 32);
@@ -507,6 +516,7 @@ int kvx_destroy(kvx_transition* t) {
     A.dev_free(t->d_live, (size_t)t->max_requests);
     A.dev_free(t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap);
     A.dev_free(t->d_commit_out, 4 * sizeof(int64_t));
+    A.dev_free(t->d_err, sizeof(int32_t));
     A.host_free(t->h_commit, t->h_commit_bytes);
     A.event_free(t->ev_commit, false);
     for (int s = 0; s < 2; ++s) {
