@@ -179,3 +179,31 @@ def test_launch_counter_moves(gpu_count):
     finally:
         m.close()
     assert kvx.launch_count() >= before + 2
+
+
+def test_device_bounds_check_catches_unbacked_source(gpu_count):
+    """With the host's per-wave source check bypassed (test hook, read at the
+    first wave of the process -- so run in a subprocess), a wave over a
+    request with no source blocks reaches the plan kernel, which neutralises
+    the segments and reports KVX_ECUDA at wait."""
+    import subprocess
+    import sys
+    code = r'''
+import os, sys
+sys.path.insert(0, os.environ["ROOT"])
+from tests.test_gpu_edges import Mini
+from paper_2510_11938_b200 import kvx
+m = Mini([40, 20, 0, 0])
+m.tr.wave([2], [0], [5])            # request 2 has no source blocks: ids are -1
+try:
+    m.tr.wait()
+    print("NOT CAUGHT")
+except kvx.KvxError as e:
+    print("CAUGHT", e.code, "bounds" in str(e))
+m.close()
+'''
+    import os
+    env = dict(os.environ, KVX_TEST_SKIP_HOST_CHECKS="1",
+               ROOT=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert "CAUGHT -4 True" in out.stdout, out.stdout + out.stderr
