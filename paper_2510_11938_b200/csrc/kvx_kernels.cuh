@@ -1,25 +1,33 @@
 // kvx_kernels.cuh -- sm_100a device code of the inflight-refactor KV transition.
 //
-// Kernels (all launched on the transition's own stream):
-//   kvx_plan_kernel    one CTA: destination block allocation (block-wide
-//                      exclusive scan of per-request new-block counts),
-//                      block-table rewrite, synced high-water marks and the
-//                      per-block copy segments of the wave.  Restates the
-//                      "which tokens move" half of engine.cpp:637-687 at
-//                      block granularity.
-//   kvx_move_kernel    persistent grid (SMs x resident CTAs): one
-//                      (segment, layer) slab per CTA iteration, 16-byte
-//                      vectorised coalesced loads/stores, 8 loads in flight
-//                      per thread.  Writes through peer pointers when the
-//                      destination pool is another GPU's (NVLink P2P push).
-//   kvx_bulk_kernel    same work list, TMA bulk engine path: one elected
-//                      thread per CTA streams slabs global -> shared ->
-//                      global with cp.async.bulk + mbarrier, multi-stage ring.
-//   kvx_commit_kernel  one CTA: Eq. 10 check per live request
-//                      (engine.cpp:707-713) with warp ballots, block-table
-//                      compaction of live rows (CSR) and free-list build for
-//                      rows that are no longer live (ballot + prefix scan).
-//   kvx_fill_kernel / kvx_verify_kernel   synthetic payload (test + bench).
+// Kernels (launched on the transition's stream):
+//   kvx_plan_kernel      one CTA: destination block allocation (block-wide
+//                        exclusive scan of per-request new-block counts; bump
+//                        rule or pops off the block manager's free stack),
+//                        block-table rewrite, synced high-water marks, the
+//                        per-block copy segments of the wave, and a bounds
+//                        check of every segment.  Reads the wave entries
+//                        straight from mapped pinned memory.  Restates the
+//                        "which tokens move" half of engine.cpp:637-687.
+//   kvx_bulk_kernel      THE mover (default): persistent, one elected thread
+//                        per CTA streams (segment, layer) slabs global ->
+//                        shared -> global through a cp.async.bulk ring with
+//                        mbarrier tx counts (SASS UBLKCP / SYNCS); local HBM
+//                        or NVLink-peer destinations; optional CTA split
+//                        between peer and local layers.  Launched with PDL
+//                        behind the plan kernel (griddepcontrol.wait).
+//   kvx_move_kernel      LSU mover (16-byte ld.global.nc / st.global, 8 in
+//                        flight per thread); kvx_move256_kernel its 256-bit
+//                        variant.  KVX_MOVE_IMPL=lsu|lsu256.
+//   kvx_copy_list_kernel bulk engine over a (src, dst, bytes) list: activation
+//                        handoff and stage weight migration.
+//   kvx_commit_kernel    one CTA: Eq. 10 check per live request
+//                        (engine.cpp:707-713) with warp ballots, CSR
+//                        compaction of live rows, free list of rows no longer
+//                        live (scans); results written into mapped pinned
+//                        memory.
+//   kvx_bm_init_kernel   block-manager stack initialisation.
+//   kvx_fill_kernel / kvx_verify_kernel   synthetic payload (tests + bench).
 #pragma once
 // Included by several translation units: non-template kernels have internal
 // linkage (static), templates are instantiated where used.
