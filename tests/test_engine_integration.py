@@ -55,3 +55,14 @@ def test_measured_time_mode_real_geometry(gpu_count, scenario):
     assert mt["measured"]["kv_sync_bw_bytes_per_ms"] > mt["modelled"]["kv_sync_bw_bytes_per_ms"]
     assert mt["measured"]["refactor_commits"] == mt["modelled"]["refactor_commits"]
     assert len(mt["measured"]["stall_ms"]) == len(mt["modelled"]["stall_ms"]) >= 1
+
+
+def test_reference_refactor_tests_with_kvx_doctest(gpu_count):
+    """tests/native/test_kvx_engine.cpp: the reference's own refactor test
+    cases (test_engine.cpp:194-263, criterion 12) with the data plane attached,
+    in the reference's doctest style."""
+    exe = os.path.join(ROOT, "tests", "native", "_build", "test_kvx_engine")
+    assert os.path.exists(exe)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "6 passed | 0 failed" in out.stdout
