@@ -55,6 +55,8 @@
 #include "pipesim/modelgraph.hpp"
 #include "pipesim/rng.hpp"
 #include "pipesim/workload.hpp"
+#include "pipesim/config.hpp"
+#include "pipesim/experiment.hpp"
 #include "scenarios.hpp"
 
 using namespace pipesim;
@@ -284,6 +286,8 @@ struct Observer {
     }
 };
 
+void run_engine(Engine& engine, const Scenario& s, const std::string& dir);
+
 void run(const Scenario& s, const std::string& dir) {
     scen::Built b = scen::build(s);
     EngineConfig& ec = b.ec;
@@ -292,6 +296,43 @@ void run(const Scenario& s, const std::string& dir) {
     Engine engine(ec, cluster, s.reqs);
     for (const auto& [t, k] : s.forced) engine.force_refactor_at(t, "m0", k);
     for (double t : s.revocations) engine.revoke_grant_at(t, "m0");
+    run_engine(engine, s, dir);
+}
+
+// BASELINE config 5 as the reference runs it: the adaptive FlexPipe policy
+// (controller Alg. 1, controller.cpp:55) decides every refactor on a gamma
+// trace, built through the public experiment API (experiment.hpp:37-47) from
+// the reference's own configs/flexpipe-demo.json, shortened.
+void run_adaptive(double cv, double duration_s, const std::string& dir) {
+    ExperimentConfig cfg = load_config("/root/reference/proj/configs/flexpipe-demo.json");
+    cfg.workload.spec.target_cv = cv;
+    cfg.workload.spec.duration_s = duration_s;
+    cfg.output_dir = "/tmp/pipesim-adaptive";
+    // A livelier controller than the demo's (hysteresis 0.5, cooldown 30 s,
+    // sigma 20 -- with which g* never leaves 4), so the trace sees
+    // controller-chosen refactors; the decisions remain the reference's own.
+    cfg.ctrl.hysteresis_margin = 0.02;
+    cfg.ctrl.refactor_cooldown_ms = 8000.0;
+    cfg.ctrl.sensitivity_sigma = 1.0;  // CV match sharp enough to move g* with the window CV
+    ExperimentSetup setup = build_setup(cfg);
+    const auto profiles = calibrate_profiles(cfg);
+    Scenario s;
+    char name[64];
+    std::snprintf(name, sizeof(name), "adaptive_cv%g", cv);
+    s.name = name;
+    s.note = "BASELINE C5: adaptive policy (controller Alg. 1) on configs/flexpipe-demo.json, gamma CV " +
+             std::to_string(cv) + ", " + std::to_string((int)duration_s) + " s";
+    s.num_ops = (int)setup.engine.graph.ops.size();
+    s.kv_bytes_per_token = setup.engine.exec.kv_bytes_per_token;
+    s.max_sync_rounds = setup.engine.max_sync_rounds;
+    s.reqs = setup.requests;
+    for (const auto& gp : setup.granularities.plans) s.stage_counts.push_back(gp.config.stages);
+    Engine engine(setup.engine, setup.cluster, setup.requests);
+    engine.set_profiles(profiles);
+    run_engine(engine, s, dir);
+}
+
+void run_engine(Engine& engine, const Scenario& s, const std::string& dir) {
 
     std::ofstream out(dir + "/" + s.name + ".jsonl");
     Observer obs;
@@ -389,6 +430,12 @@ int main(int argc, char** argv) {
     for (const auto& s : scenarios()) {
         if (!only.empty() && s.name != only) continue;
         run(s, dir);
+    }
+    for (double cv : {1.0, 4.0, 7.0}) {
+        char name[64];
+        std::snprintf(name, sizeof(name), "adaptive_cv%g", cv);
+        if (!only.empty() && only != name) continue;
+        run_adaptive(cv, 600.0, dir);
     }
     return 0;
 }

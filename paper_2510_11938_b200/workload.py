@@ -122,6 +122,10 @@ class Scenario:
     num_requests: int
     transitions: List[TransitionSpec]
     result: Dict
+    # global order of (transition index, event) across instances, as the
+    # reference dispatched them: ("wave", Wave) | ("barrier", Barrier) |
+    # ("commit" | "abort", None)
+    timeline: list = field(default_factory=list)
 
 
 def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
@@ -131,6 +135,8 @@ def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
     assert head["kind"] == "scenario"
     trans: List[TransitionSpec] = []
     cur: Dict[int, TransitionSpec] = {}
+    idx: Dict[int, int] = {}
+    timeline = []
     result = {}
     for r in rows[1:]:
         k = r["kind"]
@@ -141,6 +147,7 @@ def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
                                r.get("begin_ms", r["t_ms"]),
                                r["load_ready_ms"], r.get("param_loads", []))
             cur[r["instance"]] = t
+            idx[r["instance"]] = len(trans)
             trans.append(t)
         elif k == "wave":
             e = np.array(r["entries"], dtype=np.int64).reshape(-1, 3)
@@ -148,19 +155,22 @@ def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
                      e[:, 2].copy(), r["tokens"], r["kv_synced_bytes_total"])
             cur[r["instance"]].waves.append(w)
             cur[r["instance"]].events.append(w)
+            timeline.append((idx[r["instance"]], "wave", w))
         elif k == "barrier":
             e = np.array(r["live"], dtype=np.int64).reshape(-1, 2)
             mbs = [MicroBatchRec(m["batch"], m["where"], m["after"], int(sum(u[2] for u in m["units"])),
                                  m["act_bytes"]) for m in r.get("microbatches", [])]
-            cur[r["instance"]].events.append(Barrier(r["rounds"], r["inflight_batches"],
-                                                     e[:, 0].astype(np.int32), e[:, 1].copy(), mbs,
-                                                     r.get("barrier_ms", r["t_ms"])))
+            b = Barrier(r["rounds"], r["inflight_batches"], e[:, 0].astype(np.int32), e[:, 1].copy(), mbs,
+                        r.get("barrier_ms", r["t_ms"]))
+            cur[r["instance"]].events.append(b)
+            timeline.append((idx[r["instance"]], "barrier", b))
         elif k == "commit_state":
             e = np.array(r["live"], dtype=np.int64).reshape(-1, 2)
             t = cur[r["instance"]]
             t.live_req, t.live_kv = e[:, 0].astype(np.int32), e[:, 1].copy()
             t.commit_ms = r["t_ms"]  # RefactorCommit dispatch time
         elif k in ("commit", "abort", "end_unknown"):
+            timeline.append((idx[r["instance"]], k, None))
             t = cur.pop(r["instance"])
             t.outcome = k
             t.violations = r.get("violations")
@@ -168,7 +178,7 @@ def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
         elif k == "result":
             result = r
     return Scenario(head["name"], head["note"], head["num_layers"], head["kv_bytes_per_token"],
-                    head["max_sync_rounds"], head["num_requests"], trans, result)
+                    head["max_sync_rounds"], head["num_requests"], trans, result, timeline)
 
 
 def golden_names(golden_dir: str = GOLDEN_DIR) -> List[str]:

@@ -24,35 +24,52 @@ def test_goldens_present():
 
 @pytest.mark.parametrize("name", NAMES)
 def test_control_plane_matches_reference(name):
+    """Replays every transition in the reference's own global event order
+    (instances refactor concurrently in the adaptive goldens), one shared
+    EngineResult::kv_synced_bytes accumulator, bit-exact after every wave."""
     scn = W.load_golden(name)
     acc = np.zeros(1, np.float64)  # EngineResult::kv_synced_bytes, shared across transitions
     commits = aborts = violations = 0
-    for t in scn.transitions:
-        ctx = O.ControlCtx(scn.num_requests, scn.max_sync_rounds, scn.kv_bytes_per_token, acc)
+    gens, ctxs = {}, {}
 
+    def shim(ctx):
         class Shim:
             def begin(self, req, kv):
                 return ctx.begin(req, kv)
 
             def on_sync_complete(self, req, kv, inflight):
                 return ctx.on_sync_complete(req, kv, inflight)
+        return Shim()
 
-        for w, lo, hi in replay(Shim(), t):
-            # bit-exact double accumulation, engine.cpp:645,671,684
-            assert acc[0] == w.kv_synced_bytes_total
-        if t.outcome == "commit":
-            ctx.apply()  # engine.cpp:697-702
-            v = ctx.violations(t.live_req, t.live_kv)
+    for ti, kind, ev in scn.timeline:
+        t = scn.transitions[ti]
+        if ti not in gens:
+            ctxs[ti] = O.ControlCtx(scn.num_requests, scn.max_sync_rounds, scn.kv_bytes_per_token, acc)
+            gens[ti] = replay(shim(ctxs[ti]), t)
+        if kind == "wave":
+            w, _, _ = next(gens[ti])       # consumes the barriers before this wave
+            assert w is ev
+            assert acc[0] == w.kv_synced_bytes_total  # bit-exact, engine.cpp:645,671,684
+        elif kind == "commit":
+            ctxs[ti].apply()               # engine.cpp:697-702
+            v = ctxs[ti].violations(t.live_req, t.live_kv)
             assert v == t.violations
             violations += v
             commits += 1
-        elif t.outcome == "abort":
+            assert acc[0] == t.kv_synced_bytes_total
+        elif kind == "abort":
             aborts += 1
-        assert acc[0] == t.kv_synced_bytes_total
     assert acc[0] == scn.result["kv_synced_bytes"]
     assert commits == scn.result["refactor_commits"]
     assert aborts == scn.result["refactor_aborts"]
     assert violations == scn.result["kv_violations"]
+
+
+def test_adaptive_goldens_refactor_under_the_controller():
+    """BASELINE C5: the reference's own controller (Alg. 1) decides the
+    refactors on gamma traces; more burstiness, more refactors."""
+    n = {cv: W.load_golden(f"adaptive_cv{cv}").result["refactor_commits"] for cv in (1, 4, 7)}
+    assert n[1] == 0 and n[4] >= 1 and n[7] > n[4]
 
 
 def test_known_answers_spec():

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 SMALL = [("engine_mid_decode", 2, 64), ("engine_consolidate", 2, 64), ("criterion12", 2, 64),
          ("engine_zero_inflight", 2, 64), ("bursty_repeated", 1, 8), ("delta_rounds_cap", 2, 64),
-         ("delta_rounds_converge", 2, 64)]
+         ("delta_rounds_converge", 2, 64), ("adaptive_cv4", 1, 8), ("adaptive_cv7", 1, 8)]
 
 
 def _commit_and_compare(case):
@@ -100,3 +100,34 @@ def test_c4_same_k_replacement_full_size(gpu_count):
         assert case.tr.verify_pattern(SEED, t.live_req, t.live_kv) == 0
     finally:
         case.close()
+
+
+def test_c5_adaptive_chain_full_shape(gpu_count):
+    """BASELINE config 5: the reference controller's own refactor chain on a
+    gamma trace (CV=7, tests/golden/adaptive_cv7.jsonl: 4->16, then 16<->8
+    re-cuts chosen by Alg. 1) at the Llama-2-7B shape.  Every third
+    transition whose source + destination footprint fits one GPU (the largest
+    touches ~300k token slots, ~150 GB per side) is moved at full size:
+    tables and compaction equal the oracle's, every live word equals the
+    payload, moved bytes equal the waves' token sum.  All 39 are compared
+    byte for byte at a small geometry in test_small_goldens_bit_exact."""
+    scn = W.load_golden("adaptive_cv7")
+    L, H, D = W.SHAPES["llama2-7b"]
+    token_bytes = 2 * H * D * 2
+    ran = 0
+    for t in scn.transitions[::3]:
+        if int(t.max_tokens(scn.num_requests).sum()) * token_bytes * L * 2 > 60e9:
+            continue
+        case = GpuCase(scn, t, H, D, oracle_pools=False)
+        try:
+            case.run_ctl()
+            case.compare_tables()
+            res = _commit_and_compare(case)
+            assert res.violations == 0
+            assert case.tr.verify_pattern(SEED, t.live_req, t.live_kv) == 0
+            moved = sum(int((w.hi - w.lo).clip(min=0).sum()) for w in t.waves)
+            assert case.tr.bytes_moved() == moved * 2 * case.g.token_bytes * L
+            ran += 1
+        finally:
+            case.close()
+    assert ran >= 8
