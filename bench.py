@@ -492,12 +492,22 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     n_gpus = world
+    # KVX_BENCH_FOLD=n (functional testing only): fold the ranks onto n
+    # physical GPUs, e.g. the N=8 placement on a 4-GPU box.  NCCL refuses two
+    # ranks on one GPU, so the host plumbing goes over gloo, the NCCL baseline
+    # is skipped and the line is marked as not a measurement.
+    fold = int(os.environ.get("KVX_BENCH_FOLD", "0"))
+    dev = (local % fold if fold else local) if world > 1 else 0
+    if fold:
+        args.no_nccl = True
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(dev)
+        if fold:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    dev = local if world > 1 else 0
 
     plan = Plan(args.config)
     t = plan.t
@@ -811,6 +821,9 @@ def main():
     }
     sim = plan.t.simulated_stall_ms()
     line["stall_reference_simulated_ms"] = round(sim, 3) if sim is not None else None
+    if fold:
+        line["folded_onto_gpus"] = fold
+        line["not_a_measurement"] = "ranks share GPUs (KVX_BENCH_FOLD); functional check of the N-rank path"
     if n_gpus == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         gbs, desc, _ = cpu_sample_run(plan, 3, 1, threads)
