@@ -149,7 +149,22 @@ struct kvx_blockmgr {
     int32_t capacity = 0;
     int32_t top = 0;          // free blocks (host mirror of the device stack top)
     int32_t* d_stack = nullptr;
+    // Orders stream-side stack operations (wave pops in the plan kernel,
+    // commit / abort pushes) of transitions on different streams in host
+    // issue order, which is the order the host mirror `top` assumed.
+    cudaEvent_t order = nullptr;
+    bool order_live = false;
 };
+
+// Stack-op ordering across streams (see kvx_blockmgr::order).
+inline cudaError_t bm_order_before(kvx_blockmgr* bm, cudaStream_t s) {
+    return bm->order_live ? cudaStreamWaitEvent(s, bm->order, 0) : cudaSuccess;
+}
+inline cudaError_t bm_order_after(kvx_blockmgr* bm, cudaStream_t s) {
+    const cudaError_t e = cudaEventRecord(bm->order, s);
+    if (e == cudaSuccess) bm->order_live = true;
+    return e;
+}
 
 struct kvx_transition {
     kvx_geometry g{};

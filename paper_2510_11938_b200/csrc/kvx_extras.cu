@@ -162,6 +162,11 @@ int kvx_bm_create(int32_t device, int32_t capacity, kvx_blockmgr** out) {
         cudaGetLastError();
         return fail(KVX_ENOSPC, "block manager allocation failed");
     }
+    if (cudaEventCreateWithFlags(&bm->order, cudaEventDisableTiming) != cudaSuccess) {
+        cudaFree(bm->d_stack);
+        delete bm;
+        return fail(KVX_ECUDA, "block manager event");
+    }
     *out = bm;
     return kvx_bm_reset(bm);
 }
@@ -223,7 +228,9 @@ int kvx_bm_snapshot(const kvx_blockmgr* bm, int32_t* stack_out, int32_t* top_out
 int kvx_bm_destroy(kvx_blockmgr* bm) {
     if (!bm) return KVX_OK;
     DeviceGuard dg(bm->device);
+    cudaDeviceSynchronize();
     cudaFree(bm->d_stack);
+    if (bm->order) cudaEventDestroy(bm->order);
     delete bm;
     return KVX_OK;
 }

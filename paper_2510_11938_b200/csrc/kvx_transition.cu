@@ -276,6 +276,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     // The plan kernel reads the entries straight from the pinned (UVA-mapped)
     // staging slot: no separate H2D copy on the stream.  The slot is free
     // again once the plan kernel has run.
+    if (t->bm && new_blocks > 0) KVX_CUDA(bm_order_before(t->bm, t->stream));
     const int32_t* h_req = reinterpret_cast<const int32_t*>(h);
     const int64_t* h_lo = reinterpret_cast<const int64_t*>(h + off_lo);
     const int64_t* h_hi = reinterpret_cast<const int64_t*>(h + off_hi);
@@ -285,6 +286,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         t->src_cap, t->dst_num_blocks, t->d_err);
     KVX_LAUNCHED();
     KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
+    if (t->bm && new_blocks > 0) KVX_CUDA(bm_order_after(t->bm, t->stream));
     if (t->n_local_layers > 0) {
         const int64_t units = nseg * t->n_local_layers;
         const int64_t full = (int64_t)t->num_sms * t->move_ctas_per_sm;
@@ -393,6 +395,8 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
         if (!live[(size_t)r]) nb_free += cdiv64(t->synced_hi[(size_t)r], B);
     const int64_t need = (n_live + 1) + nb_live + nb_free;
     if (need > t->commit_i32_cap) return fail(KVX_ECUDA, "commit scratch undersized");  // sized at begin
+    if (t->bm && (int64_t)t->bm->top + nb_free > t->bm->capacity)
+        return fail(KVX_EINVAL, "block manager overflow: the freed blocks exceed its capacity (double free?)");
     int32_t* d_row_ptr = t->d_commit_i32;
     int32_t* d_blocks = d_row_ptr + (n_live + 1);
     int32_t* d_free = d_blocks + nb_live;
@@ -421,8 +425,10 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
     (void)d_row_ptr;
     (void)d_blocks;
     if (t->bm && nb_free > 0) {  // free-list update: dead rows' blocks back on the stack
+        KVX_CUDA(bm_order_before(t->bm, t->stream));
         KVX_CUDA(cudaMemcpyAsync(t->bm->d_stack + t->bm->top, d_free, sizeof(int32_t) * (size_t)nb_free,
                                  cudaMemcpyDeviceToDevice, t->stream));
+        KVX_CUDA(bm_order_after(t->bm, t->stream));
         t->bm->top += (int32_t)nb_free;
     }
     KVX_CUDA(cudaEventRecord(t->ev_commit, t->stream));
@@ -479,6 +485,8 @@ int kvx_abort(kvx_transition* t) {
         const int64_t B = t->g.block_tokens;
         int64_t nb_all = 0;
         for (int32_t r = 0; r < t->max_requests; ++r) nb_all += cdiv64(t->synced_hi[(size_t)r], B);
+        if ((int64_t)t->bm->top + nb_all > t->bm->capacity)
+            return fail(KVX_EINVAL, "block manager overflow: the taken blocks exceed its capacity");
         if (nb_all > 0) {
             int32_t* d_row_ptr = t->d_commit_i32;
             int32_t* d_free = d_row_ptr + 1;
@@ -487,8 +495,10 @@ int kvx_abort(kvx_transition* t) {
                 t->d_dst_bt, t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens,
                 d_row_ptr, nullptr, d_free, t->d_commit_out, nullptr);
             KVX_LAUNCHED();
+            KVX_CUDA(bm_order_before(t->bm, t->stream));
             KVX_CUDA(cudaMemcpyAsync(t->bm->d_stack + t->bm->top, d_free, sizeof(int32_t) * (size_t)nb_all,
                                      cudaMemcpyDeviceToDevice, t->stream));
+            KVX_CUDA(bm_order_after(t->bm, t->stream));
             t->bm->top += (int32_t)nb_all;
         }
     }

@@ -179,3 +179,47 @@ def test_abort_with_blockmgr_returns_blocks(gpu_count):
         for p in old + new:
             p.close()
         bm.close()
+
+
+def test_shared_blockmgr_across_streams(gpu_count):
+    """Two transitions popping from / pushing to ONE block manager on
+    different streams take their ids in host issue order.  B pops 6 ids, A
+    pops the next 4 behind a long kernel on its stream, then B's commit frees
+    3 ids into exactly the stack slots A popped from.  A must still get the
+    ids the host mirror promised (6..9), as the sequential oracle does."""
+    import torch
+    g = kvx.geometry(2, 1, 8)
+    N, max_blocks, cap = 4, 4, 16
+    src_bt = np.arange(N * max_blocks, dtype=np.int32).reshape(N, max_blocks)
+    old = [kvx.Pool(0, g, 2, N * max_blocks) for _ in range(2)]
+    for p in old:
+        p.zero()
+    new = [kvx.Pool(0, g, 2, cap)]
+    new[0].zero()
+    bm, ref = kvx.BlockManager(0, cap), O.StackBM(cap)
+    sA, sB = torch.cuda.Stream(), torch.cuda.Stream()
+    tA = kvx.Transition(g, [], [old[0]], [], new, 0, N, max_blocks, cap, src_bt, stream=sA.cuda_stream,
+                        dst_blockmgr=bm)
+    tB = kvx.Transition(g, [], [old[1]], [], new, 0, N, max_blocks, cap, src_bt, stream=sB.cuda_stream,
+                        dst_blockmgr=bm)
+    try:
+        req = np.array([0, 1], np.int32)
+        tB.wave(req, np.zeros(2, np.int64), np.array([40, 40], np.int64))   # pops ids 0..5
+        tB.wait()
+        ref.pop(6)
+        with torch.cuda.stream(sA):
+            torch.cuda._sleep(int(3e8))                                      # ~150 ms on sA
+        tA.wave(np.array([0], np.int32), np.zeros(1, np.int64), np.array([50], np.int64))
+        want_a = ref.pop(4)                                                  # 6, 7, 8, 9
+        res = tB.commit(np.array([0], np.int32), np.array([40], np.int64))   # request 1 finished
+        np.testing.assert_array_equal(res.free_list, [3, 4, 5])
+        ref.push(res.free_list)
+        tA.wait()
+        np.testing.assert_array_equal(tA.dst_block_table()[0], want_a)
+        np.testing.assert_array_equal(bm.snapshot(), ref.snapshot())
+    finally:
+        tA.close()
+        tB.close()
+        for p in old + new:
+            p.close()
+        bm.close()
