@@ -71,7 +71,15 @@ def wave():
 
 
 def commit():
-    state["t"].on_refactor_commit((np.array([0], np.int32), np.array([40], np.int64)), wait=False)
+    t = state["t"]
+    req, kv = np.array([0], np.int32), np.array([40], np.int64)
+    assert kvx._lib.kvx_commit_async(t._h, C.c_uint64(t.epoch), 1, req.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     kv.ctypes.data_as(C.POINTER(C.c_int64))) == 0
+
+
+def collect():
+    res = kvx._CommitResult()
+    assert kvx._lib.kvx_commit_collect(state["t"]._h, C.byref(res)) == 0
 
 
 probe("torch add_ (kernel)", torch_add)
@@ -81,9 +89,9 @@ probe("cudaMemsetAsync 4 KiB", memset)
 probe("kvx_begin (no block manager)", begin())
 probe("kvx_wave", wave)
 probe("kvx_commit_async (no block manager)", commit)
-state["t"].collect_commit(); state["t"].close()
+collect(); state["t"].close()
 bm = kvx.BlockManager(0, cap)
 probe("kvx_begin (block manager)", begin(bm))
 probe("kvx_wave (block manager)", wave)
 probe("kvx_commit_async (block manager, 3 freed)", commit)
-state["t"].collect_commit(); state["t"].close()
+collect(); state["t"].close()
