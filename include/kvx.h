@@ -64,6 +64,12 @@ int kvx_abi_version(void);
 /* Kernels this library launched in this process (evidence for bench.py). */
 uint64_t kvx_launch_count(void);
 int kvx_device_count(int32_t* out);
+/* Loads every kvx kernel on `device` now.  CUDA lazy loading would load a
+ * kernel at its first launch, and a load waits for the work running on the
+ * device, so the first refactor would stall behind the serving kernels.
+ * Pool / block-manager / transition creation call this implicitly (once per
+ * device); a server may call it at start-up. */
+int kvx_preload(int32_t device);
 
 /* Model geometry.  token_bytes = num_kv_heads * head_dim * elem_bytes must
  * be a multiple of 16 (vectorised 16-byte moves).  Replaces the scalar

@@ -2,6 +2,9 @@
 // launch counter, version / device queries and the hooks kvx_ctl.cpp uses.
 #include "kvx_common.h"
 
+#include <mutex>
+#include <set>
+
 namespace kvx_host {
 std::string& last_error() {
     thread_local std::string msg;
@@ -10,6 +13,23 @@ std::string& last_error() {
 std::atomic<uint64_t>& launches() {
     static std::atomic<uint64_t> n{0};
     return n;
+}
+int ensure_loaded(int device) {
+    static std::mutex mu;
+    static std::set<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(device)) return KVX_OK;
+    DeviceGuard dg(device);
+    if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed");
+    for (auto fn : {preload_transition_kernels, preload_pool_kernels, preload_extras_kernels}) {
+        const cudaError_t e = fn();
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(KVX_ECUDA, std::string("kernel preload: ") + cudaGetErrorString(e));
+        }
+    }
+    done.insert(device);
+    return KVX_OK;
 }
 }  // namespace kvx_host
 
@@ -20,6 +40,8 @@ extern "C" {
 const char* kvx_last_error(void) { return last_error().c_str(); }
 int kvx_abi_version(void) { return KVX_ABI_VERSION; }
 uint64_t kvx_launch_count(void) { return launches().load(); }
+
+int kvx_preload(int32_t device) { return ensure_loaded(device); }
 
 int kvx_device_count(int32_t* out) {
     if (!out) return fail(KVX_EINVAL, "out is null");

@@ -112,6 +112,17 @@ inline void CUDART_CB release_pieces(void* arg) {
     delete r;
 }
 
+// Eager kernel loading.  Under CUDA lazy loading (the default) a kernel's
+// module is loaded at its first launch or attribute query, and the load waits
+// for the work already running on the device: the first refactor of a
+// serving process would stall behind the serving kernels.  ensure_loaded()
+// loads every kvx kernel the first time a device is touched (pool, block
+// manager or transition creation; kvx_preload), once per device.
+cudaError_t preload_transition_kernels();
+cudaError_t preload_pool_kernels();
+cudaError_t preload_extras_kernels();
+int ensure_loaded(int device);
+
 // (ring depth, chunk bytes) of the TMA bulk mover; KVX_BULK_CFG=<index> pins one.
 using BulkFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, uint64_t, int32_t,
                         int32_t, int32_t);

@@ -4,6 +4,28 @@
 
 using namespace kvx_host;
 
+namespace {
+// copy-list rings: handoff rows (short runs) and weight layers (long runs)
+constexpr int kHandoffStages = 4, kWeightStages = 6;
+constexpr uint32_t kCopyChunk = 32768;
+}  // namespace
+
+namespace kvx_host {
+cudaError_t preload_extras_kernels() {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kHandoffStages, kCopyChunk>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kHandoffStages * (int)kCopyChunk)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kWeightStages, kCopyChunk>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kWeightStages * (int)kCopyChunk)) != cudaSuccess)
+        return e;
+    cudaFuncAttributes a;
+    return cudaFuncGetAttributes(&a, (const void*)kvx::kvx_bm_init_kernel);
+}
+}  // namespace kvx_host
+
 extern "C" {
 
 int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n,
@@ -71,11 +93,8 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
     KVX_CUDA(cudaMemcpyAsync(t->d_pieces, t->h_pieces, sizeof(kvx::Piece) * pieces.size(),
                              cudaMemcpyHostToDevice, t->stream));
     KVX_CUDA(cudaEventRecord(t->pieces_free, t->stream));
-    constexpr int kStages = 4;
-    constexpr uint32_t kChunk = 32768;
-    // per-device attribute: set on every call (cheap; the handle's device may differ)
-    KVX_CUDA(cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kStages, kChunk>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * (int)kChunk));
+    constexpr int kStages = kHandoffStages;
+    constexpr uint32_t kChunk = kCopyChunk;  // smem attribute set by preload_extras_kernels
     const unsigned grid = (unsigned)std::min<int64_t>(2 * (int64_t)t->num_sms, (int64_t)pieces.size());
     kvx::kvx_copy_list_kernel<kStages, kChunk><<<grid, kvx::kBulkThreads, kStages * kChunk, t->stream>>>(
         t->d_pieces, (int64_t)pieces.size());
@@ -136,10 +155,9 @@ int kvx_weights_migrate(int32_t device, void* stream, int32_t num_layers, uint64
     KVX_CUDA(A.host_alloc(&h, bytes));
     std::memcpy(h, pieces.data(), bytes);
     KVX_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
-    constexpr int kStages = 6;
-    constexpr uint32_t kChunk = 32768;
-    KVX_CUDA(cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kStages, kChunk>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kStages * (int)kChunk));
+    constexpr int kStages = kWeightStages;
+    constexpr uint32_t kChunk = kCopyChunk;  // smem attribute set by preload_extras_kernels
+    if (const int rc = ensure_loaded(device)) return rc;
     const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms, (int64_t)pieces.size());
     kvx::kvx_copy_list_kernel<kStages, kChunk><<<grid, kvx::kBulkThreads, kStages * kChunk, st>>>(
         static_cast<const kvx::Piece*>(d), (int64_t)pieces.size());
@@ -154,6 +172,7 @@ int kvx_bm_create(int32_t device, int32_t capacity, kvx_blockmgr** out) {
     *out = nullptr;
     DeviceGuard dg(device);
     if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed");
+    if (const int rc = ensure_loaded(device)) return rc;
     auto* bm = new kvx_blockmgr;
     bm->device = device;
     bm->capacity = capacity;

@@ -4,6 +4,13 @@
 
 using namespace kvx_host;
 
+namespace kvx_host {
+cudaError_t preload_pool_kernels() {
+    cudaFuncAttributes a;
+    return cudaFuncGetAttributes(&a, (const void*)kvx::kvx_fill_kernel);
+}
+}  // namespace kvx_host
+
 extern "C" {
 
 // ------------------------------------------------------------------ pools
@@ -16,6 +23,7 @@ int kvx_pool_create(int32_t device, const kvx_geometry* g, int32_t num_layers, i
     if (num_layers < 1 || num_blocks < 1) return fail(KVX_EINVAL, "num_layers/num_blocks must be >= 1");
     DeviceGuard dg(device);
     if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed for pool device");
+    if (const int rc = ensure_loaded(device)) return rc;
     auto* p = new kvx_pool;
     p->device = device;
     p->g = *g;
@@ -72,6 +80,7 @@ int kvx_pool_import(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_BYTES],
     *out = nullptr;
     if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
     DeviceGuard dg(device);
+    if (const int rc = ensure_loaded(device)) return rc;
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle, sizeof(h));
     void* ptr = nullptr;

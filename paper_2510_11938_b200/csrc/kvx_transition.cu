@@ -12,6 +12,22 @@
 
 using namespace kvx_host;
 
+namespace kvx_host {
+cudaError_t preload_transition_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaSuccess;
+    for (const void* fn : {(const void*)kvx::kvx_plan_kernel, (const void*)kvx::kvx_move_kernel,
+                           (const void*)kvx::kvx_move256_kernel, (const void*)kvx::kvx_commit_kernel,
+                           (const void*)kvx::kvx_verify_kernel})
+        if ((e = cudaFuncGetAttributes(&a, fn)) != cudaSuccess) return e;
+    for (const BulkVariant& bv : kBulkVariants)
+        if ((e = cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      bv.stages * (int)bv.chunk)) != cudaSuccess)
+            return e;
+    return e;
+}
+}  // namespace kvx_host
+
 extern "C" {
 
 // ------------------------------------------------------------- transition
@@ -70,6 +86,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
 
     DeviceGuard dg(d->device);
     if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed");
+    if (const int rc = ensure_loaded(d->device)) return rc;
     auto* t = new kvx_transition;
     t->g = g;
     t->device = d->device;

@@ -117,6 +117,7 @@ def _load() -> C.CDLL:
         "kvx_abi_version": (C.c_int, []),
         "kvx_launch_count": (U64, []),
         "kvx_device_count": (C.c_int, [P(I32)]),
+        "kvx_preload": (C.c_int, [I32]),
         "kvx_pool_create": (C.c_int, [I32, P(Geometry), I32, I32, P(VP)]),
         "kvx_pool_wrap": (C.c_int, [I32, VP, U64, P(Geometry), I32, I32, P(VP)]),
         "kvx_pool_export": (C.c_int, [VP, C.c_char_p]),
@@ -207,6 +208,11 @@ def device_count() -> int:
     n = C.c_int32(0)
     rc = _lib.kvx_device_count(C.byref(n))
     return int(n.value) if rc == KVX_OK else 0
+
+
+def preload(device: int) -> None:
+    """Loads every kvx kernel on `device` now (kvx_preload)."""
+    _check(_lib.kvx_preload(device))
 
 
 def geometry(num_layers: int, num_kv_heads: int, head_dim: int = 128, elem_bytes: int = 2,

@@ -196,6 +196,15 @@ def test_shared_blockmgr_across_streams(gpu_count):
         p.zero()
     new = [kvx.Pool(0, g, 2, cap)]
     new[0].zero()
+    # warm-up cycle: every kernel of the path launched once, so no lazy
+    # module load (which waits for the device to go idle) can order the
+    # streams for us below
+    bm = kvx.BlockManager(0, cap)
+    tw = kvx.Transition(g, [], [old[0]], [], new, 0, N, max_blocks, cap, src_bt, dst_blockmgr=bm)
+    tw.wave(np.array([0, 1], np.int32), np.zeros(2, np.int64), np.array([20, 20], np.int64))
+    tw.commit(np.array([0], np.int32), np.array([20], np.int64))
+    tw.close()
+    bm.close()
     bm, ref = kvx.BlockManager(0, cap), O.StackBM(cap)
     sA, sB = torch.cuda.Stream(), torch.cuda.Stream()
     tA = kvx.Transition(g, [], [old[0]], [], new, 0, N, max_blocks, cap, src_bt, stream=sA.cuda_stream,
