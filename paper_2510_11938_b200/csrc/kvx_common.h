@@ -197,7 +197,7 @@ struct kvx_transition {
     enum State { kActive, kCommitPending, kCommitted, kAborted } state = kActive;
 
     // device state
-    int32_t* d_err = nullptr;  // device error word (plan-kernel bounds check)
+    int32_t* d_err = nullptr;  // error word (plan/commit bounds check) in pinned, device-mapped memory
     int32_t src_cap = 0;       // smallest old-pool block count: valid source ids are [0, src_cap)
     int32_t* d_src_bt = nullptr;
     int32_t* d_dst_bt = nullptr;

@@ -171,7 +171,7 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
                 // validation): an id outside its pool becomes an empty run, so the
                 // mover never touches memory out of range; the error word reports it
                 if (sg.src_blk < 0 || sg.src_blk >= src_cap || sg.dst_blk < 0 || sg.dst_blk >= dst_cap) {
-                    atomicOr(err, 1);
+                    *reinterpret_cast<volatile int32_t*>(err) = 1;  // idempotent; err is host-mapped
                     sg.t0 = sg.t1 = 0;
                 }
                 out[k] = sg;

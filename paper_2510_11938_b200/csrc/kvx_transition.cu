@@ -159,8 +159,9 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         A.dev_alloc((void**)&t->d_wave, wave_bytes) != cudaSuccess ||
         A.dev_alloc((void**)&t->d_live, (size_t)d->max_requests) != cudaSuccess ||
         A.dev_alloc((void**)&t->d_commit_out, 4 * sizeof(int64_t)) != cudaSuccess ||
-        A.dev_alloc((void**)&t->d_err, sizeof(int32_t)) != cudaSuccess)
+        A.host_alloc((void**)&t->d_err, sizeof(int32_t)) != cudaSuccess)
         return bail(fail(KVX_ENOSPC, "transition state allocation failed"));
+    *t->d_err = 0;  // pinned, device-mapped error word: no stream op resets or reads it
     t->src_cap = min_old_blocks;  // INT32_MAX when no old pool is visible here (no local sources)
     for (int s = 0; s < 2; ++s)
         if (A.host_alloc((void**)&t->h_wave[s], wave_bytes) != cudaSuccess ||
@@ -170,8 +171,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
             cudaSuccess ||
         cudaMemsetAsync(t->d_dst_bt, 0xff, bt_bytes, t->stream) != cudaSuccess ||
         cudaMemsetAsync(t->d_synced_hi, 0, sizeof(int64_t) * (size_t)d->max_requests, t->stream) !=
-            cudaSuccess ||
-        cudaMemsetAsync(t->d_err, 0, sizeof(int32_t), t->stream) != cudaSuccess)
+            cudaSuccess)
         return bail(fail(KVX_ECUDA, "transition state init"));
 
     // Worst-case wave and commit buffers up front, so no allocation happens
@@ -377,7 +377,7 @@ int kvx_wait(kvx_transition* t, uint64_t epoch, double* measured_ms) {
     DeviceGuard dg(t->device);
     KVX_CUDA(cudaStreamSynchronize(t->stream));
     int32_t err = 0;
-    KVX_CUDA(cudaMemcpy(&err, t->d_err, sizeof(err), cudaMemcpyDeviceToHost));
+    err = *reinterpret_cast<volatile int32_t*>(t->d_err);  // zero-copy word; the stream has drained
     if (err) return fail(KVX_ECUDA, "device bounds check failed: a wave referenced a block outside its pool");
     float ms = 0.f;
     if (t->timing_open) {
@@ -545,7 +545,7 @@ int kvx_destroy(kvx_transition* t) {
     A.dev_free(t->d_live, (size_t)t->max_requests);
     A.dev_free(t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap);
     A.dev_free(t->d_commit_out, 4 * sizeof(int64_t));
-    A.dev_free(t->d_err, sizeof(int32_t));
+    A.host_free(t->d_err, sizeof(int32_t));
     A.host_free(t->h_commit, t->h_commit_bytes);
     A.event_free(t->ev_commit, false);
     for (int s = 0; s < 2; ++s) {
@@ -624,12 +624,14 @@ int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_
         max_tok = std::max(max_tok, kv[i]);
     }
     if (max_tok == 0) return KVX_OK;
+    // scratch from the arena: cudaMalloc / cudaFree would synchronise the device
+    kvx::Arena& A = kvx::Arena::of(t->device);
     int32_t* d_req = nullptr;
     int64_t* d_kv = nullptr;
     unsigned long long* d_bad = nullptr;
-    KVX_CUDA(cudaMalloc(&d_req, sizeof(int32_t) * n));
-    KVX_CUDA(cudaMalloc(&d_kv, sizeof(int64_t) * n));
-    KVX_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+    KVX_CUDA(A.dev_alloc((void**)&d_req, sizeof(int32_t) * n));
+    KVX_CUDA(A.dev_alloc((void**)&d_kv, sizeof(int64_t) * n));
+    KVX_CUDA(A.dev_alloc((void**)&d_bad, sizeof(unsigned long long)));
     KVX_CUDA(cudaMemcpyAsync(d_req, req, sizeof(int32_t) * n, cudaMemcpyHostToDevice, t->stream));
     KVX_CUDA(cudaMemcpyAsync(d_kv, kv, sizeof(int64_t) * n, cudaMemcpyHostToDevice, t->stream));
     KVX_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), t->stream));
@@ -645,9 +647,9 @@ int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_
     unsigned long long bad = 0;
     KVX_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, t->stream));
     KVX_CUDA(cudaStreamSynchronize(t->stream));
-    cudaFree(d_req);
-    cudaFree(d_kv);
-    cudaFree(d_bad);
+    A.dev_free(d_req, sizeof(int32_t) * n);
+    A.dev_free(d_kv, sizeof(int64_t) * n);
+    A.dev_free(d_bad, sizeof(unsigned long long));
     *mismatched_words = (int64_t)bad;
     return KVX_OK;
 }
