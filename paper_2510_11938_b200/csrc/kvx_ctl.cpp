@@ -35,21 +35,29 @@ int64_t unsynced(const CtlState& c, int32_t n, const int32_t* req, const int64_t
 
 // snapshot_sync_targets (engine.cpp:548-556) + the device wave over
 // [synced, target) of every snapshotted request.
+// The mirror is updated only once kvx_wave accepted the wave, so a refused
+// wave (e.g. KVX_ENOSPC -> hold / abort) leaves no target behind that a later
+// apply() would count as synced.
 int snapshot_and_issue(kvx_transition* t, int32_t n, const int32_t* req, const int64_t* kv) {
     CtlState& c = kvx::ctl_of(t);
+    std::vector<int64_t> lo((size_t)n), hi((size_t)n);
+    for (int32_t i = 0; i < n; ++i) {
+        const size_t r = (size_t)req[i];
+        lo[(size_t)i] = c.synced[r];
+        hi[(size_t)i] = std::max(kv[i], c.synced[r]);
+    }
+    const int rc = kvx_wave(t, kvx::epoch_of(t), n, req, lo.data(), hi.data());
+    if (rc != KVX_OK) return rc;
     for (int32_t k : c.target_keys) c.in_target[(size_t)k] = 0;
     c.target_keys.clear();
-    std::vector<int64_t> lo((size_t)n), hi((size_t)n);
     for (int32_t i = 0; i < n; ++i) {
         const size_t r = (size_t)req[i];
         c.target[r] = kv[i];
         c.in_target[r] = 1;
         c.target_keys.push_back(req[i]);
-        lo[(size_t)i] = c.synced[r];
-        hi[(size_t)i] = std::max(kv[i], c.synced[r]);
     }
     ++c.waves;
-    return kvx_wave(t, kvx::epoch_of(t), n, req, lo.data(), hi.data());
+    return KVX_OK;
 }
 
 // engine.cpp:657-662 / 697-702
@@ -96,9 +104,9 @@ int kvx_ctl_sync_complete(kvx_transition* t, uint64_t epoch, int32_t n, const in
     if (!c.barrier) {
         const int64_t delta = unsynced(c, n, req, kv);
         if (delta > 0 && c.rounds < c.max_sync_rounds) {
-            ++c.rounds;
             const int rc = snapshot_and_issue(t, n, req, kv);
             if (rc != KVX_OK) return rc;
+            ++c.rounds;
             c.kv_synced_bytes += (double)delta * c.kv_bytes_per_token;  // engine.cpp:671
             c.last_wave_tokens = delta;
             if (tokens_out) *tokens_out = delta;

@@ -133,6 +133,29 @@ def test_destination_full_is_enospc(gpu_count):
         m.close()
 
 
+def test_refused_control_wave_leaves_the_mirror_untouched(gpu_count):
+    """A delta wave refused for space (KVX_ENOSPC -> the engine holds or
+    aborts) must not leave targets behind: request 1 never moved, so the
+    commit's Eq. 10 counts it as a violation, on the device and the mirror."""
+    m = Mini([48, 32, 0, 0], dst_blocks=4)
+    try:
+        live0 = (np.array([0], np.int32), np.array([48], np.int64))
+        live01 = (np.array([0, 1], np.int32), np.array([48, 32], np.int64))
+        m.tr.begin_refactor(live0)                                    # 3 blocks
+        before = m.tr.ctl_state()
+        with pytest.raises(kvx.NoSpace):
+            m.tr.on_kv_sync_complete(live01, 0)                       # delta needs 2 more > 4
+        after = m.tr.ctl_state()
+        assert (after["rounds"], after["waves"], after["kv_synced_bytes"]) == \
+               (before["rounds"], before["waves"], before["kv_synced_bytes"])
+        act, tok = m.tr.on_kv_sync_complete(live0, 0)                 # request 1 dropped meanwhile
+        assert act == kvx.ACT_FINAL and tok == 0
+        res = m.tr.on_refactor_commit(live01)                         # but it is live at commit
+        assert res.violations == 1
+    finally:
+        m.close()
+
+
 def test_abort_drops_destination_and_invalidates_epoch(gpu_count):
     m = Mini([40, 20, 0, 0])
     try:
