@@ -652,27 +652,29 @@ kvx_fill_kernel(char* __restrict__ pool, int32_t pool_blocks, int32_t first_laye
                 const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
                 int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed,
                 const int64_t* __restrict__ from = nullptr) {
-    const int32_t i = blockIdx.x, b = blockIdx.y;
+    const int32_t i = blockIdx.x;
     const int32_t r = req[i];
-    int64_t t_begin = (int64_t)b * block_tokens;
-    if (t_begin >= tokens[i]) return;
-    const int64_t t_end = min(tokens[i], t_begin + block_tokens);
-    if (from) {
-        if (t_end <= from[i]) return;
-        t_begin = max(t_begin, from[i]);
-    }
-    const int32_t blk = bt[(int64_t)r * max_blocks + b];
     const uint64_t block_bytes = 2ull * block_tokens * token_bytes;
     const uint32_t vecs = (uint32_t)(token_bytes >> 4);
-    const int32_t rows = (int32_t)(t_end - t_begin);
-    const int32_t row0 = (int32_t)(t_begin - (int64_t)b * block_tokens);  // first row inside the block
-    for (int32_t l = 0; l < num_layers; ++l) {
-        char* slab = pool + ((uint64_t)l * pool_blocks + blk) * block_bytes;
-        for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
-            const int32_t kvi = kvr / rows, t = kvr % rows;
-            const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
-            uint4* row = reinterpret_cast<uint4*>(slab + ((uint64_t)kvi * block_tokens + row0 + t) * token_bytes);
-            for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) row[v] = pattern_vec(th, v);
+    for (int32_t b = blockIdx.y; (int64_t)b * block_tokens < tokens[i]; b += gridDim.y) {  // grid.y <= 65535
+        int64_t t_begin = (int64_t)b * block_tokens;
+        const int64_t t_end = min(tokens[i], t_begin + block_tokens);
+        if (from) {
+            if (t_end <= from[i]) continue;
+            t_begin = max(t_begin, from[i]);
+        }
+        const int32_t blk = bt[(int64_t)r * max_blocks + b];
+        const int32_t rows = (int32_t)(t_end - t_begin);
+        const int32_t row0 = (int32_t)(t_begin - (int64_t)b * block_tokens);  // first row inside the block
+        for (int32_t l = 0; l < num_layers; ++l) {
+            char* slab = pool + ((uint64_t)l * pool_blocks + blk) * block_bytes;
+            for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
+                const int32_t kvi = kvr / rows, t = kvr % rows;
+                const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
+                uint4* row =
+                    reinterpret_cast<uint4*>(slab + ((uint64_t)kvi * block_tokens + row0 + t) * token_bytes);
+                for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) row[v] = pattern_vec(th, v);
+            }
         }
     }
 }
@@ -683,19 +685,20 @@ kvx_verify_kernel(const char* __restrict__ pool, int32_t pool_blocks, int32_t fi
                   const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
                   int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed,
                   unsigned long long* __restrict__ mismatches) {
-    const int32_t i = blockIdx.x, b = blockIdx.y;
+    const int32_t i = blockIdx.x;
     const int32_t r = req[i];
-    const int64_t t_begin = (int64_t)b * block_tokens;
-    if (t_begin >= tokens[i]) return;
-    const int64_t t_end = min(tokens[i], t_begin + block_tokens);
-    const int32_t blk = bt[(int64_t)r * max_blocks + b];
     const uint32_t vecs = (uint32_t)(token_bytes >> 4);
-    const int32_t rows = (int32_t)(t_end - t_begin);
+    const uint64_t block_bytes = 2ull * block_tokens * token_bytes;
     unsigned long long bad = 0;
-    if (blk < 0) {
-        bad = threadIdx.x == 0 ? (unsigned long long)num_layers * 2 * rows * vecs * 8 : 0;
-    } else {
-        const uint64_t block_bytes = 2ull * block_tokens * token_bytes;
+    for (int32_t b = blockIdx.y; (int64_t)b * block_tokens < tokens[i]; b += gridDim.y) {  // grid.y <= 65535
+        const int64_t t_begin = (int64_t)b * block_tokens;
+        const int64_t t_end = min(tokens[i], t_begin + block_tokens);
+        const int32_t blk = bt[(int64_t)r * max_blocks + b];
+        const int32_t rows = (int32_t)(t_end - t_begin);
+        if (blk < 0) {
+            bad += threadIdx.x == 0 ? (unsigned long long)num_layers * 2 * rows * vecs * 8 : 0;
+            continue;
+        }
         for (int32_t l = 0; l < num_layers; ++l) {
             const char* slab = pool + ((uint64_t)l * pool_blocks + blk) * block_bytes;
             for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {

@@ -175,7 +175,7 @@ int kvx_pool_fill_pattern(kvx_pool* p, uint64_t seed, int32_t first_layer, int32
     KVX_CUDA(cudaMemcpy(sc.req, req, sc.nreq, cudaMemcpyHostToDevice));
     KVX_CUDA(cudaMemcpy(sc.tok, tokens, sc.ntok, cudaMemcpyHostToDevice));
     KVX_CUDA(cudaMemcpy(sc.bt, bt, sc.nbt, cudaMemcpyHostToDevice));
-    dim3 grid((unsigned)n, (unsigned)cdiv64(max_tok, p->g.block_tokens));
+    dim3 grid((unsigned)n, (unsigned)std::min<int64_t>(65535, cdiv64(max_tok, p->g.block_tokens)));
     kvx::kvx_fill_kernel<<<grid, 256>>>(p->base, p->num_blocks, first_layer, p->num_layers,
                                         static_cast<const int32_t*>(sc.req), static_cast<const int64_t*>(sc.tok),
                                         static_cast<const int32_t*>(sc.bt), max_blocks, p->g.block_tokens,
@@ -220,7 +220,7 @@ int kvx_pool_append_pattern(kvx_pool* p, void* stream, uint64_t seed, int32_t fi
     std::memcpy(hc + o_bt, bt, bytes - o_bt);
     KVX_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
     char* dc = static_cast<char*>(d);
-    dim3 grid((unsigned)n, (unsigned)cdiv64(max_tok, p->g.block_tokens));
+    dim3 grid((unsigned)n, (unsigned)std::min<int64_t>(65535, cdiv64(max_tok, p->g.block_tokens)));
     kvx::kvx_fill_kernel<<<grid, 256, 0, st>>>(p->base, p->num_blocks, first_layer, p->num_layers,
                                                reinterpret_cast<const int32_t*>(dc),
                                                reinterpret_cast<const int64_t*>(dc + o_to),

@@ -635,7 +635,7 @@ int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_
     KVX_CUDA(cudaMemcpyAsync(d_req, req, sizeof(int32_t) * n, cudaMemcpyHostToDevice, t->stream));
     KVX_CUDA(cudaMemcpyAsync(d_kv, kv, sizeof(int64_t) * n, cudaMemcpyHostToDevice, t->stream));
     KVX_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), t->stream));
-    dim3 grid((unsigned)n, (unsigned)cdiv64(max_tok, t->g.block_tokens));
+    dim3 grid((unsigned)n, (unsigned)std::min<int64_t>(65535, cdiv64(max_tok, t->g.block_tokens)));
     for (size_t k = 0; k < t->new_pools.size(); ++k) {
         const kvx_pool* p = t->new_pools[k];
         if (!p || p->imported) continue;  // the owning rank verifies it

@@ -230,3 +230,35 @@ m.close()
                ROOT=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
     assert "CAUGHT -4 True" in out.stdout, out.stdout + out.stderr
+
+
+def test_request_longer_than_grid_y(gpu_count):
+    """One request of 1.1M tokens = 68,750 blocks (> 65,535, the grid.y
+    limit of the payload kernels, which stride over blocks): fill, move,
+    commit and verify, bytes compared with the oracle."""
+    L, T = 2, 1_100_000
+    g, og = kvx.geometry(L, 1, 8), O.geo(L, 1, 8)          # 16 B tokens, 512 B blocks
+    mb = (T + 15) // 16
+    tokens = np.array([T], np.int64)
+    src_bt, cap0 = W.fragmented_block_table(tokens, mb, 16, seed=5, slack=0.0)
+    live = np.array([0], np.int32)
+    old = [kvx.Pool(0, g, 1, cap0) for _ in range(2)]
+    for k, p in enumerate(old):
+        p.zero()
+        p.fill_pattern(SEED, k, live, tokens, src_bt)
+    new = [kvx.Pool(0, g, L, mb)]
+    new[0].zero()
+    tr = kvx.Transition(g, [1], old, [], new, 0, 1, mb, mb, src_bt)
+    dp = O.DataPlane(og, [1], [], cap0, mb, 1, mb, src_bt)
+    dp.fill_source(SEED, live, tokens)
+    try:
+        tr.wave(live, [0], [T])
+        assert dp.wave(live, [0], [T]) == 0
+        tr.wait()
+        np.testing.assert_array_equal(new[0].read(), dp.new_pools[0])
+        assert tr.commit(live, tokens).violations == 0
+        assert tr.verify_pattern(SEED, live, tokens) == 0
+    finally:
+        tr.close()
+        for p in old + new:
+            p.close()
