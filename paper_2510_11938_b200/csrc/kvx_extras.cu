@@ -79,12 +79,12 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
     if (!t->pieces_free) KVX_CUDA(A.event(&t->pieces_free, false));
     KVX_CUDA(cudaEventSynchronize(t->pieces_free));  // previous handoff's upload consumed
     if ((int64_t)pieces.size() > t->piece_cap) {
+        KVX_CUDA(cudaStreamSynchronize(t->stream));  // a previous copy-list kernel may still read them
         A.dev_free(t->d_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
         A.host_free(t->h_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
         t->d_pieces = nullptr;
         t->h_pieces = nullptr;
         const int64_t cap = (int64_t)(kvx::size_class(sizeof(kvx::Piece) * pieces.size()) / sizeof(kvx::Piece));
-        KVX_CUDA(cudaStreamSynchronize(t->stream));
         KVX_CUDA(A.dev_alloc((void**)&t->d_pieces, sizeof(kvx::Piece) * (size_t)cap));
         KVX_CUDA(A.host_alloc((void**)&t->h_pieces, sizeof(kvx::Piece) * (size_t)cap));
         t->piece_cap = cap;
@@ -119,17 +119,20 @@ int kvx_weights_migrate(int32_t device, void* stream, int32_t num_layers, uint64
     np2.pools = &dummy;
     if (!plan_ok(op2, num_layers, &why, &ob)) return fail(KVX_EINVAL, "weights old plan: " + why);
     if (!plan_ok(np2, num_layers, &why, &nb)) return fail(KVX_EINVAL, "weights new plan: " + why);
+    // validate every layer before anything is enqueued (nothing half-applied)
+    for (int32_t l = 0; l < num_layers; ++l) {
+        if (!new_ptrs[stage_of_layer(nb, l)]) return fail(KVX_EINVAL, "weights: every new stage buffer is required");
+        if (from_host && from_host[l] && !host_cache)
+            return fail(KVX_EINVAL, "weights: from_host without a host cache");
+    }
     std::vector<kvx::Piece> pieces;
     uint64_t dev_b = 0, host_b = 0;
     DeviceGuard dg(device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     for (int32_t l = 0; l < num_layers; ++l) {
         const int so = stage_of_layer(ob, l), sn = stage_of_layer(nb, l);
-        char* dst = static_cast<char*>(new_ptrs[sn]);
-        if (!dst) return fail(KVX_EINVAL, "weights: every new stage buffer is required");
-        dst += (uint64_t)(l - stage_begin(nb, sn)) * layer_bytes;
+        char* dst = static_cast<char*>(new_ptrs[sn]) + (uint64_t)(l - stage_begin(nb, sn)) * layer_bytes;
         if (from_host && from_host[l]) {
-            if (!host_cache) return fail(KVX_EINVAL, "weights: from_host without a host cache");
             // host tier: only the rank that would otherwise source the layer loads it
             if (!old_ptrs[so]) continue;
             KVX_CUDA(cudaMemcpyAsync(dst, static_cast<const char*>(host_cache) + (uint64_t)l * layer_bytes,
