@@ -226,7 +226,17 @@ def stage_ranges(num_layers: int, boundaries: Sequence[int]) -> list:
     return [(cuts[k], cuts[k + 1]) for k in range(len(cuts) - 1)]
 
 
-class Pool:
+class _Handle:
+    """close() on scope exit: ``with kvx.Pool(...) as p: ...``."""
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
+
+class Pool(_Handle):
     """One stage's paged KV pool on one GPU (local or imported from a peer)."""
 
     def __init__(self, device: int, geom: Geometry, num_layers: int, num_blocks: int,
@@ -315,7 +325,7 @@ class Pool:
             pass
 
 
-class BlockManager:
+class BlockManager(_Handle):
     """Device-resident free list of one pool set (kvx_bm_*)."""
 
     def __init__(self, device: int, capacity: int):
@@ -370,7 +380,7 @@ class CommitResult:
     free_list: np.ndarray
 
 
-class Transition:
+class Transition(_Handle):
     """One inflight refactor of one pipeline instance (RefactorCtx,
     engine.hpp:149-158), on one local GPU."""
 
