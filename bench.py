@@ -16,8 +16,10 @@ block-table compaction).  All through the kvx C-ABI (include/kvx.h).
             descriptors H2D, the commit result (violations + compacted block
             table + free list) D2H, host wall clock.
   stall_ms  barrier -> commit done (final wave + commit), engine.cpp:676-686.
-  roofline  dominant kernel = kvx_move_kernel of wave 0: algorithmic
-            read+write bytes / its CUDA-event duration vs MEASURED_PEAKS hbm_gbs.
+  roofline  dominant kernel = the TMA bulk mover (kvx_bulk_kernel) of wave 0:
+            algorithmic read+write bytes / its CUDA-event duration vs
+            MEASURED_PEAKS hbm_gbs (N>1: vs the HBM / NVLink bound of the
+            busiest GPU); traffic from the committed ncu capture.
 
 `--impl reference` times the reference's CPU path for the same metric: the
 oracle restatement (oracle/kvx_oracle.c, all host threads) on a bounded
