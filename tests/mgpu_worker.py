@@ -47,91 +47,106 @@ def cpu_worker(rank, world, port, out):
         out.put((rank, "err", traceback.format_exc()))
 
 
-def gpu_worker(rank, world, port, name, heads, dim, mode, pull, out):
+def gpu_worker(rank, world, port, name, heads, dim, mode, pull, stride, out):
+    """stride=0: the scenario's last committed transition; stride=k: every
+    k-th transition of the scenario (e.g. the controller-chosen chain)."""
     try:
         dist = _init(rank, world, port)
-        import numpy as np
-        from oracle import pyoracle as O
-        from paper_2510_11938_b200 import kvx
-        from paper_2510_11938_b200 import shard as S
         from paper_2510_11938_b200 import workload as W
-        from tests.replay import replay
 
         scn = W.load_golden(name)
-        t = [x for x in scn.transitions if x.outcome == "commit"][-1]
-        L = scn.num_layers
-        g = kvx.geometry(L, heads, dim)
-        N = scn.num_requests
-        tokens = t.max_tokens(N)
-        max_blocks = int(max(1, (tokens.max() + 15) // 16))
-        src_bt, old_blocks = W.fragmented_block_table(tokens, max_blocks, 16, seed=7)
-        dst_blocks = max(1, int(((tokens + 15) // 16).sum()))
-        live = np.nonzero(tokens)[0].astype(np.int32)
-        old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, world, mode)
+        ts = [[x for x in scn.transitions if x.outcome == "commit"][-1]] if not stride \
+            else scn.transitions[::stride]
+        checked, moved = 0, 0
+        for t in ts:
+            c, m, old_dev, new_dev = _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull)
+            checked += c
+            moved += m
+        dist.destroy_process_group()
+        out.put((rank, "ok", {"checked": checked, "moved": moved, "old_dev": old_dev,
+                              "new_dev": new_dev, "transitions": len(ts)}))
+    except Exception:
+        out.put((rank, "err", traceback.format_exc()))
 
-        def gather(obj):
-            o = [None] * world
-            dist.all_gather_object(o, obj)
-            return o
 
-        old_pools, new_pools = S.setup_rank_pools(
-            kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, rank, old_blocks,
-            dst_blocks, all_gather=gather, fill=(SEED, live, tokens[live], src_bt), pull=pull)
-        dist.barrier()
-        tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, rank, N,
-                            max_blocks, dst_blocks, src_bt, epoch=t.epoch,
-                            max_sync_rounds=scn.max_sync_rounds,
-                            kv_bytes_per_token=scn.kv_bytes_per_token, pull=pull)
-        octx = O.ControlCtx(N, scn.max_sync_rounds, scn.kv_bytes_per_token)
-        dp = O.DataPlane(O.geo(L, heads, dim), t.old_boundaries, t.new_boundaries, old_blocks,
-                         dst_blocks, N, max_blocks, src_bt)
-        dp.fill_source(SEED, live, tokens[live])
+def _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull):
+    import numpy as np
+    from oracle import pyoracle as O
+    from paper_2510_11938_b200 import kvx
+    from paper_2510_11938_b200 import shard as S
+    from paper_2510_11938_b200 import workload as W
+    from tests.replay import replay
 
-        class Shim:
-            def begin(self, req, kv):
-                tr.begin_refactor((req, kv))
-                r = octx.begin(req, kv)
-                assert dp.wave(req, r[1], r[2]) == 0
-                return r
+    L = scn.num_layers
+    g = kvx.geometry(L, heads, dim)
+    N = scn.num_requests
+    tokens = t.max_tokens(N)
+    max_blocks = int(max(1, (tokens.max() + 15) // 16))
+    src_bt, old_blocks = W.fragmented_block_table(tokens, max_blocks, 16, seed=7)
+    dst_blocks = max(1, int(((tokens + 15) // 16).sum()))
+    live = np.nonzero(tokens)[0].astype(np.int32)
+    old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, world, mode)
 
-            def on_sync_complete(self, req, kv, inflight):
-                act, tok = tr.on_kv_sync_complete((req, kv), inflight)
-                r = octx.on_sync_complete(req, kv, inflight)
-                assert (act, tok) == (r[0], r[1])
-                if act != kvx.ACT_BARRIER_WAIT:
-                    assert dp.wave(req, r[2], r[3]) == 0
-                return r
+    def gather(obj):
+        o = [None] * world
+        dist.all_gather_object(o, obj)
+        return o
 
-        for _ in replay(Shim(), t):
-            pass
+    old_pools, new_pools = S.setup_rank_pools(
+        kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, rank, old_blocks,
+        dst_blocks, all_gather=gather, fill=(SEED, live, tokens[live], src_bt), pull=pull)
+    dist.barrier()
+    tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, rank, N,
+                        max_blocks, dst_blocks, src_bt, epoch=t.epoch,
+                        max_sync_rounds=scn.max_sync_rounds,
+                        kv_bytes_per_token=scn.kv_bytes_per_token, pull=pull)
+    octx = O.ControlCtx(N, scn.max_sync_rounds, scn.kv_bytes_per_token)
+    dp = O.DataPlane(O.geo(L, heads, dim), t.old_boundaries, t.new_boundaries, old_blocks,
+                     dst_blocks, N, max_blocks, src_bt)
+    dp.fill_source(SEED, live, tokens[live])
+
+    class Shim:
+        def begin(self, req, kv):
+            tr.begin_refactor((req, kv))
+            r = octx.begin(req, kv)
+            assert dp.wave(req, r[1], r[2]) == 0
+            return r
+
+        def on_sync_complete(self, req, kv, inflight):
+            act, tok = tr.on_kv_sync_complete((req, kv), inflight)
+            r = octx.on_sync_complete(req, kv, inflight)
+            assert (act, tok) == (r[0], r[1])
+            if act != kvx.ACT_BARRIER_WAIT:
+                assert dp.wave(req, r[2], r[3]) == 0
+            return r
+
+    for _ in replay(Shim(), t):
+        pass
+    if t.outcome == "commit":
         res = tr.on_refactor_commit((t.live_req, t.live_kv))
         ov, row_ptr, blocks, free = dp.commit(t.live_req, t.live_kv)
         assert res.violations == ov == t.violations
         assert np.array_equal(res.blocks, blocks) and np.array_equal(res.free_list, free)
-        assert np.array_equal(tr.dst_block_table(), dp.bt)
-        dist.barrier()  # every rank's pushes have landed (kernels end with a system fence)
-        checked = 0
-        for j, p in enumerate(new_pools):
-            if new_dev[j] == rank:
-                got = p.read()
-                assert np.array_equal(got, dp.new_pools[j]), f"new stage {j} differs on rank {rank}"
-                checked += 1
-        moved = tr.bytes_moved()
-        tr.close()
-        dist.barrier()
-        for p in old_pools + new_pools:      # unmap peers' pools first ...
-            if p is not None and p.imported:
-                p.close()
-        dist.barrier()
-        for p in old_pools + new_pools:      # ... then free our own
-            if p is not None and not p.imported:
-                p.close()
-        dist.barrier()
-        dist.destroy_process_group()
-        out.put((rank, "ok", {"checked": checked, "moved": moved, "old_dev": old_dev,
-                              "new_dev": new_dev}))
-    except Exception:
-        out.put((rank, "err", traceback.format_exc()))
+    assert np.array_equal(tr.dst_block_table(), dp.bt)
+    dist.barrier()  # every rank's pushes have landed (kernels end with a system fence)
+    checked = 0
+    for j, p in enumerate(new_pools):
+        if new_dev[j] == rank:
+            got = p.read()
+            assert np.array_equal(got, dp.new_pools[j]), f"new stage {j} differs on rank {rank}"
+            checked += 1
+    moved = tr.bytes_moved()
+    tr.close()
+    dist.barrier()
+    for p in old_pools + new_pools:      # unmap peers' pools first ...
+        if p is not None and p.imported:
+            p.close()
+    dist.barrier()
+    for p in old_pools + new_pools:      # ... then free our own
+        if p is not None and not p.imported:
+            p.close()
+    dist.barrier()
+    return checked, moved, old_dev, new_dev
 
 
 def handoff_worker(rank, world, port, out):

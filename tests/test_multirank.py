@@ -53,8 +53,22 @@ def test_ranks_shard_every_layer_once_cpu(world):
 def test_two_gpu_transition_bit_exact(gpu_count, mode, name, heads, dim, pull):
     if gpu_count < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
-    res = _run(mgpu_worker.gpu_worker, 2, name, heads, dim, mode, pull)
+    res = _run(mgpu_worker.gpu_worker, 2, name, heads, dim, mode, pull, 0)
     assert sum(r["checked"] for r in res.values()) >= 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["affinity", "spread"])
+def test_two_gpu_controller_chain_bit_exact(gpu_count, mode):
+    """BASELINE C5 across 2 GPUs: every 4th transition of the refactor chain
+    the reference's own controller chose on the CV=7 gamma trace (4->16,
+    16<->8 re-cuts; tests/golden/adaptive_cv7.jsonl), each pushed over
+    NVLink and compared with the oracle byte for byte."""
+    if gpu_count < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    res = _run(mgpu_worker.gpu_worker, 2, "adaptive_cv7", 1, 8, mode, False, 4)
+    assert all(r["transitions"] == 10 for r in res.values())
+    assert sum(r["checked"] for r in res.values()) >= 10
 
 
 @pytest.mark.gpu
