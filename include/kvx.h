@@ -102,6 +102,33 @@ int kvx_pool_export(const kvx_pool* p, uint8_t handle[KVX_IPC_HANDLE_BYTES]);
 int kvx_pool_import(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_BYTES],
                     const kvx_geometry* g, int32_t num_layers, int32_t num_blocks,
                     kvx_pool** out);
+
+/* Per-layer KV layouts.  A transition reads and writes each pool in its own
+ * layout, so a refactor can also convert the cache between serving backends.
+ *   KVX_LAYOUT_BLOCKS    layer = [num_blocks][2][block_tokens][H][D]: K and V
+ *                        rows of a block side by side (FlashInfer NHD paged
+ *                        cache; the default of every call above)
+ *   KVX_LAYOUT_KV_PLANES layer = [2][num_blocks][block_tokens][H][D]: a K plane
+ *                        and a V plane (FlashAttention paged cache) */
+#define KVX_LAYOUT_BLOCKS 0
+#define KVX_LAYOUT_KV_PLANES 1
+/* kvx_pool_create / _import with an explicit per-layer layout (one
+ * allocation, layers back to back). */
+int kvx_pool_create_layout(int32_t device, const kvx_geometry* g, int32_t num_layers,
+                           int32_t num_blocks, int32_t layout, kvx_pool** out);
+int kvx_pool_import_layout(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_BYTES],
+                           const kvx_geometry* g, int32_t num_layers, int32_t num_blocks,
+                           int32_t layout, kvx_pool** out);
+/* A pool over one caller-owned allocation PER LAYER, as serving engines keep
+ * their caches (e.g. one [2, num_blocks, block, H, D] tensor per layer):
+ * layer_ptrs[l] holds >= num_blocks * 2 * block_tokens * token_bytes bytes
+ * (layer_bytes), 16-byte aligned, on `device`.  Not freed by destroy; not
+ * readable through kvx_pool_read / _write (no single allocation), not
+ * exportable. */
+int kvx_pool_wrap_layers(int32_t device, int32_t num_layers, void* const* layer_ptrs,
+                         uint64_t layer_bytes, const kvx_geometry* g, int32_t num_blocks,
+                         int32_t layout, kvx_pool** out);
+int kvx_pool_layout(const kvx_pool* p, int32_t* layout);
 int kvx_pool_info(const kvx_pool* p, void** dptr, uint64_t* bytes, int32_t* device,
                   int32_t* imported);
 int kvx_pool_destroy(kvx_pool* p);

@@ -68,6 +68,8 @@ inline bool geometry_ok(const kvx_geometry* g, std::string* why) {
     return true;
 }
 
+inline bool layout_ok(int32_t layout) { return layout == KVX_LAYOUT_BLOCKS || layout == KVX_LAYOUT_KV_PLANES; }
+
 inline uint64_t token_bytes(const kvx_geometry& g) {
     return (uint64_t)g.num_kv_heads * (uint64_t)g.head_dim * (uint64_t)g.elem_bytes;
 }
@@ -146,12 +148,35 @@ struct kvx_pool {
     int32_t device = -1;
     bool imported = false;
     bool wrapped = false;  // caller-owned memory
-    char* base = nullptr;
+    bool per_layer = false;  // kvx_pool_wrap_layers: one allocation per layer
+    char* base = nullptr;    // single allocation (layer 0 of a per-layer pool)
     uint64_t bytes = 0;
     kvx_geometry g{};
     int32_t num_layers = 0;
     int32_t num_blocks = 0;
+    int32_t layout = KVX_LAYOUT_BLOCKS;
+    std::vector<char*> layer_base;  // per layer, in every pool
+
+    uint64_t layer_bytes() const { return (uint64_t)num_blocks * 2ull * g.block_tokens * kvx_host::token_bytes(g); }
+    // bytes between consecutive blocks of a layer, and from a block's K rows to its V rows
+    uint64_t blk_stride() const {
+        const uint64_t plane = (uint64_t)g.block_tokens * kvx_host::token_bytes(g);
+        return layout == KVX_LAYOUT_KV_PLANES ? plane : 2 * plane;
+    }
+    uint64_t kv_stride() const {
+        const uint64_t plane = (uint64_t)g.block_tokens * kvx_host::token_bytes(g);
+        return layout == KVX_LAYOUT_KV_PLANES ? (uint64_t)num_blocks * plane : plane;
+    }
+    void set_contiguous_layers() {
+        layer_base.resize((size_t)num_layers);
+        for (int32_t l = 0; l < num_layers; ++l) layer_base[(size_t)l] = base + (uint64_t)l * layer_bytes();
+    }
 };
+
+// A pool's addressing for the payload kernels; d_layers = its layer_base on the device.
+inline kvx::PoolAddr pool_addr(const kvx_pool* p, char* const* d_layers) {
+    return kvx::PoolAddr{d_layers, p->blk_stride(), p->kv_stride()};
+}
 
 // Device-resident block manager: a free-id stack on the GPU, its top mirrored
 // on the host so every capacity decision is synchronous and deterministic.

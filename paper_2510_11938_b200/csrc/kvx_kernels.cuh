@@ -44,9 +44,16 @@ struct Seg {  // one logical block of one request inside one wave
     int32_t t1;  // one past the last token
 };
 
-struct LayerPtr {  // base of layer l's slab array in the old / new pool
+struct LayerPtr {  // layer l in the old / new pool: base, block stride, K->V offset
     char* src;
     char* dst;
+    uint64_t src_bs, dst_bs;  // bytes between consecutive blocks (layout-dependent)
+    uint64_t src_kv, dst_kv;  // bytes from a block's K rows to its V rows
+};
+
+struct PoolAddr {  // one pool for the payload kernels: per-layer bases + strides
+    char* const* layer;  // device array, one base per layer
+    uint64_t blk_stride, kv_stride;
 };
 
 // ---------------------------------------------------------------- payload
@@ -263,15 +270,16 @@ kvx_move256_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* _
         const int32_t layer = (int32_t)(u / nseg);
         const Seg sg = segs[u - (int64_t)layer * nseg];
         const LayerPtr lp = layers[layer];
-        const char* src = lp.src + (uint64_t)sg.src_blk * block_bytes;
-        char* dst = lp.dst + (uint64_t)sg.dst_blk * block_bytes;
-        if (sg.t0 == 0 && sg.t1 == block_tokens) {
+        const char* src = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
+        char* dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
+        if (sg.t0 == 0 && sg.t1 == block_tokens && lp.src_kv == half && lp.dst_kv == half) {
             cta_copy256(reinterpret_cast<V8*>(dst), reinterpret_cast<const V8*>(src), (uint32_t)(block_bytes >> 5));
         } else {
             const uint64_t off = (uint64_t)sg.t0 * token_bytes;
             const uint32_t n = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * token_bytes) >> 5);
             cta_copy256(reinterpret_cast<V8*>(dst + off), reinterpret_cast<const V8*>(src + off), n);
-            cta_copy256(reinterpret_cast<V8*>(dst + half + off), reinterpret_cast<const V8*>(src + half + off), n);
+            cta_copy256(reinterpret_cast<V8*>(dst + lp.dst_kv + off), reinterpret_cast<const V8*>(src + lp.src_kv + off),
+                        n);
         }
     }
     if (fence_system) __threadfence_system();
@@ -293,9 +301,9 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
         const int32_t layer = (int32_t)(u / nseg);
         const Seg sg = segs[u - (int64_t)layer * nseg];
         const LayerPtr lp = layers[layer];
-        const char* src = lp.src + (uint64_t)sg.src_blk * block_bytes;
-        char* dst = lp.dst + (uint64_t)sg.dst_blk * block_bytes;
-        if (sg.t0 == 0 && sg.t1 == block_tokens) {
+        const char* src = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
+        char* dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
+        if (sg.t0 == 0 && sg.t1 == block_tokens && lp.src_kv == half && lp.dst_kv == half) {
             cta_copy(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src),
                      (uint32_t)(block_bytes >> 4));
         } else {
@@ -303,8 +311,8 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
             const uint32_t nvec = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * token_bytes) >> 4);
             cta_copy(reinterpret_cast<uint4*>(dst + off), reinterpret_cast<const uint4*>(src + off),
                      nvec);
-            cta_copy(reinterpret_cast<uint4*>(dst + half + off),
-                     reinterpret_cast<const uint4*>(src + half + off), nvec);
+            cta_copy(reinterpret_cast<uint4*>(dst + lp.dst_kv + off),
+                     reinterpret_cast<const uint4*>(src + lp.src_kv + off), nvec);
         }
     }
     if (fence_system) __threadfence_system();  // peer (NVLink) stores visible before host sync
@@ -376,20 +384,24 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
     uint64_t run_bytes, off0;
     const char* base_src;
     char* base_dst;
+    uint64_t src_kv, dst_kv;  // K -> V offsets of the current unit's layer
 
     __device__ bool load_unit() {
         while (u < units) {
             const int32_t layer = (int32_t)(u / nseg);
             const Seg sg = segs[u - (int64_t)layer * nseg];
             const LayerPtr lp = layers[layer];
-            base_src = lp.src + (uint64_t)sg.src_blk * block_bytes;
-            base_dst = lp.dst + (uint64_t)sg.dst_blk * block_bytes;
-            if (sg.t0 == 0 && sg.t1 == block_tokens) {
-                run = 1;  // one run covering K and V
+            base_src = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
+            base_dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
+            src_kv = lp.src_kv;
+            dst_kv = lp.dst_kv;
+            const uint64_t half = block_bytes >> 1;
+            if (sg.t0 == 0 && sg.t1 == block_tokens && src_kv == half && dst_kv == half) {
+                run = 1;  // one run covering K and V (adjacent on both sides)
                 off0 = 0;
                 run_bytes = block_bytes;
             } else {
-                run = 0;
+                run = 0;  // K rows, then V rows
                 off0 = (uint64_t)sg.t0 * token_bytes;
                 run_bytes = (uint64_t)(sg.t1 - sg.t0) * token_bytes;
             }
@@ -402,10 +414,10 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
     }
     __device__ bool next(const char** s, char** d, uint32_t* n) {
         while (left == 0) {
-            if (run == 0) {  // move on to the V half of the partial block
+            if (run == 0) {  // move on to the V rows
                 run = 1;
-                src = base_src + (block_bytes >> 1) + off0;
-                dst = base_dst + (block_bytes >> 1) + off0;
+                src = base_src + src_kv + off0;
+                dst = base_dst + dst_kv + off0;
                 left = run_bytes;
                 break;
             }
@@ -647,14 +659,13 @@ kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ k
 // looping over the pool's layers and the block's K/V token rows.
 // from == nullptr: tokens [0, tokens[i]); else [from[i], tokens[i]) (decode appends).
 static __global__ void __launch_bounds__(256)
-kvx_fill_kernel(char* __restrict__ pool, int32_t pool_blocks, int32_t first_layer,
+kvx_fill_kernel(PoolAddr pa, int32_t first_layer,
                 int32_t num_layers, const int32_t* __restrict__ req,
                 const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
                 int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed,
                 const int64_t* __restrict__ from = nullptr) {
     const int32_t i = blockIdx.x;
     const int32_t r = req[i];
-    const uint64_t block_bytes = 2ull * block_tokens * token_bytes;
     const uint32_t vecs = (uint32_t)(token_bytes >> 4);
     for (int32_t b = blockIdx.y; (int64_t)b * block_tokens < tokens[i]; b += gridDim.y) {  // grid.y <= 65535
         int64_t t_begin = (int64_t)b * block_tokens;
@@ -667,12 +678,12 @@ kvx_fill_kernel(char* __restrict__ pool, int32_t pool_blocks, int32_t first_laye
         const int32_t rows = (int32_t)(t_end - t_begin);
         const int32_t row0 = (int32_t)(t_begin - (int64_t)b * block_tokens);  // first row inside the block
         for (int32_t l = 0; l < num_layers; ++l) {
-            char* slab = pool + ((uint64_t)l * pool_blocks + blk) * block_bytes;
+            char* slab = pa.layer[l] + (uint64_t)blk * pa.blk_stride;
             for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
                 const int32_t kvi = kvr / rows, t = kvr % rows;
                 const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
-                uint4* row =
-                    reinterpret_cast<uint4*>(slab + ((uint64_t)kvi * block_tokens + row0 + t) * token_bytes);
+                uint4* row = reinterpret_cast<uint4*>(slab + (uint64_t)kvi * pa.kv_stride +
+                                                      (uint64_t)(row0 + t) * token_bytes);
                 for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) row[v] = pattern_vec(th, v);
             }
         }
@@ -680,7 +691,7 @@ kvx_fill_kernel(char* __restrict__ pool, int32_t pool_blocks, int32_t first_laye
 }
 
 static __global__ void __launch_bounds__(256)
-kvx_verify_kernel(const char* __restrict__ pool, int32_t pool_blocks, int32_t first_layer,
+kvx_verify_kernel(PoolAddr pa, int32_t first_layer,
                   int32_t num_layers, const int32_t* __restrict__ req,
                   const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
                   int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed,
@@ -688,7 +699,6 @@ kvx_verify_kernel(const char* __restrict__ pool, int32_t pool_blocks, int32_t fi
     const int32_t i = blockIdx.x;
     const int32_t r = req[i];
     const uint32_t vecs = (uint32_t)(token_bytes >> 4);
-    const uint64_t block_bytes = 2ull * block_tokens * token_bytes;
     unsigned long long bad = 0;
     for (int32_t b = blockIdx.y; (int64_t)b * block_tokens < tokens[i]; b += gridDim.y) {  // grid.y <= 65535
         const int64_t t_begin = (int64_t)b * block_tokens;
@@ -700,12 +710,12 @@ kvx_verify_kernel(const char* __restrict__ pool, int32_t pool_blocks, int32_t fi
             continue;
         }
         for (int32_t l = 0; l < num_layers; ++l) {
-            const char* slab = pool + ((uint64_t)l * pool_blocks + blk) * block_bytes;
+            const char* slab = pa.layer[l] + (uint64_t)blk * pa.blk_stride;
             for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
                 const int32_t kvi = kvr / rows, t = kvr % rows;
                 const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
-                const uint4* row =
-                    reinterpret_cast<const uint4*>(slab + ((uint64_t)kvi * block_tokens + t) * token_bytes);
+                const uint4* row = reinterpret_cast<const uint4*>(slab + (uint64_t)kvi * pa.kv_stride +
+                                                                  (uint64_t)t * token_bytes);
                 for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) {
                     const uint4 want = pattern_vec(th, v), got = row[v];
                     const uint32_t d[4] = {want.x ^ got.x, want.y ^ got.y, want.z ^ got.z, want.w ^ got.w};

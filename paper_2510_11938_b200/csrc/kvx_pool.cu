@@ -16,11 +16,17 @@ extern "C" {
 // ------------------------------------------------------------------ pools
 int kvx_pool_create(int32_t device, const kvx_geometry* g, int32_t num_layers, int32_t num_blocks,
                     kvx_pool** out) {
+    return kvx_pool_create_layout(device, g, num_layers, num_blocks, KVX_LAYOUT_BLOCKS, out);
+}
+
+int kvx_pool_create_layout(int32_t device, const kvx_geometry* g, int32_t num_layers, int32_t num_blocks,
+                           int32_t layout, kvx_pool** out) {
     std::string why;
     if (!out) return fail(KVX_EINVAL, "out is null");
     *out = nullptr;
     if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
     if (num_layers < 1 || num_blocks < 1) return fail(KVX_EINVAL, "num_layers/num_blocks must be >= 1");
+    if (!layout_ok(layout)) return fail(KVX_EINVAL, "unknown layout");
     DeviceGuard dg(device);
     if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed for pool device");
     if (const int rc = ensure_loaded(device)) return rc;
@@ -29,6 +35,7 @@ int kvx_pool_create(int32_t device, const kvx_geometry* g, int32_t num_layers, i
     p->g = *g;
     p->num_layers = num_layers;
     p->num_blocks = num_blocks;
+    p->layout = layout;
     p->bytes = (uint64_t)num_layers * (uint64_t)num_blocks * block_bytes(*g);
     cudaError_t e = cudaMalloc(&p->base, p->bytes);
     if (e != cudaSuccess) {
@@ -37,6 +44,7 @@ int kvx_pool_create(int32_t device, const kvx_geometry* g, int32_t num_layers, i
         return fail(e == cudaErrorMemoryAllocation ? KVX_ENOSPC : KVX_ECUDA,
                     std::string("pool cudaMalloc: ") + cudaGetErrorString(e));
     }
+    p->set_contiguous_layers();
     *out = p;
     return KVX_OK;
 }
@@ -59,12 +67,48 @@ int kvx_pool_wrap(int32_t device, void* ptr, uint64_t bytes, const kvx_geometry*
     p->num_layers = num_layers;
     p->num_blocks = num_blocks;
     p->bytes = need;
+    p->set_contiguous_layers();
     *out = p;
     return KVX_OK;
 }
 
+int kvx_pool_wrap_layers(int32_t device, int32_t num_layers, void* const* layer_ptrs, uint64_t layer_bytes,
+                         const kvx_geometry* g, int32_t num_blocks, int32_t layout, kvx_pool** out) {
+    std::string why;
+    if (!out) return fail(KVX_EINVAL, "out is null");
+    *out = nullptr;
+    if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
+    if (num_layers < 1 || num_blocks < 1) return fail(KVX_EINVAL, "num_layers/num_blocks must be >= 1");
+    if (!layout_ok(layout)) return fail(KVX_EINVAL, "unknown layout");
+    if (!layer_ptrs) return fail(KVX_EINVAL, "layer_ptrs is null");
+    if (layer_bytes < (uint64_t)num_blocks * block_bytes(*g))
+        return fail(KVX_EINVAL, "layer allocation smaller than num_blocks blocks");
+    for (int32_t l = 0; l < num_layers; ++l)
+        if (!layer_ptrs[l] || (reinterpret_cast<uintptr_t>(layer_ptrs[l]) & 15))
+            return fail(KVX_EINVAL, "layer pointers must be non-null and 16-byte aligned");
+    auto* p = new kvx_pool;
+    p->device = device;
+    p->wrapped = true;
+    p->per_layer = true;
+    p->base = static_cast<char*>(layer_ptrs[0]);
+    p->g = *g;
+    p->num_layers = num_layers;
+    p->num_blocks = num_blocks;
+    p->layout = layout;
+    p->bytes = (uint64_t)num_layers * (uint64_t)num_blocks * block_bytes(*g);
+    p->layer_base.assign((char* const*)layer_ptrs, (char* const*)layer_ptrs + num_layers);
+    *out = p;
+    return KVX_OK;
+}
+
+int kvx_pool_layout(const kvx_pool* p, int32_t* layout) {
+    if (!p || !layout) return fail(KVX_EINVAL, "null argument");
+    *layout = p->layout;
+    return KVX_OK;
+}
+
 int kvx_pool_export(const kvx_pool* p, uint8_t handle[KVX_IPC_HANDLE_BYTES]) {
-    if (!p || !handle || p->imported) return fail(KVX_EINVAL, "export needs a local pool");
+    if (!p || !handle || p->imported || p->per_layer) return fail(KVX_EINVAL, "export needs a local single-allocation pool");
     static_assert(sizeof(cudaIpcMemHandle_t) == KVX_IPC_HANDLE_BYTES, "ipc handle size");
     DeviceGuard dg(p->device);
     cudaIpcMemHandle_t h;
@@ -75,10 +119,17 @@ int kvx_pool_export(const kvx_pool* p, uint8_t handle[KVX_IPC_HANDLE_BYTES]) {
 
 int kvx_pool_import(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_BYTES],
                     const kvx_geometry* g, int32_t num_layers, int32_t num_blocks, kvx_pool** out) {
+    return kvx_pool_import_layout(device, handle, g, num_layers, num_blocks, KVX_LAYOUT_BLOCKS, out);
+}
+
+int kvx_pool_import_layout(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_BYTES], const kvx_geometry* g,
+                           int32_t num_layers, int32_t num_blocks, int32_t layout, kvx_pool** out) {
     std::string why;
     if (!out || !handle) return fail(KVX_EINVAL, "null argument");
     *out = nullptr;
     if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
+    if (num_layers < 1 || num_blocks < 1) return fail(KVX_EINVAL, "num_layers/num_blocks must be >= 1");
+    if (!layout_ok(layout)) return fail(KVX_EINVAL, "unknown layout");
     DeviceGuard dg(device);
     if (const int rc = ensure_loaded(device)) return rc;
     cudaIpcMemHandle_t h;
@@ -92,7 +143,9 @@ int kvx_pool_import(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_BYTES],
     p->g = *g;
     p->num_layers = num_layers;
     p->num_blocks = num_blocks;
+    p->layout = layout;
     p->bytes = (uint64_t)num_layers * (uint64_t)num_blocks * block_bytes(*g);
+    p->set_contiguous_layers();
     *out = p;
     return KVX_OK;
 }
@@ -119,13 +172,18 @@ int kvx_pool_destroy(kvx_pool* p) {
 int kvx_pool_zero(kvx_pool* p) {
     if (!p) return fail(KVX_EINVAL, "pool is null");
     DeviceGuard dg(p->device);
-    KVX_CUDA(cudaMemset(p->base, 0, p->bytes));
+    if (p->per_layer) {
+        for (char* b : p->layer_base) KVX_CUDA(cudaMemset(b, 0, p->layer_bytes()));
+    } else {
+        KVX_CUDA(cudaMemset(p->base, 0, p->bytes));
+    }
     KVX_CUDA(cudaDeviceSynchronize());
     return KVX_OK;
 }
 
 int kvx_pool_read(const kvx_pool* p, uint64_t offset, uint64_t bytes, void* host) {
     if (!p || !host || offset + bytes > p->bytes) return fail(KVX_EINVAL, "read out of range");
+    if (p->per_layer) return fail(KVX_EINVAL, "per-layer pool: read each layer's own allocation");
     DeviceGuard dg(p->device);
     KVX_CUDA(cudaMemcpy(host, p->base + offset, bytes, cudaMemcpyDeviceToHost));
     return KVX_OK;
@@ -133,6 +191,7 @@ int kvx_pool_read(const kvx_pool* p, uint64_t offset, uint64_t bytes, void* host
 
 int kvx_pool_write(kvx_pool* p, uint64_t offset, uint64_t bytes, const void* host) {
     if (!p || !host || offset + bytes > p->bytes) return fail(KVX_EINVAL, "write out of range");
+    if (p->per_layer) return fail(KVX_EINVAL, "per-layer pool: write each layer's own allocation");
     DeviceGuard dg(p->device);
     KVX_CUDA(cudaMemcpy(p->base + offset, host, bytes, cudaMemcpyHostToDevice));
     return KVX_OK;
@@ -161,22 +220,26 @@ int kvx_pool_fill_pattern(kvx_pool* p, uint64_t seed, int32_t first_layer, int32
     const size_t bt_bytes = sizeof(int32_t) * (size_t)max_requests * (size_t)max_blocks;
     struct Scratch {  // released on every return path
         kvx::Arena& a;
-        void *req = nullptr, *tok = nullptr, *bt = nullptr;
-        size_t nreq, ntok, nbt;
+        void *req = nullptr, *tok = nullptr, *bt = nullptr, *lay = nullptr;
+        size_t nreq, ntok, nbt, nlay;
         ~Scratch() {
             a.dev_free(req, nreq);
             a.dev_free(tok, ntok);
             a.dev_free(bt, nbt);
+            a.dev_free(lay, nlay);
         }
-    } sc{A, nullptr, nullptr, nullptr, sizeof(int32_t) * n, sizeof(int64_t) * n, bt_bytes};
+    } sc{A, nullptr, nullptr, nullptr, nullptr, sizeof(int32_t) * n, sizeof(int64_t) * n, bt_bytes,
+         sizeof(char*) * p->layer_base.size()};
     KVX_CUDA(A.dev_alloc(&sc.req, sc.nreq));
     KVX_CUDA(A.dev_alloc(&sc.tok, sc.ntok));
     KVX_CUDA(A.dev_alloc(&sc.bt, sc.nbt));
+    KVX_CUDA(A.dev_alloc(&sc.lay, sc.nlay));
     KVX_CUDA(cudaMemcpy(sc.req, req, sc.nreq, cudaMemcpyHostToDevice));
     KVX_CUDA(cudaMemcpy(sc.tok, tokens, sc.ntok, cudaMemcpyHostToDevice));
     KVX_CUDA(cudaMemcpy(sc.bt, bt, sc.nbt, cudaMemcpyHostToDevice));
+    KVX_CUDA(cudaMemcpy(sc.lay, p->layer_base.data(), sc.nlay, cudaMemcpyHostToDevice));
     dim3 grid((unsigned)n, (unsigned)std::min<int64_t>(65535, cdiv64(max_tok, p->g.block_tokens)));
-    kvx::kvx_fill_kernel<<<grid, 256>>>(p->base, p->num_blocks, first_layer, p->num_layers,
+    kvx::kvx_fill_kernel<<<grid, 256>>>(pool_addr(p, static_cast<char* const*>(sc.lay)), first_layer, p->num_layers,
                                         static_cast<const int32_t*>(sc.req), static_cast<const int64_t*>(sc.tok),
                                         static_cast<const int32_t*>(sc.bt), max_blocks, p->g.block_tokens,
                                         token_bytes(p->g), seed);
@@ -209,7 +272,8 @@ int kvx_pool_append_pattern(kvx_pool* p, void* stream, uint64_t seed, int32_t fi
     const size_t o_from = ((sizeof(int32_t) * (size_t)n) + 15) & ~size_t(15);
     const size_t o_to = o_from + sizeof(int64_t) * (size_t)n;
     const size_t o_bt = o_to + sizeof(int64_t) * (size_t)n;
-    const size_t bytes = o_bt + sizeof(int32_t) * (size_t)max_requests * (size_t)max_blocks;
+    const size_t o_lay = (o_bt + sizeof(int32_t) * (size_t)max_requests * (size_t)max_blocks + 15) & ~size_t(15);
+    const size_t bytes = o_lay + sizeof(char*) * p->layer_base.size();
     void *d = nullptr, *h = nullptr;
     KVX_CUDA(A.dev_alloc(&d, bytes));
     KVX_CUDA(A.host_alloc(&h, bytes));
@@ -217,11 +281,13 @@ int kvx_pool_append_pattern(kvx_pool* p, void* stream, uint64_t seed, int32_t fi
     std::memcpy(hc, req, sizeof(int32_t) * (size_t)n);
     std::memcpy(hc + o_from, from, sizeof(int64_t) * (size_t)n);
     std::memcpy(hc + o_to, to, sizeof(int64_t) * (size_t)n);
-    std::memcpy(hc + o_bt, bt, bytes - o_bt);
+    std::memcpy(hc + o_bt, bt, sizeof(int32_t) * (size_t)max_requests * (size_t)max_blocks);
+    std::memcpy(hc + o_lay, p->layer_base.data(), sizeof(char*) * p->layer_base.size());
     KVX_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
     char* dc = static_cast<char*>(d);
     dim3 grid((unsigned)n, (unsigned)std::min<int64_t>(65535, cdiv64(max_tok, p->g.block_tokens)));
-    kvx::kvx_fill_kernel<<<grid, 256, 0, st>>>(p->base, p->num_blocks, first_layer, p->num_layers,
+    kvx::kvx_fill_kernel<<<grid, 256, 0, st>>>(pool_addr(p, reinterpret_cast<char* const*>(dc + o_lay)),
+                                               first_layer, p->num_layers,
                                                reinterpret_cast<const int32_t*>(dc),
                                                reinterpret_cast<const int64_t*>(dc + o_to),
                                                reinterpret_cast<const int32_t*>(dc + o_bt), max_blocks,

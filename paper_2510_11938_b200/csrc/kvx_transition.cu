@@ -191,7 +191,6 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     // Per-layer slab bases for the layers this GPU sources.
     std::vector<kvx::LayerPtr> layers;
     std::vector<uint8_t> layer_is_peer;
-    const uint64_t bb = block_bytes(g);
     for (int32_t l = 0; l < g.num_layers; ++l) {
         const int so = stage_of_layer(ob, l), sn = stage_of_layer(nb, l);
         kvx_pool* src = t->old_pools[(size_t)so];
@@ -203,9 +202,9 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         } else if (!src || src->imported || src->device != d->device) {
             continue;
         }
-        const uint64_t ls = (uint64_t)(l - stage_begin(ob, so)) * (uint64_t)src->num_blocks * bb;
-        const uint64_t ld = (uint64_t)(l - stage_begin(nb, sn)) * (uint64_t)dst->num_blocks * bb;
-        layers.push_back({src->base + ls, dst->base + ld});
+        layers.push_back({src->layer_base[(size_t)(l - stage_begin(ob, so))],
+                          dst->layer_base[(size_t)(l - stage_begin(nb, sn))], src->blk_stride(), dst->blk_stride(),
+                          src->kv_stride(), dst->kv_stride()});
         layer_is_peer.push_back(dst->imported || src->imported ? 1 : 0);
         if (dst->imported) t->has_peer_dst = true;
     }
@@ -635,14 +634,24 @@ int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_
     KVX_CUDA(cudaMemcpyAsync(d_req, req, sizeof(int32_t) * n, cudaMemcpyHostToDevice, t->stream));
     KVX_CUDA(cudaMemcpyAsync(d_kv, kv, sizeof(int64_t) * n, cudaMemcpyHostToDevice, t->stream));
     KVX_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), t->stream));
+    std::vector<char*> lay;  // every local new pool's layer bases, back to back
+    for (const kvx_pool* p : t->new_pools)
+        if (p && !p->imported) lay.insert(lay.end(), p->layer_base.begin(), p->layer_base.end());
+    char** d_lay = nullptr;
+    const size_t lay_bytes = sizeof(char*) * std::max<size_t>(1, lay.size());
+    KVX_CUDA(A.dev_alloc((void**)&d_lay, lay_bytes));
+    if (!lay.empty())
+        KVX_CUDA(cudaMemcpyAsync(d_lay, lay.data(), sizeof(char*) * lay.size(), cudaMemcpyHostToDevice, t->stream));
     dim3 grid((unsigned)n, (unsigned)std::min<int64_t>(65535, cdiv64(max_tok, t->g.block_tokens)));
+    size_t at = 0;
     for (size_t k = 0; k < t->new_pools.size(); ++k) {
         const kvx_pool* p = t->new_pools[k];
         if (!p || p->imported) continue;  // the owning rank verifies it
         kvx::kvx_verify_kernel<<<grid, 256, 0, t->stream>>>(
-            p->base, p->num_blocks, stage_begin(t->new_b, (int)k), p->num_layers, d_req, d_kv,
+            pool_addr(p, d_lay + at), stage_begin(t->new_b, (int)k), p->num_layers, d_req, d_kv,
             t->d_dst_bt, t->max_blocks, t->g.block_tokens, token_bytes(t->g), seed, d_bad);
         KVX_LAUNCHED();
+        at += p->layer_base.size();
     }
     unsigned long long bad = 0;
     KVX_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, t->stream));
@@ -650,6 +659,7 @@ int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_
     A.dev_free(d_req, sizeof(int32_t) * n);
     A.dev_free(d_kv, sizeof(int64_t) * n);
     A.dev_free(d_bad, sizeof(unsigned long long));
+    A.dev_free(d_lay, lay_bytes);
     *mismatched_words = (int64_t)bad;
     return KVX_OK;
 }

@@ -31,6 +31,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libkvx.so")
 
 KVX_OK, KVX_EINVAL, KVX_ESTALE, KVX_ENOSPC, KVX_ECUDA, KVX_ESTATE = 0, -1, -2, -3, -4, -5
 ACT_DELTA, ACT_BARRIER_WAIT, ACT_FINAL = 0, 1, 2
+LAYOUT_BLOCKS, LAYOUT_KV_PLANES = 0, 1  # per layer [blocks][2][B][H][D] | [2][blocks][B][H][D]
 IPC_HANDLE_BYTES = 64
 
 
@@ -122,6 +123,10 @@ def _load() -> C.CDLL:
         "kvx_pool_wrap": (C.c_int, [I32, VP, U64, P(Geometry), I32, I32, P(VP)]),
         "kvx_pool_export": (C.c_int, [VP, C.c_char_p]),
         "kvx_pool_import": (C.c_int, [I32, C.c_char_p, P(Geometry), I32, I32, P(VP)]),
+        "kvx_pool_create_layout": (C.c_int, [I32, P(Geometry), I32, I32, I32, P(VP)]),
+        "kvx_pool_import_layout": (C.c_int, [I32, C.c_char_p, P(Geometry), I32, I32, I32, P(VP)]),
+        "kvx_pool_wrap_layers": (C.c_int, [I32, I32, P(VP), U64, P(Geometry), I32, I32, P(VP)]),
+        "kvx_pool_layout": (C.c_int, [VP, P(I32)]),
         "kvx_pool_info": (C.c_int, [VP, P(VP), P(U64), P(I32), P(I32)]),
         "kvx_pool_destroy": (C.c_int, [VP]),
         "kvx_pool_zero": (C.c_int, [VP]),
@@ -240,23 +245,35 @@ class Pool(_Handle):
     """One stage's paged KV pool on one GPU (local or imported from a peer)."""
 
     def __init__(self, device: int, geom: Geometry, num_layers: int, num_blocks: int,
-                 _handle: Optional[int] = None, imported: bool = False):
+                 layout: int = LAYOUT_BLOCKS, _handle: Optional[int] = None, imported: bool = False):
         self.geom, self.num_layers, self.num_blocks = geom, num_layers, num_blocks
-        self.device, self.imported = device, imported
+        self.device, self.imported, self.layout = device, imported, layout
         if _handle is None:
             h = C.c_void_p()
-            _check(_lib.kvx_pool_create(device, C.byref(geom), num_layers, num_blocks, C.byref(h)))
+            _check(_lib.kvx_pool_create_layout(device, C.byref(geom), num_layers, num_blocks, layout,
+                                               C.byref(h)))
             self._h = h
         else:
             self._h = C.c_void_p(_handle)
 
     @classmethod
     def import_ipc(cls, device: int, handle: bytes, geom: Geometry, num_layers: int,
-                   num_blocks: int) -> "Pool":
+                   num_blocks: int, layout: int = LAYOUT_BLOCKS) -> "Pool":
         h = C.c_void_p()
-        _check(_lib.kvx_pool_import(device, handle, C.byref(geom), num_layers, num_blocks,
-                                    C.byref(h)))
-        return cls(device, geom, num_layers, num_blocks, _handle=h.value, imported=True)
+        _check(_lib.kvx_pool_import_layout(device, handle, C.byref(geom), num_layers, num_blocks, layout,
+                                           C.byref(h)))
+        return cls(device, geom, num_layers, num_blocks, layout, _handle=h.value, imported=True)
+
+    @classmethod
+    def wrap_layers(cls, device: int, layer_ptrs: Sequence[int], layer_bytes: int, geom: Geometry,
+                    num_blocks: int, layout: int = LAYOUT_KV_PLANES) -> "Pool":
+        """A pool over one caller-owned allocation per layer (e.g. a serving
+        engine's per-layer cache tensors, data_ptr() each)."""
+        ptrs = (C.c_void_p * len(layer_ptrs))(*layer_ptrs)
+        h = C.c_void_p()
+        _check(_lib.kvx_pool_wrap_layers(device, len(layer_ptrs), ptrs, layer_bytes, C.byref(geom), num_blocks,
+                                         layout, C.byref(h)))
+        return cls(device, geom, len(layer_ptrs), num_blocks, layout, _handle=h.value)
 
     @classmethod
     def wrap(cls, device: int, ptr: int, nbytes: int, geom: Geometry, num_layers: int,
@@ -264,7 +281,7 @@ class Pool(_Handle):
         """A pool over caller-owned device memory (e.g. a torch tensor's data_ptr())."""
         h = C.c_void_p()
         _check(_lib.kvx_pool_wrap(device, ptr, nbytes, C.byref(geom), num_layers, num_blocks, C.byref(h)))
-        return cls(device, geom, num_layers, num_blocks, _handle=h.value)
+        return cls(device, geom, num_layers, num_blocks, LAYOUT_BLOCKS, _handle=h.value)
 
     def export_ipc(self) -> bytes:
         buf = C.create_string_buffer(IPC_HANDLE_BYTES)

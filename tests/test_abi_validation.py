@@ -93,6 +93,28 @@ def test_pool_wrap_validation():
     assert L.kvx_pool_wrap(0, C.c_void_p(0x1000), 16, C.byref(g), 2, 4, C.byref(h)) == kvx.KVX_EINVAL      # too small
 
 
+def test_layout_validation():
+    g = kvx.geometry(4, 2, 64)
+    h = C.c_void_p()
+    assert L.kvx_pool_create_layout(0, C.byref(g), 2, 4, 7, C.byref(h)) == kvx.KVX_EINVAL   # unknown layout
+    ok = (C.c_void_p * 2)(0x1000, 0x2000)
+    bb = g.block_bytes
+    W = L.kvx_pool_wrap_layers
+    assert W(0, 2, None, 4 * bb, C.byref(g), 4, kvx.LAYOUT_KV_PLANES, C.byref(h)) == kvx.KVX_EINVAL
+    assert W(0, 2, ok, 4 * bb, C.byref(g), 4, 9, C.byref(h)) == kvx.KVX_EINVAL               # unknown layout
+    assert W(0, 2, ok, 4 * bb - 16, C.byref(g), 4, 1, C.byref(h)) == kvx.KVX_EINVAL          # layer too small
+    assert W(0, 2, (C.c_void_p * 2)(0x1000, None), 4 * bb, C.byref(g), 4, 1, C.byref(h)) == kvx.KVX_EINVAL
+    assert W(0, 2, (C.c_void_p * 2)(0x1000, 0x2008), 4 * bb, C.byref(g), 4, 1, C.byref(h)) == kvx.KVX_EINVAL
+    # bookkeeping only: a valid per-layer wrap needs no GPU; it cannot be read or exported
+    assert W(0, 2, ok, 4 * bb, C.byref(g), 4, kvx.LAYOUT_KV_PLANES, C.byref(h)) == kvx.KVX_OK
+    lay = C.c_int32(-1)
+    assert L.kvx_pool_layout(h, C.byref(lay)) == kvx.KVX_OK and lay.value == kvx.LAYOUT_KV_PLANES
+    buf = (C.c_uint8 * 16)()
+    assert L.kvx_pool_read(h, 0, 16, buf) == kvx.KVX_EINVAL
+    assert L.kvx_pool_export(h, (C.c_char * 64)()) == kvx.KVX_EINVAL
+    assert L.kvx_pool_destroy(h) == kvx.KVX_OK
+
+
 def test_weights_validation():
     ob = (C.c_int32 * 1)(2)
     ptrs = (C.c_void_p * 2)(None, None)
