@@ -77,7 +77,8 @@ def link_bytes(L: int, ob, nb, old_dev, new_dev, layer_bytes: int, n_gpus: int):
 
 def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, old_blocks: int,
                      dst_blocks: int, all_gather: Optional[Callable] = None,
-                     fill: Optional[tuple] = None, zero_new: bool = True, pull: bool = False):
+                     fill: Optional[tuple] = None, zero_new: bool = True, pull: bool = False,
+                     old_layout: int = 0, new_layout: int = 0):
     """Creates this rank's pools and maps every peer's new-stage pool.
 
     fill = (seed, live_req, tokens, src_bt) writes the synthetic payload into
@@ -86,6 +87,8 @@ def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, o
     pull=False maps peers' NEW pools (this rank pushes its old layers into
     them); pull=True maps peers' OLD pools (this rank pulls the layers of its
     new stages out of them).
+    old_layout / new_layout: KVX_LAYOUT_* of the old / new pools (peers map
+    them with the same layout).
     Returns (old_pools, new_pools) indexed by stage (None where remote/absent).
     """
     L = g.num_layers
@@ -93,7 +96,7 @@ def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, o
     mine = {}
     for k, (b, e) in enumerate(W.stage_ranges(L, ob)):
         if old_dev[k] == rank:
-            p = kvx.Pool(device, g, e - b, old_blocks)
+            p = kvx.Pool(device, g, e - b, old_blocks, old_layout)
             if fill is not None:
                 seed, live, tokens, src_bt = fill
                 p.zero()
@@ -104,19 +107,19 @@ def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, o
     new_pools: List = [None] * (len(nb) + 1)
     for j, (b, e) in enumerate(W.stage_ranges(L, nb)):
         if new_dev[j] == rank:
-            p = kvx.Pool(device, g, e - b, dst_blocks)
+            p = kvx.Pool(device, g, e - b, dst_blocks, new_layout)
             if zero_new:
                 p.zero()
             new_pools[j] = p
             if not pull and all_gather is not None:
                 mine[j] = p.export_ipc()
     if all_gather is not None:
-        target, ranges, blocks = (old_pools, W.stage_ranges(L, ob), old_blocks) if pull else \
-            (new_pools, W.stage_ranges(L, nb), dst_blocks)
+        target, ranges, blocks, layout = (old_pools, W.stage_ranges(L, ob), old_blocks, old_layout) if pull else \
+            (new_pools, W.stage_ranges(L, nb), dst_blocks, new_layout)
         for r, handles in enumerate(all_gather(mine)):
             if r == rank:
                 continue
             for j, h in handles.items():
                 b, e = ranges[int(j)]
-                target[int(j)] = kvx.Pool.import_ipc(device, h, g, e - b, blocks)
+                target[int(j)] = kvx.Pool.import_ipc(device, h, g, e - b, blocks, layout)
     return old_pools, new_pools

@@ -47,9 +47,10 @@ def cpu_worker(rank, world, port, out):
         out.put((rank, "err", traceback.format_exc()))
 
 
-def gpu_worker(rank, world, port, name, heads, dim, mode, pull, stride, out):
+def gpu_worker(rank, world, port, name, heads, dim, mode, pull, stride, layouts, out):
     """stride=0: the scenario's last committed transition; stride=k: every
-    k-th transition of the scenario (e.g. the controller-chosen chain)."""
+    k-th transition of the scenario (e.g. the controller-chosen chain).
+    layouts = (old, new) KVX_LAYOUT_* of the pools."""
     try:
         dist = _init(rank, world, port)
         from paper_2510_11938_b200 import workload as W
@@ -59,7 +60,7 @@ def gpu_worker(rank, world, port, name, heads, dim, mode, pull, stride, out):
             else scn.transitions[::stride]
         checked, moved = 0, 0
         for t in ts:
-            c, m, old_dev, new_dev = _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull)
+            c, m, old_dev, new_dev = _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull, layouts)
             checked += c
             moved += m
         dist.destroy_process_group()
@@ -69,7 +70,7 @@ def gpu_worker(rank, world, port, name, heads, dim, mode, pull, stride, out):
         out.put((rank, "err", traceback.format_exc()))
 
 
-def _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull):
+def _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull, layouts=(0, 0)):
     import numpy as np
     from oracle import pyoracle as O
     from paper_2510_11938_b200 import kvx
@@ -94,7 +95,8 @@ def _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull):
 
     old_pools, new_pools = S.setup_rank_pools(
         kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, rank, old_blocks,
-        dst_blocks, all_gather=gather, fill=(SEED, live, tokens[live], src_bt), pull=pull)
+        dst_blocks, all_gather=gather, fill=(SEED, live, tokens[live], src_bt), pull=pull,
+        old_layout=layouts[0], new_layout=layouts[1])
     dist.barrier()
     tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, rank, N,
                         max_blocks, dst_blocks, src_bt, epoch=t.epoch,
@@ -130,10 +132,14 @@ def _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull):
     assert np.array_equal(tr.dst_block_table(), dp.bt)
     dist.barrier()  # every rank's pushes have landed (kernels end with a system fence)
     checked = 0
-    for j, p in enumerate(new_pools):
+    for j, (b, e) in enumerate(W.stage_ranges(L, t.new_boundaries)):
         if new_dev[j] == rank:
-            got = p.read()
-            assert np.array_equal(got, dp.new_pools[j]), f"new stage {j} differs on rank {rank}"
+            got = new_pools[j].read().reshape(e - b, -1)
+            want = dp.new_pools[j].reshape(e - b, dst_blocks, 2, -1)
+            if layouts[1] == kvx.LAYOUT_KV_PLANES:     # the oracle is in the block layout
+                want = want.transpose(0, 2, 1, 3)
+            assert np.array_equal(got, np.ascontiguousarray(want).reshape(e - b, -1)), \
+                f"new stage {j} differs on rank {rank}"
             checked += 1
     moved = tr.bytes_moved()
     tr.close()

@@ -53,7 +53,7 @@ def test_ranks_shard_every_layer_once_cpu(world):
 def test_two_gpu_transition_bit_exact(gpu_count, mode, name, heads, dim, pull):
     if gpu_count < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
-    res = _run(mgpu_worker.gpu_worker, 2, name, heads, dim, mode, pull, 0)
+    res = _run(mgpu_worker.gpu_worker, 2, name, heads, dim, mode, pull, 0, (0, 0))
     assert sum(r["checked"] for r in res.values()) >= 2
 
 
@@ -66,9 +66,23 @@ def test_two_gpu_controller_chain_bit_exact(gpu_count, mode):
     NVLink and compared with the oracle byte for byte."""
     if gpu_count < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
-    res = _run(mgpu_worker.gpu_worker, 2, "adaptive_cv7", 1, 8, mode, False, 4)
+    res = _run(mgpu_worker.gpu_worker, 2, "adaptive_cv7", 1, 8, mode, False, 4, (0, 0))
     assert all(r["transitions"] == 10 for r in res.values())
     assert sum(r["checked"] for r in res.values()) >= 10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pull", [False, True], ids=["push", "pull"])
+@pytest.mark.parametrize("layouts", [(1, 0), (0, 1), (1, 1)], ids=["planes-to-blocks", "blocks-to-planes",
+                                                                     "planes"])
+def test_two_gpu_layout_conversion_bit_exact(gpu_count, layouts, pull):
+    """Cross-GPU transitions between K/V-plane and block pools: peers map each
+    other's pools with their layout (kvx_pool_import_layout); the moved
+    bytes land permuted into the destination layout, bit for bit."""
+    if gpu_count < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    res = _run(mgpu_worker.gpu_worker, 2, "criterion12", 2, 64, "disjoint", pull, 0, layouts)
+    assert sum(r["checked"] for r in res.values()) >= 2
 
 
 @pytest.mark.gpu
