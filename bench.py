@@ -478,6 +478,9 @@ def main():
     ap.add_argument("--pull", action="store_true",
                     help="cross-GPU moves pulled by the destination GPU instead of pushed")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--layouts", default="blocks,blocks",
+                    help="old,new pool layouts: blocks (FlashInfer [blocks][2][B][H][D]) or planes "
+                         "(FlashAttention [2][blocks][B][H][D]); unequal = the refactor converts")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -514,6 +517,7 @@ def main():
     plan = Plan(args.config)
     t = plan.t
     L = plan.L
+    layouts = [{"blocks": kvx.LAYOUT_BLOCKS, "planes": kvx.LAYOUT_KV_PLANES}[x] for x in args.layouts.split(",")]
     g = kvx.geometry(L, plan.H, plan.D)
     old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, n_gpus, args.placement)
 
@@ -526,7 +530,8 @@ def main():
     old_pools, new_pools = S.setup_rank_pools(
         kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, dev, plan.old_blocks,
         plan.dst_blocks, all_gather=gather if world > 1 else None,
-        fill=(SEED, plan.live, plan.tokens[plan.live], plan.src_bt), pull=args.pull)
+        fill=(SEED, plan.live, plan.tokens[plan.live], plan.src_bt), pull=args.pull,
+        old_layout=layouts[0], new_layout=layouts[1])
     if world > 1:
         dist.barrier()
 
@@ -810,6 +815,7 @@ def main():
         "config": {"workload": plan.desc, "golden_wave_plan": plan.golden,
                    "bytes_per_step": plan.step_bytes, "tokens_per_step": plan.step_tokens,
                    "placement": {"mode": args.placement, "old_stage_gpu": old_dev, "new_stage_gpu": new_dev},
+                   "kv_layouts": args.layouts,
                    "l2": "inputs (17 GB) larger than L2 (126 MB); no flush needed"},
         "stall_ms": round(stall_med, 4), "stall_ms_all": [round(x, 4) for x in (stalls[0], stalls[-1])],
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
