@@ -103,6 +103,74 @@ int main() {
     CK(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
     CK(cudaSetDevice(1));
     CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+    // ---- bidirectional: both link directions loaded at once
+    {
+        char *g0_src, *g1_dst, *g0_dst2, *g1_src2;
+        CK(cudaSetDevice(0));
+        CK(cudaMalloc(&g0_src, bytes));
+        CK(cudaMemset(g0_src, 3, bytes));
+        CK(cudaSetDevice(1));
+        CK(cudaMalloc(&g1_dst, bytes));
+        (void)g0_dst2;
+        (void)g1_src2;
+        const char* names[] = {"bi_push", "bi_pull", "bi_push01_pull10", "bi_copy_engine"};
+        for (int ctas : {64, 148}) {
+            for (int mode = 0; mode < 4; ++mode) {
+                double best = 1e30;
+                for (int rep = 0; rep < 4; ++rep) {
+                    CK(cudaSetDevice(0));
+                    CK(cudaDeviceSynchronize());
+                    CK(cudaSetDevice(1));
+                    CK(cudaDeviceSynchronize());
+                    cudaEvent_t a, b, done1;
+                    CK(cudaSetDevice(0));
+                    CK(cudaEventCreate(&a));
+                    CK(cudaEventCreate(&b));
+                    CK(cudaSetDevice(1));
+                    CK(cudaEventCreateWithFlags(&done1, cudaEventDisableTiming));
+                    CK(cudaSetDevice(0));
+                    CK(cudaEventRecord(a, s0));
+                    CK(cudaSetDevice(1));
+                    CK(cudaStreamWaitEvent(s1, a, 0));
+                    // direction 1->0 (g1_src_push -> g0_dst_push) and 0->1 (g0_src -> g1_dst)
+                    if (mode == 0) {  // each GPU pushes its outgoing data
+                        bulk_copy<<<ctas, 32, kStages * kChunk, s1>>>(g1_src_push, g0_dst_push, bytes);
+                    } else if (mode == 1) {  // each GPU pulls its incoming data
+                        bulk_copy<<<ctas, 32, kStages * kChunk, s1>>>(g0_src, g1_dst, bytes);
+                    } else if (mode == 2) {  // GPU0 pushes 0->1 and pulls 1->0; GPU1 idle
+                    } else {
+                        CK(cudaMemcpyPeerAsync(g0_dst_push, 0, g1_src_push, 1, bytes, s1));
+                    }
+                    CK(cudaEventRecord(done1, s1));
+                    CK(cudaSetDevice(0));
+                    if (mode == 0) {
+                        bulk_copy<<<ctas, 32, kStages * kChunk, s0>>>(g0_src, g1_dst, bytes);
+                    } else if (mode == 1) {
+                        bulk_copy<<<ctas, 32, kStages * kChunk, s0>>>(g1_src_pull, g0_dst_pull, bytes);
+                    } else if (mode == 2) {
+                        bulk_copy<<<ctas / 2, 32, kStages * kChunk, s0>>>(g0_src, g1_dst, bytes);
+                        bulk_copy<<<ctas / 2, 32, kStages * kChunk, s0>>>(g1_src_pull, g0_dst_pull, bytes);
+                    } else {
+                        CK(cudaMemcpyPeerAsync(g1_dst, 1, g0_src, 0, bytes, s0));
+                    }
+                    CK(cudaStreamWaitEvent(s0, done1, 0));
+                    CK(cudaEventRecord(b, s0));
+                    CK(cudaEventSynchronize(b));
+                    CK(cudaGetLastError());
+                    float ms = 0;
+                    CK(cudaEventElapsedTime(&ms, a, b));
+                    if (rep) best = ms < best ? ms : best;
+                    if (rep == 3)
+                        printf("{\"ctas\": %d, \"mode\": \"%s\", \"GBps_per_direction\": %.1f, \"ms\": %.3f}\n",
+                               ctas, names[mode], (double)bytes / (best * 1e-3) / 1e9, best);
+                    CK(cudaEventDestroy(a));
+                    CK(cudaEventDestroy(b));
+                    CK(cudaSetDevice(1));
+                    CK(cudaEventDestroy(done1));
+                }
+            }
+        }
+    }
     int ctas_list[] = {16, 32, 64, 148};
     for (int ctas : ctas_list) {
         for (int mode = 0; mode < 4; ++mode) {  // 0 push, 1 pull, 2 push+pull, 3 copy engine
