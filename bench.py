@@ -470,13 +470,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kvx", choices=["kvx", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + ["c5"])
-    ap.add_argument("--placement", default="affinity", choices=["affinity", "disjoint", "spread"])
+    ap.add_argument("--placement", default="affinity", choices=["affinity", "disjoint", "spread", "oneway"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-weights", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
-    ap.add_argument("--pull", action="store_true",
-                    help="cross-GPU moves pulled by the destination GPU instead of pushed")
+    ap.add_argument("--move", default="auto", choices=["auto", "push", "pull"],
+                    help="who moves a cross-GPU layer: auto = pull on one-way traffic, push on two-way "
+                         "(shard.move_plan); push = the source GPU; pull = the destination GPU")
+    ap.add_argument("--pull", action="store_true", help="alias of --move pull")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--layouts", default="blocks,blocks",
                     help="old,new pool layouts: blocks (FlashInfer [blocks][2][B][H][D]) or planes "
@@ -520,6 +522,9 @@ def main():
     layouts = [{"blocks": kvx.LAYOUT_BLOCKS, "planes": kvx.LAYOUT_KV_PLANES}[x] for x in args.layouts.split(",")]
     g = kvx.geometry(L, plan.H, plan.D)
     old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, n_gpus, args.placement)
+    if args.pull:
+        args.move = "pull"
+    layer_pull = S.move_plan(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev, args.move)
 
     # ---- pools on this GPU; new-stage pools of peers mapped through CUDA IPC
     def gather(obj):
@@ -530,7 +535,7 @@ def main():
     old_pools, new_pools = S.setup_rank_pools(
         kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, dev, plan.old_blocks,
         plan.dst_blocks, all_gather=gather if world > 1 else None,
-        fill=(SEED, plan.live, plan.tokens[plan.live], plan.src_bt), pull=args.pull,
+        fill=(SEED, plan.live, plan.tokens[plan.live], plan.src_bt), layer_pull=layer_pull,
         old_layout=layouts[0], new_layout=layouts[1])
     if world > 1:
         dist.barrier()
@@ -542,7 +547,7 @@ def main():
         return kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, dev,
                               plan.N, plan.max_blocks, plan.dst_blocks, plan.src_bt, epoch=t.epoch,
                               max_sync_rounds=plan.scn.max_sync_rounds,
-                              kv_bytes_per_token=plan.kv_bytes_per_token, stream=sp, pull=args.pull)
+                              kv_bytes_per_token=plan.kv_bytes_per_token, stream=sp, layer_pull=layer_pull)
 
     K, Wm = args.steps, args.warmup
     trs = [make() for _ in range(Wm + K)]
@@ -816,6 +821,9 @@ def main():
                    "bytes_per_step": plan.step_bytes, "tokens_per_step": plan.step_tokens,
                    "placement": {"mode": args.placement, "old_stage_gpu": old_dev, "new_stage_gpu": new_dev},
                    "kv_layouts": args.layouts,
+                   "movers": {"policy": args.move, "pulled_layers": int(sum(layer_pull)),
+                              "cross_gpu_layers": sum(1 for l in range(L) if old_dev[S.stage_of(t.old_boundaries, l)]
+                                                      != new_dev[S.stage_of(t.new_boundaries, l)])},
                    "l2": "inputs (17 GB) larger than L2 (126 MB); no flush needed"},
         "stall_ms": round(stall_med, 4), "stall_ms_all": [round(x, 4) for x in (stalls[0], stalls[-1])],
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define KVX_ABI_VERSION 1
+#define KVX_ABI_VERSION 2  /* 2: kvx_transition_desc.layer_pull */
 
 #define KVX_OK 0
 #define KVX_EINVAL (-1)  /* bad argument (null, out of range, unsorted wave) */
@@ -196,6 +196,13 @@ typedef struct kvx_transition_desc {
     int32_t pull;                 /* 0: move the layers whose OLD pool is local (push to peers);
                                      1: move the layers whose NEW pool is local, reading peers'
                                      (imported) old pools over NVLink (pull) */
+    const uint8_t* layer_pull;    /* optional, per layer (overrides `pull`): 1 = the GPU holding
+                                     the layer's NEW pool pulls it, 0 = the GPU holding its OLD
+                                     pool pushes it.  Every rank passes the same array.  One-way
+                                     NVLink traffic is faster pulled, two-way faster pushed
+                                     (DESIGN.md 4); shard.py derives it from the placement.
+                                     Layers whose old and new pools are both local always move
+                                     here.  NULL = `pull` for every layer. */
 } kvx_transition_desc;
 
 typedef struct kvx_transition kvx_transition;

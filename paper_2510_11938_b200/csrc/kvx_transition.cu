@@ -46,7 +46,9 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     for (int k = 0; k < d->new_plan.num_stages; ++k) {
         const kvx_pool* p = d->new_plan.pools[k];
         if (!p) {
-            if (d->pull) continue;  // pull: only the local new pools are written here
+            // pull / per-layer movers: only the pools of layers moved here are needed
+            // (checked per layer below)
+            if (d->pull || d->layer_pull) continue;
             return fail(KVX_EINVAL, "every new-stage pool is required");
         }
         const int32_t layers = (k + 1 < d->new_plan.num_stages ? nb[(size_t)k] : g.num_layers) -
@@ -195,12 +197,18 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         const int so = stage_of_layer(ob, l), sn = stage_of_layer(nb, l);
         kvx_pool* src = t->old_pools[(size_t)so];
         kvx_pool* dst = t->new_pools[(size_t)sn];
-        if (d->pull) {  // this GPU owns the layer's destination; the source may be a peer's
-            if (!dst || dst->imported || dst->device != d->device) continue;
+        const bool src_local = src && !src->imported && src->device == d->device;
+        const bool dst_local = dst && !dst->imported && dst->device == d->device;
+        const bool pulled = d->layer_pull ? d->layer_pull[l] != 0 : d->pull != 0;
+        if (src_local && dst_local) {
+            // both pools here: a local move whichever side would otherwise move it
+        } else if (pulled) {  // this GPU owns the layer's destination; the source is a peer's
+            if (!dst_local) continue;
             if (!src) return bail(fail(KVX_EINVAL, "pull: a local destination layer has no mapped source pool"));
-            if (src->imported) t->has_peer_dst = true;  // peer traffic on this handle
-        } else if (!src || src->imported || src->device != d->device) {
-            continue;
+            t->has_peer_dst = true;  // peer traffic on this handle
+        } else {  // this GPU owns the layer's source and pushes it into the (peer) destination
+            if (!src_local) continue;
+            if (!dst) return bail(fail(KVX_EINVAL, "push: a local source layer has no mapped destination pool"));
         }
         layers.push_back({src->layer_base[(size_t)(l - stage_begin(ob, so))],
                           dst->layer_base[(size_t)(l - stage_begin(nb, sn))], src->blk_stride(), dst->blk_stride(),

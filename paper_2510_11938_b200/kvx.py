@@ -80,7 +80,7 @@ class _Desc(C.Structure):
                 ("dst_num_blocks", C.c_int32), ("src_block_table", C.POINTER(C.c_int32)),
                 ("epoch", C.c_uint64), ("max_sync_rounds", C.c_int32),
                 ("kv_bytes_per_token", C.c_double), ("stream", C.c_void_p),
-                ("dst_blockmgr", C.c_void_p), ("pull", C.c_int32)]
+                ("dst_blockmgr", C.c_void_p), ("pull", C.c_int32), ("layer_pull", C.POINTER(C.c_uint8))]
 
 
 class _CommitResult(C.Structure):
@@ -406,7 +406,8 @@ class Transition(_Handle):
                  max_requests: int, max_blocks: int, dst_num_blocks: int,
                  src_block_table: np.ndarray, epoch: int = 1, max_sync_rounds: int = 8,
                  kv_bytes_per_token: float = 0.0, stream: int = 0,
-                 dst_blockmgr: Optional["BlockManager"] = None, pull: bool = False):
+                 dst_blockmgr: Optional["BlockManager"] = None, pull: bool = False,
+                 layer_pull: Optional[Sequence[int]] = None):
         self.geom = geom
         self.max_requests, self.max_blocks = max_requests, max_blocks
         self._ob = _i32(list(old_boundaries))
@@ -432,6 +433,11 @@ class Transition(_Handle):
         d.dst_blockmgr = dst_blockmgr.handle.value if dst_blockmgr is not None else None
         self._bm = dst_blockmgr
         d.pull = 1 if pull else 0
+        if layer_pull is not None:   # per layer: 1 = destination pulls, 0 = source pushes
+            self._layer_pull = np.ascontiguousarray(layer_pull, dtype=np.uint8)
+            if self._layer_pull.shape != (geom.num_layers,):
+                raise ValueError("layer_pull needs one entry per layer")
+            d.layer_pull = self._layer_pull.ctypes.data_as(C.POINTER(C.c_uint8))
         h = C.c_void_p()
         _check(_lib.kvx_begin(C.byref(d), C.byref(h)))
         self._h = h

@@ -35,12 +35,17 @@ def placement(L: int, ob: Sequence[int], nb: Sequence[int], n_gpus: int,
     mode='disjoint' shifts each new stage by N/2 GPUs so all of its KV crosses
     NVLink, the physical analogue of the reference's disjoint grant.
     mode='spread' puts new stage j on GPU floor(j * N / K_new): a split fans
-    its new stages out over every GPU (what a split is for)."""
+    its new stages out over every GPU (what a split is for).
+    mode='oneway' puts every new stage on GPU 0: GPU 0 keeps its own layers
+    and receives the rest one way -- at N=2 the traffic pattern of a C3
+    receiver at N=8 (half local, half from one partner)."""
     k_old = len(ob) + 1
     old_dev = [k * n_gpus // k_old for k in range(k_old)]
     if mode == "spread":
         k_new = len(nb) + 1
         return old_dev, [j * n_gpus // k_new for j in range(k_new)]
+    if mode == "oneway":
+        return old_dev, [0] * (len(nb) + 1)
     new_dev = []
     for b, e in W.stage_ranges(L, nb):
         share: Dict[int, int] = {}
@@ -52,6 +57,32 @@ def placement(L: int, ob: Sequence[int], nb: Sequence[int], n_gpus: int,
             best = (best + n_gpus // 2) % n_gpus
         new_dev.append(best)
     return old_dev, new_dev
+
+
+def move_plan(L: int, ob: Sequence[int], nb: Sequence[int], old_dev: Sequence[int],
+              new_dev: Sequence[int], policy: str = "auto") -> List[int]:
+    """kvx_transition_desc.layer_pull: per layer, 1 = the destination GPU pulls
+    it, 0 = the source GPU pushes it (same-GPU layers move locally either way).
+    policy 'push' / 'pull' for every layer; 'auto' pulls a cross-GPU layer
+    s -> d when the traffic is one way at both ends (d sends nothing over
+    NVLink, s receives nothing) and pushes it otherwise.  Through NVSwitch
+    every GPU's links carry all of its egress and ingress; a pull's read
+    requests travel d -> s.  Measured on B200 NVLink 5
+    (profiles/r01_nvlink_split.jsonl): one way, TMA pull 790 GB/s vs push 718;
+    both ways, push 712 vs pull 677 per direction."""
+    if policy in ("push", "pull"):
+        return [1 if policy == "pull" else 0] * L
+    sends, recvs = set(), set()
+    for l in range(L):
+        s, d = old_dev[stage_of(ob, l)], new_dev[stage_of(nb, l)]
+        if s != d:
+            sends.add(s)
+            recvs.add(d)
+    plan = []
+    for l in range(L):
+        s, d = old_dev[stage_of(ob, l)], new_dev[stage_of(nb, l)]
+        plan.append(1 if s != d and d not in sends and s not in recvs else 0)
+    return plan
 
 
 def layers_of_rank(L: int, ob: Sequence[int], old_dev: Sequence[int], rank: int) -> List[int]:
@@ -78,7 +109,7 @@ def link_bytes(L: int, ob, nb, old_dev, new_dev, layer_bytes: int, n_gpus: int):
 def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, old_blocks: int,
                      dst_blocks: int, all_gather: Optional[Callable] = None,
                      fill: Optional[tuple] = None, zero_new: bool = True, pull: bool = False,
-                     old_layout: int = 0, new_layout: int = 0):
+                     old_layout: int = 0, new_layout: int = 0, layer_pull: Optional[Sequence[int]] = None):
     """Creates this rank's pools and maps every peer's new-stage pool.
 
     fill = (seed, live_req, tokens, src_bt) writes the synthetic payload into
@@ -89,11 +120,17 @@ def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, o
     new stages out of them).
     old_layout / new_layout: KVX_LAYOUT_* of the old / new pools (peers map
     them with the same layout).
+    layer_pull (move_plan): peers' pools are mapped on the side each layer's
+    mover needs -- peers' NEW pools for the layers this rank pushes, peers'
+    OLD pools for the layers it pulls.
     Returns (old_pools, new_pools) indexed by stage (None where remote/absent).
     """
     L = g.num_layers
+    # which side of the peers' pools this rank maps
+    map_old = pull or layer_pull is not None
+    map_new = not pull or layer_pull is not None
     old_pools: List = [None] * (len(ob) + 1)
-    mine = {}
+    mine = {"old": {}, "new": {}}
     for k, (b, e) in enumerate(W.stage_ranges(L, ob)):
         if old_dev[k] == rank:
             p = kvx.Pool(device, g, e - b, old_blocks, old_layout)
@@ -102,8 +139,8 @@ def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, o
                 p.zero()
                 p.fill_pattern(seed, b, live, tokens, src_bt)
             old_pools[k] = p
-            if pull and all_gather is not None:
-                mine[k] = p.export_ipc()
+            if map_old and all_gather is not None:
+                mine["old"][k] = p.export_ipc()
     new_pools: List = [None] * (len(nb) + 1)
     for j, (b, e) in enumerate(W.stage_ranges(L, nb)):
         if new_dev[j] == rank:
@@ -111,15 +148,16 @@ def setup_rank_pools(kvx, g, ob, nb, old_dev, new_dev, rank: int, device: int, o
             if zero_new:
                 p.zero()
             new_pools[j] = p
-            if not pull and all_gather is not None:
-                mine[j] = p.export_ipc()
+            if map_new and all_gather is not None:
+                mine["new"][j] = p.export_ipc()
     if all_gather is not None:
-        target, ranges, blocks, layout = (old_pools, W.stage_ranges(L, ob), old_blocks, old_layout) if pull else \
-            (new_pools, W.stage_ranges(L, nb), dst_blocks, new_layout)
+        sides = {"old": (old_pools, W.stage_ranges(L, ob), old_blocks, old_layout),
+                 "new": (new_pools, W.stage_ranges(L, nb), dst_blocks, new_layout)}
         for r, handles in enumerate(all_gather(mine)):
             if r == rank:
                 continue
-            for j, h in handles.items():
-                b, e = ranges[int(j)]
-                target[int(j)] = kvx.Pool.import_ipc(device, h, g, e - b, blocks, layout)
+            for side, (target, ranges, blocks, layout) in sides.items():
+                for j, h in handles[side].items():
+                    b, e = ranges[int(j)]
+                    target[int(j)] = kvx.Pool.import_ipc(device, h, g, e - b, blocks, layout)
     return old_pools, new_pools

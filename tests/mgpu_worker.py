@@ -87,6 +87,9 @@ def _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull, layouts=(
     dst_blocks = max(1, int(((tokens + 15) // 16).sum()))
     live = np.nonzero(tokens)[0].astype(np.int32)
     old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, world, mode)
+    # pull: False (push), True (pull) or "auto" (per-layer movers, shard.move_plan)
+    layer_pull = S.move_plan(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev) if pull == "auto" else None
+    pull = pull is True
 
     def gather(obj):
         o = [None] * world
@@ -96,12 +99,12 @@ def _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull, layouts=(
     old_pools, new_pools = S.setup_rank_pools(
         kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, rank, old_blocks,
         dst_blocks, all_gather=gather, fill=(SEED, live, tokens[live], src_bt), pull=pull,
-        old_layout=layouts[0], new_layout=layouts[1])
+        old_layout=layouts[0], new_layout=layouts[1], layer_pull=layer_pull)
     dist.barrier()
     tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, rank, N,
                         max_blocks, dst_blocks, src_bt, epoch=t.epoch,
                         max_sync_rounds=scn.max_sync_rounds,
-                        kv_bytes_per_token=scn.kv_bytes_per_token, pull=pull)
+                        kv_bytes_per_token=scn.kv_bytes_per_token, pull=pull, layer_pull=layer_pull)
     octx = O.ControlCtx(N, scn.max_sync_rounds, scn.kv_bytes_per_token)
     dp = O.DataPlane(O.geo(L, heads, dim), t.old_boundaries, t.new_boundaries, old_blocks,
                      dst_blocks, N, max_blocks, src_bt)

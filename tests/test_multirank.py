@@ -46,9 +46,33 @@ def test_ranks_shard_every_layer_once_cpu(world):
         assert old_dev == list(range(8)) and new_dev == [0, 2, 4, 6]   # half of each stage crosses NVLink
 
 
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("placement", ["affinity", "disjoint", "spread", "oneway"])
+@pytest.mark.parametrize("policy", ["auto", "push", "pull"])
+def test_move_plan_moves_every_layer_once_cpu(world, placement, policy):
+    """kvx_begin's per-layer mover selection (both pools local: move here;
+    else layer_pull[l] ? the destination's rank : the source's rank), run
+    over every rank: each layer of C3 is moved by exactly one rank, and
+    'auto' pulls exactly the one-way cross-GPU layers."""
+    from paper_2510_11938_b200 import shard as S
+    ob, nb, L = [5, 10, 15, 20, 25, 30, 35], [10, 20, 30], 40
+    old_dev, new_dev = S.placement(L, ob, nb, world, placement)
+    lp = S.move_plan(L, ob, nb, old_dev, new_dev, policy)
+    for l in range(L):
+        s, d = old_dev[S.stage_of(ob, l)], new_dev[S.stage_of(nb, l)]
+        movers = [r for r in range(world)
+                  if (s == r and d == r) or (s != d and ((lp[l] and d == r) or (not lp[l] and s == r)))]
+        assert len(movers) == 1, (l, s, d, movers)
+    cross = [l for l in range(L) if old_dev[S.stage_of(ob, l)] != new_dev[S.stage_of(nb, l)]]
+    if policy == "auto" and world == 8 and placement == "affinity":
+        assert [l for l in range(L) if lp[l]] == cross and len(cross) == 20   # one-way pairs: pulled
+    if policy == "auto" and placement == "disjoint" and world in (2, 4):
+        assert sum(lp) == 0                                                   # two-way: pushed
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("pull", [False, True], ids=["push", "pull"])
-@pytest.mark.parametrize("mode", ["affinity", "disjoint"])
+@pytest.mark.parametrize("pull", [False, True, "auto"], ids=["push", "pull", "auto"])
+@pytest.mark.parametrize("mode", ["affinity", "disjoint", "oneway"])
 @pytest.mark.parametrize("name,heads,dim", [("criterion12", 2, 64), ("engine_consolidate", 2, 64)])
 def test_two_gpu_transition_bit_exact(gpu_count, mode, name, heads, dim, pull):
     if gpu_count < 2:
