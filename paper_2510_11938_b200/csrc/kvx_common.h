@@ -229,7 +229,8 @@ struct kvx_transition {
     int64_t* d_synced_hi = nullptr;
     kvx::LayerPtr* d_layers = nullptr;
     int32_t n_local_layers = 0;
-    int32_t n_peer_layers = 0;  // layers [0, n_peer_layers) of d_layers push to a peer
+    int32_t n_peer_layers = 0;  // layers [0, n_peer_layers) of d_layers cross NVLink (pushed or pulled)
+    int32_t n_pull_layers = 0;  // of which pulled (read from a peer's old pool)
     bool has_peer_dst = false;
     // wave staging: pinned host ring of 2 + device buffer
     char* h_wave[2] = {nullptr, nullptr};

@@ -206,6 +206,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
             if (!dst_local) continue;
             if (!src) return bail(fail(KVX_EINVAL, "pull: a local destination layer has no mapped source pool"));
             t->has_peer_dst = true;  // peer traffic on this handle
+            ++t->n_pull_layers;
         } else {  // this GPU owns the layer's source and pushes it into the (peer) destination
             if (!src_local) continue;
             if (!dst) return bail(fail(KVX_EINVAL, "push: a local source layer has no mapped destination pool"));
@@ -328,16 +329,18 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             const BulkVariant& bv = kBulkVariants[vi];
             // Grid: measured on B200 (profiles/r01_grid_sweep.jsonl), 128 one-CTA-per-SM
             // streams beat all 148 SMs for HBM-bound waves (1.034 vs 0.98 of the copy
-            // peak); NVLink pushes saturate with ~16 CTAs, so mixed waves give the
-            // peer layers kPeerCtas of them and the local layers the rest.
-            constexpr int64_t kLocalGrid = 128, kPeerCtas = 32;
+            // peak).  Mixed waves give the peer layers their own CTAs and the local
+            // layers the rest: NVLink pushes saturate with ~16-32 CTAs, pulls (TMA
+            // loads from the peer) want ~64 (profiles/r01_nvlink_split.jsonl,
+            // r01_movers_n2.jsonl).
+            constexpr int64_t kLocalGrid = 128, kPushCtas = 32, kPullCtas = 64;
+            int32_t peer_ctas = (int32_t)(t->n_pull_layers > 0 ? kPullCtas : kPushCtas);
+            if (const char* pc = getenv("KVX_PEER_CTAS")) peer_ctas = std::max(0, atoi(pc));
             int64_t full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid);
             if (t->n_peer_layers > 0 && t->n_peer_layers < t->n_local_layers)
-                full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid + kPeerCtas);
+                full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid + peer_ctas);
             if (const char* cap = getenv("KVX_BULK_GRID"))
                 full_b = std::max<int64_t>(1, std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], atoll(cap)));
-            int32_t peer_ctas = (int32_t)kPeerCtas;
-            if (const char* pc = getenv("KVX_PEER_CTAS")) peer_ctas = std::max(0, atoi(pc));
             const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
             // programmatic dependent launch: the mover's launch overlaps the
             // plan kernel; it waits (griddepcontrol.wait) for its segments
