@@ -277,10 +277,13 @@ def nccl_baseline(kvx, torch, dist, plan, g, old_pools, old_dev, new_dev, rank, 
 
 
 # -------------------------------------------------------------- CPU baseline
-def cpu_sample_run(plan: Plan, steps: int, warmup: int, threads: int, target_bytes: float = 1.0e9):
+def cpu_sample_run(plan: Plan, steps, warmup: int, threads: int, target_bytes: float = 2.0e9,
+                   seconds: float = 8.0):
     """The oracle executor (oracle/kvx_oracle.c, pthreads) on a bounded sample
     of the same transition: the first requests whose KV totals ~target_bytes.
-    Returns (GB/s, sample description, bytes per step)."""
+    steps=None: as many steps as fill ~`seconds` of CPU work (at least 2),
+    sized from the warm-up step.  Returns (GB/s, sample description, bytes
+    per step)."""
     from oracle import pyoracle as O
     per_req = plan.tokens * plan.kv_bytes_per_token
     order = plan.live
@@ -301,21 +304,25 @@ def cpu_sample_run(plan: Plan, steps: int, warmup: int, threads: int, target_byt
     dp = O.DataPlane(g, t.old_boundaries, t.new_boundaries, old_blocks, dst_blocks, plan.N,
                      plan.max_blocks, src_bt)
     for p in dp.old_pools:  # touch every page (a real KV cache is resident)
-        p[:] = np.arange(p.size, dtype=np.uint64).astype(np.uint8)
+        p.fill(0x5A)
     for p in dp.new_pools:
         p[:] = 0
-    times = []
-    for s in range(warmup + steps):
+    live_m = np.isin(t.live_req, sel)
+
+    def one_step():
         dp.bt[:] = -1
         dp.synced_hi[:] = 0
         dp.d.next_block = 0
         t0 = time.perf_counter()
         for req, lo, hi in waves:
             assert dp.wave(req, lo, hi, threads=threads) == 0
-        live_m = np.isin(t.live_req, sel)
         dp.commit(t.live_req[live_m], t.live_kv[live_m])
-        if s >= warmup:
-            times.append(time.perf_counter() - t0)
+        return time.perf_counter() - t0
+
+    warm = [one_step() for _ in range(max(1, warmup))]
+    if steps is None:
+        steps = int(min(500, max(2, round(seconds / max(1e-6, min(warm))))))
+    times = [one_step() for _ in range(steps)]
     gbs = step_bytes * len(times) / sum(times) / 1e9
     desc = (f"{len(sel)} of {len(plan.live)} live requests of {plan.golden} "
             f"({step_bytes / 1e9:.2f} GB of KV per step, real geometry), same wave plan, "
@@ -842,8 +849,8 @@ def main():
         line["not_a_measurement"] = "ranks share GPUs (KVX_BENCH_FOLD); functional check of the N-rank path"
     if n_gpus == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        gbs, desc, _ = cpu_sample_run(plan, 3, 1, threads)
-        gbs1, desc1, _ = cpu_sample_run(plan, 2, 1, 1, target_bytes=0.25e9)
+        gbs, desc, _ = cpu_sample_run(plan, None, 1, threads, seconds=8.0)
+        gbs1, desc1, _ = cpu_sample_run(plan, None, 1, 1, target_bytes=0.5e9, seconds=3.0)
         line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                                 "sample": desc, "value_1_thread": round(gbs1, 3), "sample_1_thread": desc1,
                                 "reference_control_plane": reference_control_plane(plan.golden)}
