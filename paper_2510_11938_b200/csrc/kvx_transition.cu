@@ -327,13 +327,14 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             const uint64_t run_bytes = nseg > 0 ? (uint64_t)tokens * 2ull * token_bytes(t->g) / (uint64_t)nseg : 0;
             const int vi = t->bulk_variant >= 0 ? t->bulk_variant : (run_bytes >= 65536 ? 2 : 0);
             const BulkVariant& bv = kBulkVariants[vi];
-            // Grid: measured on B200 (profiles/r01_grid_sweep.jsonl), 128 one-CTA-per-SM
-            // streams beat all 148 SMs for HBM-bound waves (1.034 vs 0.98 of the copy
-            // peak).  Mixed waves give the peer layers their own CTAs and the local
-            // layers the rest: NVLink pushes saturate with ~16-32 CTAs, pulls (TMA
-            // loads from the peer) want ~64 (profiles/r01_nvlink_split.jsonl,
-            // r01_movers_n2.jsonl).
-            constexpr int64_t kLocalGrid = 128, kPushCtas = 32, kPullCtas = 64;
+            // Grid: measured on B200 across boxes (profiles/grid_cross_box/): 96
+            // one-CTA-per-SM streams are the best HBM-bound grid on every chip tried
+            // (5.02-5.07 ms for C3 wave 0); 128 ranged 5.02-5.40 and all 148 SMs
+            // 5.26-5.30, depending on the chip.  Mixed waves give the peer layers their
+            // own CTAs and the local layers the rest: NVLink pushes saturate with
+            // ~16-32 CTAs, pulls (TMA loads from the peer) want ~64
+            // (profiles/r01_nvlink_split.jsonl, r01_movers_n2.jsonl).
+            constexpr int64_t kLocalGrid = 96, kPushCtas = 32, kPullCtas = 64;
             int32_t peer_ctas = (int32_t)(t->n_pull_layers > 0 ? kPullCtas : kPushCtas);
             if (const char* pc = getenv("KVX_PEER_CTAS")) peer_ctas = std::max(0, atoi(pc));
             int64_t full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid);
