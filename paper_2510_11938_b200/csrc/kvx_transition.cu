@@ -334,12 +334,17 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             // own CTAs and the local layers the rest: NVLink pushes saturate with
             // ~16-32 CTAs, pulls (TMA loads from the peer) want ~64
             // (profiles/r01_nvlink_split.jsonl, r01_movers_n2.jsonl).
-            constexpr int64_t kLocalGrid = 96, kPushCtas = 32, kPullCtas = 64;
+            // Token-granular waves (delta / final: runs of a few KiB) want more
+            // streams than slab waves: 128 (KVX_BULK_GRID_TOK overrides).
+            constexpr int64_t kLocalGrid = 96, kLocalGridTok = 128, kPushCtas = 32, kPullCtas = 64;
+            static const int64_t grid_tok = getenv("KVX_BULK_GRID_TOK") ? atoll(getenv("KVX_BULK_GRID_TOK"))
+                                                                          : kLocalGridTok;
+            const int64_t local_grid = run_bytes >= 65536 ? kLocalGrid : grid_tok;
             int32_t peer_ctas = (int32_t)(t->n_pull_layers > 0 ? kPullCtas : kPushCtas);
             if (const char* pc = getenv("KVX_PEER_CTAS")) peer_ctas = std::max(0, atoi(pc));
-            int64_t full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid);
+            int64_t full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], local_grid);
             if (t->n_peer_layers > 0 && t->n_peer_layers < t->n_local_layers)
-                full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], kLocalGrid + peer_ctas);
+                full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], local_grid + peer_ctas);
             if (const char* cap = getenv("KVX_BULK_GRID"))
                 full_b = std::max<int64_t>(1, std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], atoll(cap)));
             const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
