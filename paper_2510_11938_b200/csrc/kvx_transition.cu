@@ -334,9 +334,10 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             // own CTAs and the local layers the rest: NVLink pushes saturate with
             // ~16-32 CTAs, pulls (TMA loads from the peer) want ~64
             // (profiles/r01_nvlink_split.jsonl, r01_movers_n2.jsonl).
-            // Token-granular waves (delta / final: runs of a few KiB) want more
-            // streams than slab waves: 128 (KVX_BULK_GRID_TOK overrides).
-            constexpr int64_t kLocalGrid = 96, kLocalGridTok = 128, kPushCtas = 32, kPullCtas = 64;
+            // Token-granular waves (delta / final: runs of a few KiB) want every SM
+            // (C3 final wave: 148 -> 73.8 us, 128 -> 75.8, 96 -> 86.0;
+            // profiles/grid_cross_box/grid_tok.jsonl; KVX_BULK_GRID_TOK overrides).
+            constexpr int64_t kLocalGrid = 96, kLocalGridTok = 148, kPushCtas = 32, kPullCtas = 64;
             static const int64_t grid_tok = getenv("KVX_BULK_GRID_TOK") ? atoll(getenv("KVX_BULK_GRID_TOK"))
                                                                           : kLocalGridTok;
             const int64_t local_grid = run_bytes >= 65536 ? kLocalGrid : grid_tok;
