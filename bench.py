@@ -75,9 +75,10 @@ def ncu_traffic(cfg: str):
     if not files:
         return None, None
     total = 0.0
-    for row in csv.reader(open(files[-1])):
-        if len(row) > 14 and row[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            total += float(row[14].replace(",", ""))
+    with open(files[-1]) as f:
+        for row in csv.reader(f):
+            if len(row) > 14 and row[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                total += float(row[14].replace(",", ""))
     return (total or None), os.path.relpath(files[-1], ROOT)
 
 

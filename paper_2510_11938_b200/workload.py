@@ -130,7 +130,8 @@ class Scenario:
 
 def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
     path = os.path.join(golden_dir, name + ".jsonl")
-    rows = [json.loads(l) for l in open(path)]
+    with open(path) as f:
+        rows = [json.loads(l) for l in f]
     head = rows[0]
     assert head["kind"] == "scenario"
     trans: List[TransitionSpec] = []
