@@ -8,6 +8,9 @@ namespace {
 // copy-list rings: handoff rows (short runs) and weight layers (long runs)
 constexpr int kHandoffStages = 4, kWeightStages = 6;
 constexpr uint32_t kCopyChunk = 32768;
+// weight layers are long contiguous runs: the slab ring (3 x 64 KiB)
+constexpr int kWeightSlabStages = 3;
+constexpr uint32_t kWeightSlabChunk = 65536;
 }  // namespace
 
 namespace kvx_host {
@@ -20,6 +23,10 @@ cudaError_t preload_extras_kernels() {
     if ((e = cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kWeightStages, kCopyChunk>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kWeightStages * (int)kCopyChunk)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(kvx::kvx_copy_list_kernel<kWeightSlabStages, kWeightSlabChunk>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kWeightSlabStages * (int)kWeightSlabChunk)) != cudaSuccess)
         return e;
     cudaFuncAttributes a;
     return cudaFuncGetAttributes(&a, (const void*)kvx::kvx_bm_init_kernel);
@@ -158,12 +165,20 @@ int kvx_weights_migrate(int32_t device, void* stream, int32_t num_layers, uint64
     KVX_CUDA(A.host_alloc(&h, bytes));
     std::memcpy(h, pieces.data(), bytes);
     KVX_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
-    constexpr int kStages = kWeightStages;
-    constexpr uint32_t kChunk = kCopyChunk;  // smem attribute set by preload_extras_kernels
-    if (const int rc = ensure_loaded(device)) return rc;
-    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)sms, (int64_t)pieces.size());
-    kvx::kvx_copy_list_kernel<kStages, kChunk><<<grid, kvx::kBulkThreads, kStages * kChunk, st>>>(
-        static_cast<const kvx::Piece*>(d), (int64_t)pieces.size());
+    if (const int rc = ensure_loaded(device)) return rc;  // also sets the smem attributes
+    // experiment knobs: KVX_WEIGHTS_RING=slab|32k, KVX_WEIGHTS_GRID=<ctas>
+    const char* ring = getenv("KVX_WEIGHTS_RING");
+    const bool slab = !(ring && std::string(ring) == "32k");
+    int64_t gcap = slab ? 96 : (int64_t)sms;
+    if (const char* gg = getenv("KVX_WEIGHTS_GRID")) gcap = std::max<int64_t>(1, atoll(gg));
+    const unsigned grid = (unsigned)std::min<int64_t>(std::min<int64_t>(gcap, sms), (int64_t)pieces.size());
+    if (slab)
+        kvx::kvx_copy_list_kernel<kWeightSlabStages, kWeightSlabChunk>
+            <<<grid, kvx::kBulkThreads, kWeightSlabStages * kWeightSlabChunk, st>>>(
+                static_cast<const kvx::Piece*>(d), (int64_t)pieces.size());
+    else
+        kvx::kvx_copy_list_kernel<kWeightStages, kCopyChunk><<<grid, kvx::kBulkThreads, kWeightStages * kCopyChunk, st>>>(
+            static_cast<const kvx::Piece*>(d), (int64_t)pieces.size());
     KVX_LAUNCHED();
     KVX_CUDA(cudaLaunchHostFunc(st, release_pieces, new PieceRelease{device, d, h, bytes}));
     return KVX_OK;
