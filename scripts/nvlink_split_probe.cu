@@ -113,9 +113,15 @@ int main() {
         CK(cudaMalloc(&g1_dst, bytes));
         (void)g0_dst2;
         (void)g1_src2;
-        const char* names[] = {"bi_push", "bi_pull", "bi_push01_pull10", "bi_copy_engine"};
+        const char* names[] = {"bi_push", "bi_pull", "bi_push01_pull10", "bi_copy_engine", "bi_half_push_half_pull"};
+        cudaStream_t s0b, s1b;
+        CK(cudaSetDevice(0));
+        CK(cudaStreamCreateWithFlags(&s0b, cudaStreamNonBlocking));
+        CK(cudaSetDevice(1));
+        CK(cudaStreamCreateWithFlags(&s1b, cudaStreamNonBlocking));
         for (int ctas : {64, 148}) {
-            for (int mode = 0; mode < 4; ++mode) {
+            for (int mode = 0; mode < 5; ++mode) {
+                if (mode == 2) continue;  // superseded by mode 4
                 double best = 1e30;
                 for (int rep = 0; rep < 4; ++rep) {
                     CK(cudaSetDevice(0));
@@ -138,6 +144,17 @@ int main() {
                     } else if (mode == 1) {  // each GPU pulls its incoming data
                         bulk_copy<<<ctas, 32, kStages * kChunk, s1>>>(g0_src, g1_dst, bytes);
                     } else if (mode == 2) {  // GPU0 pushes 0->1 and pulls 1->0; GPU1 idle
+                    } else if (mode == 4) {  // each direction: half pushed by its sender, half pulled by its receiver
+                        const uint64_t h = bytes / 2;
+                        // GPU1: push first half of 1->0, pull second half of 0->1
+                        CK(cudaStreamWaitEvent(s1b, a, 0));
+                        bulk_copy<<<ctas / 2, 32, kStages * kChunk, s1>>>(g1_src_push, g0_dst_push, h);
+                        bulk_copy<<<ctas / 2, 32, kStages * kChunk, s1b>>>(g0_src + h, g1_dst + h, h);
+                        cudaEvent_t j1;
+                        CK(cudaEventCreateWithFlags(&j1, cudaEventDisableTiming));
+                        CK(cudaEventRecord(j1, s1b));
+                        CK(cudaStreamWaitEvent(s1, j1, 0));
+                        CK(cudaEventDestroy(j1));
                     } else {
                         CK(cudaMemcpyPeerAsync(g0_dst_push, 0, g1_src_push, 1, bytes, s1));
                     }
@@ -150,6 +167,16 @@ int main() {
                     } else if (mode == 2) {
                         bulk_copy<<<ctas / 2, 32, kStages * kChunk, s0>>>(g0_src, g1_dst, bytes);
                         bulk_copy<<<ctas / 2, 32, kStages * kChunk, s0>>>(g1_src_pull, g0_dst_pull, bytes);
+                    } else if (mode == 4) {  // GPU0: push first half of 0->1, pull second half of 1->0
+                        const uint64_t h = bytes / 2;
+                        CK(cudaStreamWaitEvent(s0b, a, 0));
+                        bulk_copy<<<ctas / 2, 32, kStages * kChunk, s0>>>(g0_src, g1_dst, h);
+                        bulk_copy<<<ctas / 2, 32, kStages * kChunk, s0b>>>(g1_src_push + h, g0_dst_push + h, h);
+                        cudaEvent_t j0;
+                        CK(cudaEventCreateWithFlags(&j0, cudaEventDisableTiming));
+                        CK(cudaEventRecord(j0, s0b));
+                        CK(cudaStreamWaitEvent(s0, j0, 0));
+                        CK(cudaEventDestroy(j0));
                     } else {
                         CK(cudaMemcpyPeerAsync(g1_dst, 1, g0_src, 0, bytes, s0));
                     }
