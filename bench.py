@@ -489,8 +489,9 @@ def main():
     ap.add_argument("--pull", action="store_true", help="alias of --move pull")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--layouts", default="blocks,blocks",
-                    help="old,new pool layouts: blocks (FlashInfer [blocks][2][B][H][D]) or planes "
-                         "(FlashAttention [2][blocks][B][H][D]); unequal = the refactor converts")
+                    help="old,new pool layouts: blocks (FlashInfer NHD [blocks][2][B][H][D]), planes "
+                         "(FlashAttention [2][blocks][B][H][D]) or heads (FlashInfer HND [blocks][2][H][B][D], "
+                         "vLLM's FlashInfer layout on B200); unequal = the refactor converts")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -527,7 +528,8 @@ def main():
     plan = Plan(args.config)
     t = plan.t
     L = plan.L
-    layouts = [{"blocks": kvx.LAYOUT_BLOCKS, "planes": kvx.LAYOUT_KV_PLANES}[x] for x in args.layouts.split(",")]
+    layouts = [{"blocks": kvx.LAYOUT_BLOCKS, "planes": kvx.LAYOUT_KV_PLANES, "heads": kvx.LAYOUT_HEADS}[x]
+               for x in args.layouts.split(",")]
     g = kvx.geometry(L, plan.H, plan.D)
     old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, n_gpus, args.placement)
     if args.pull:

@@ -109,9 +109,16 @@ int kvx_pool_import(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_BYTES],
  *                        rows of a block side by side (FlashInfer NHD paged
  *                        cache; the default of every call above)
  *   KVX_LAYOUT_KV_PLANES layer = [2][num_blocks][block_tokens][H][D]: a K plane
- *                        and a V plane (FlashAttention paged cache) */
+ *                        and a V plane (FlashAttention paged cache)
+ *   KVX_LAYOUT_HEADS     layer = [num_blocks][2][H][block_tokens][D]: head-major
+ *                        blocks (FlashInfer HND, which vLLM's FlashInfer backend
+ *                        requires on compute capability 10, i.e. B200)
+ * Token-major (BLOCKS, KV_PLANES) to token-major and head-major to head-major
+ * moves are run copies; a move between the two families transposes each
+ * block's (token, head) rows. */
 #define KVX_LAYOUT_BLOCKS 0
 #define KVX_LAYOUT_KV_PLANES 1
+#define KVX_LAYOUT_HEADS 2
 /* kvx_pool_create / _import with an explicit per-layer layout (one
  * allocation, layers back to back). */
 int kvx_pool_create_layout(int32_t device, const kvx_geometry* g, int32_t num_layers,

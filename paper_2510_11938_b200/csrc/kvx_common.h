@@ -68,7 +68,9 @@ inline bool geometry_ok(const kvx_geometry* g, std::string* why) {
     return true;
 }
 
-inline bool layout_ok(int32_t layout) { return layout == KVX_LAYOUT_BLOCKS || layout == KVX_LAYOUT_KV_PLANES; }
+inline bool layout_ok(int32_t layout) {
+    return layout == KVX_LAYOUT_BLOCKS || layout == KVX_LAYOUT_KV_PLANES || layout == KVX_LAYOUT_HEADS;
+}
 
 inline uint64_t token_bytes(const kvx_geometry& g) {
     return (uint64_t)g.num_kv_heads * (uint64_t)g.head_dim * (uint64_t)g.elem_bytes;
@@ -158,7 +160,9 @@ struct kvx_pool {
     std::vector<char*> layer_base;  // per layer, in every pool
 
     uint64_t layer_bytes() const { return (uint64_t)num_blocks * 2ull * g.block_tokens * kvx_host::token_bytes(g); }
-    // bytes between consecutive blocks of a layer, and from a block's K rows to its V rows
+    // Address of (block b, K|V k, token t, head h) in a layer:
+    //   base + b*blk_stride + k*kv_stride + t*tok_stride + h*head_stride
+    uint64_t head_bytes() const { return (uint64_t)g.head_dim * (uint64_t)g.elem_bytes; }
     uint64_t blk_stride() const {
         const uint64_t plane = (uint64_t)g.block_tokens * kvx_host::token_bytes(g);
         return layout == KVX_LAYOUT_KV_PLANES ? plane : 2 * plane;
@@ -167,6 +171,11 @@ struct kvx_pool {
         const uint64_t plane = (uint64_t)g.block_tokens * kvx_host::token_bytes(g);
         return layout == KVX_LAYOUT_KV_PLANES ? (uint64_t)num_blocks * plane : plane;
     }
+    uint64_t tok_stride() const { return layout == KVX_LAYOUT_HEADS ? head_bytes() : kvx_host::token_bytes(g); }
+    uint64_t head_stride() const {
+        return layout == KVX_LAYOUT_HEADS ? (uint64_t)g.block_tokens * head_bytes() : head_bytes();
+    }
+    bool head_major() const { return layout == KVX_LAYOUT_HEADS; }
     void set_contiguous_layers() {
         layer_base.resize((size_t)num_layers);
         for (int32_t l = 0; l < num_layers; ++l) layer_base[(size_t)l] = base + (uint64_t)l * layer_bytes();
@@ -175,7 +184,8 @@ struct kvx_pool {
 
 // A pool's addressing for the payload kernels; d_layers = its layer_base on the device.
 inline kvx::PoolAddr pool_addr(const kvx_pool* p, char* const* d_layers) {
-    return kvx::PoolAddr{d_layers, p->blk_stride(), p->kv_stride()};
+    return kvx::PoolAddr{d_layers, p->blk_stride(), p->kv_stride(), p->tok_stride(), p->head_stride(),
+                         (uint32_t)p->head_bytes()};
 }
 
 // Device-resident block manager: a free-id stack on the GPU, its top mirrored
@@ -231,6 +241,7 @@ struct kvx_transition {
     int32_t n_local_layers = 0;
     int32_t n_peer_layers = 0;  // layers [0, n_peer_layers) of d_layers cross NVLink (pushed or pulled)
     int32_t n_pull_layers = 0;  // of which pulled (read from a peer's old pool)
+    bool transpose = false;     // some layer pairs a token-major with a head-major pool
     bool has_peer_dst = false;
     // wave staging: pinned host ring of 2 + device buffer
     char* h_wave[2] = {nullptr, nullptr};

@@ -44,16 +44,22 @@ struct Seg {  // one logical block of one request inside one wave
     int32_t t1;  // one past the last token
 };
 
-struct LayerPtr {  // layer l in the old / new pool: base, block stride, K->V offset
+struct LayerPtr {  // layer l in the old / new pool (address of block b, K|V k, token t, head h:
+                   //   base + b*bs + k*kv + t*ts + h*hs)
     char* src;
     char* dst;
     uint64_t src_bs, dst_bs;  // bytes between consecutive blocks (layout-dependent)
     uint64_t src_kv, dst_kv;  // bytes from a block's K rows to its V rows
+    uint64_t src_ts, dst_ts;  // token stride
+    uint64_t src_hs, dst_hs;  // head stride
+    uint32_t run_tok;         // run copies: bytes per token of one run (token_bytes or head bytes)
+    uint32_t nh;              // run copies: runs per K/V of a partial block (1 token-major, H head-major)
 };
 
 struct PoolAddr {  // one pool for the payload kernels: per-layer bases + strides
     char* const* layer;  // device array, one base per layer
-    uint64_t blk_stride, kv_stride;
+    uint64_t blk_stride, kv_stride, tok_stride, head_stride;
+    uint32_t head_bytes;
 };
 
 // ---------------------------------------------------------------- payload
@@ -274,12 +280,14 @@ kvx_move256_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* _
         char* dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
         if (sg.t0 == 0 && sg.t1 == block_tokens && lp.src_kv == half && lp.dst_kv == half) {
             cta_copy256(reinterpret_cast<V8*>(dst), reinterpret_cast<const V8*>(src), (uint32_t)(block_bytes >> 5));
-        } else {
-            const uint64_t off = (uint64_t)sg.t0 * token_bytes;
-            const uint32_t n = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * token_bytes) >> 5);
-            cta_copy256(reinterpret_cast<V8*>(dst + off), reinterpret_cast<const V8*>(src + off), n);
-            cta_copy256(reinterpret_cast<V8*>(dst + lp.dst_kv + off), reinterpret_cast<const V8*>(src + lp.src_kv + off),
-                        n);
+        } else {  // K then V rows; per head for head-major pools
+            const uint64_t off = (uint64_t)sg.t0 * lp.run_tok;
+            const uint32_t n = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * lp.run_tok) >> 5);
+            for (uint32_t r = 0; r < 2 * lp.nh; ++r) {
+                const uint32_t kv = r / lp.nh, h = r % lp.nh;
+                cta_copy256(reinterpret_cast<V8*>(dst + kv * lp.dst_kv + h * lp.dst_hs + off),
+                            reinterpret_cast<const V8*>(src + kv * lp.src_kv + h * lp.src_hs + off), n);
+            }
         }
     }
     if (fence_system) __threadfence_system();
@@ -306,16 +314,50 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
         if (sg.t0 == 0 && sg.t1 == block_tokens && lp.src_kv == half && lp.dst_kv == half) {
             cta_copy(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src),
                      (uint32_t)(block_bytes >> 4));
-        } else {
-            const uint64_t off = (uint64_t)sg.t0 * token_bytes;
-            const uint32_t nvec = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * token_bytes) >> 4);
-            cta_copy(reinterpret_cast<uint4*>(dst + off), reinterpret_cast<const uint4*>(src + off),
-                     nvec);
-            cta_copy(reinterpret_cast<uint4*>(dst + lp.dst_kv + off),
-                     reinterpret_cast<const uint4*>(src + lp.src_kv + off), nvec);
+        } else {  // K then V rows; per head for head-major pools
+            const uint64_t off = (uint64_t)sg.t0 * lp.run_tok;
+            const uint32_t nvec = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * lp.run_tok) >> 4);
+            for (uint32_t r = 0; r < 2 * lp.nh; ++r) {
+                const uint32_t kv = r / lp.nh, h = r % lp.nh;
+                cta_copy(reinterpret_cast<uint4*>(dst + kv * lp.dst_kv + h * lp.dst_hs + off),
+                         reinterpret_cast<const uint4*>(src + kv * lp.src_kv + h * lp.src_hs + off), nvec);
+            }
         }
     }
     if (fence_system) __threadfence_system();  // peer (NVLink) stores visible before host sync
+}
+
+// --------------------------------------------- layout-transposing mover
+// Moves between token-major (BLOCKS, KV_PLANES) and head-major (HEADS) pools:
+// every (K|V, token, head) row of head_bytes is its own piece, addressed
+// through both layouts' strides.  Consecutive threads take consecutive
+// 16-byte vectors of a row, then the next head of the same token, so one side
+// is read or written fully coalesced and the other in head_bytes pieces
+// (D*elem, 256 B at D=128 fp16: whole DRAM sectors).
+static __global__ void __launch_bounds__(kMoveThreads)
+kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
+                    int32_t nlayers, int32_t heads, uint32_t head_bytes, int32_t fence_system) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int64_t units = (int64_t)nseg * nlayers;
+    const uint32_t vph = head_bytes >> 4;  // 16-byte vectors per head row
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t layer = (int32_t)(u / nseg);
+        const Seg sg = segs[u - (int64_t)layer * nseg];
+        const LayerPtr lp = layers[layer];
+        const char* sb = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
+        char* db = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
+        const uint32_t ntok = (uint32_t)(sg.t1 - sg.t0);
+        const uint32_t per_kv = ntok * (uint32_t)heads * vph;
+        for (uint32_t i = threadIdx.x; i < 2 * per_kv; i += kMoveThreads) {
+            const uint32_t kv = i / per_kv, r = i - kv * per_kv;
+            const uint32_t w = r % vph, th = r / vph;
+            const uint32_t h = th % (uint32_t)heads, t = (uint32_t)sg.t0 + th / (uint32_t)heads;
+            const uint4* s = reinterpret_cast<const uint4*>(sb + kv * lp.src_kv + t * lp.src_ts + h * lp.src_hs) + w;
+            uint4* d = reinterpret_cast<uint4*>(db + kv * lp.dst_kv + t * lp.dst_ts + h * lp.dst_hs) + w;
+            st_stream(d, ld_stream(s));
+        }
+    }
+    if (fence_system) __threadfence_system();
 }
 
 // ------------------------------------------------------- TMA bulk mover
@@ -380,11 +422,12 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
     const char* src;
     char* dst;
     uint64_t left;
-    int run;       // 0 or 1 (K then V of a partial block)
+    int run, nrun;  // current run / runs of the unit: 1 (whole block), 2 (K, V) or 2*nh
+    uint32_t nh;    // runs per K/V (head-major pools: one per head)
     uint64_t run_bytes, off0;
     const char* base_src;
     char* base_dst;
-    uint64_t src_kv, dst_kv;  // K -> V offsets of the current unit's layer
+    uint64_t src_kv, dst_kv, src_hs, dst_hs;  // of the current unit's layer
 
     __device__ bool load_unit() {
         while (u < units) {
@@ -395,15 +438,20 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
             base_dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
             src_kv = lp.src_kv;
             dst_kv = lp.dst_kv;
+            src_hs = lp.src_hs;
+            dst_hs = lp.dst_hs;
             const uint64_t half = block_bytes >> 1;
+            run = 0;
             if (sg.t0 == 0 && sg.t1 == block_tokens && src_kv == half && dst_kv == half) {
-                run = 1;  // one run covering K and V (adjacent on both sides)
+                nrun = 1;  // the whole block is one run on both sides (BLOCKS, HEADS)
+                nh = 1;
                 off0 = 0;
                 run_bytes = block_bytes;
-            } else {
-                run = 0;  // K rows, then V rows
-                off0 = (uint64_t)sg.t0 * token_bytes;
-                run_bytes = (uint64_t)(sg.t1 - sg.t0) * token_bytes;
+            } else {  // K rows then V rows; per head for head-major pools
+                nh = lp.nh;
+                nrun = 2 * (int)nh;
+                off0 = (uint64_t)sg.t0 * lp.run_tok;
+                run_bytes = (uint64_t)(sg.t1 - sg.t0) * lp.run_tok;
             }
             src = base_src + off0;
             dst = base_dst + off0;
@@ -414,10 +462,10 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
     }
     __device__ bool next(const char** s, char** d, uint32_t* n) {
         while (left == 0) {
-            if (run == 0) {  // move on to the V rows
-                run = 1;
-                src = base_src + src_kv + off0;
-                dst = base_dst + dst_kv + off0;
+            if (++run < nrun) {  // next (K|V, head) run of the unit
+                const uint32_t kv = (uint32_t)run / nh, h = (uint32_t)run % nh;
+                src = base_src + kv * src_kv + h * src_hs + off0;
+                dst = base_dst + kv * dst_kv + h * dst_hs + off0;
                 left = run_bytes;
                 break;
             }
@@ -682,9 +730,11 @@ kvx_fill_kernel(PoolAddr pa, int32_t first_layer,
             for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
                 const int32_t kvi = kvr / rows, t = kvr % rows;
                 const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
-                uint4* row = reinterpret_cast<uint4*>(slab + (uint64_t)kvi * pa.kv_stride +
-                                                      (uint64_t)(row0 + t) * token_bytes);
-                for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) row[v] = pattern_vec(th, v);
+                char* row = slab + (uint64_t)kvi * pa.kv_stride + (uint64_t)(row0 + t) * pa.tok_stride;
+                const uint32_t vph = pa.head_bytes >> 4;  // vector v of the token lies in head v / vph
+                for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x)
+                    *reinterpret_cast<uint4*>(row + (uint64_t)(v / vph) * pa.head_stride + (v % vph) * 16u) =
+                        pattern_vec(th, v);
             }
         }
     }
@@ -714,10 +764,12 @@ kvx_verify_kernel(PoolAddr pa, int32_t first_layer,
             for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
                 const int32_t kvi = kvr / rows, t = kvr % rows;
                 const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
-                const uint4* row = reinterpret_cast<const uint4*>(slab + (uint64_t)kvi * pa.kv_stride +
-                                                                  (uint64_t)t * token_bytes);
+                const char* row = slab + (uint64_t)kvi * pa.kv_stride + (uint64_t)t * pa.tok_stride;
+                const uint32_t vph = pa.head_bytes >> 4;
                 for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) {
-                    const uint4 want = pattern_vec(th, v), got = row[v];
+                    const uint4 want = pattern_vec(th, v);
+                    const uint4 got =
+                        *reinterpret_cast<const uint4*>(row + (uint64_t)(v / vph) * pa.head_stride + (v % vph) * 16u);
                     const uint32_t d[4] = {want.x ^ got.x, want.y ^ got.y, want.z ^ got.z, want.w ^ got.w};
 #pragma unroll
                     for (int q = 0; q < 4; ++q) bad += ((d[q] & 0xffffu) != 0) + ((d[q] >> 16) != 0);

@@ -17,6 +17,7 @@ cudaError_t preload_transition_kernels() {
     cudaFuncAttributes a;
     cudaError_t e = cudaSuccess;
     for (const void* fn : {(const void*)kvx::kvx_plan_kernel, (const void*)kvx::kvx_move_kernel,
+                           (const void*)kvx::kvx_move_any_kernel,
                            (const void*)kvx::kvx_move256_kernel, (const void*)kvx::kvx_commit_kernel,
                            (const void*)kvx::kvx_verify_kernel})
         if ((e = cudaFuncGetAttributes(&a, fn)) != cudaSuccess) return e;
@@ -211,9 +212,16 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
             if (!src_local) continue;
             if (!dst) return bail(fail(KVX_EINVAL, "push: a local source layer has no mapped destination pool"));
         }
+        // run copies need both sides token-major or both head-major; otherwise the
+        // wave goes through the transposing mover (kvx_move_any_kernel)
+        const bool heads_runs = src->head_major() && dst->head_major();
+        if (src->head_major() != dst->head_major()) t->transpose = true;
         layers.push_back({src->layer_base[(size_t)(l - stage_begin(ob, so))],
                           dst->layer_base[(size_t)(l - stage_begin(nb, sn))], src->blk_stride(), dst->blk_stride(),
-                          src->kv_stride(), dst->kv_stride()});
+                          src->kv_stride(), dst->kv_stride(), src->tok_stride(), dst->tok_stride(),
+                          src->head_stride(), dst->head_stride(),
+                          (uint32_t)(heads_runs ? src->head_bytes() : token_bytes(g)),
+                          heads_runs ? (uint32_t)g.num_kv_heads : 1u});
         layer_is_peer.push_back(dst->imported || src->imported ? 1 : 0);
         if (dst->imported) t->has_peer_dst = true;
     }
@@ -323,7 +331,11 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         t->move_bytes.push_back(2ull * (uint64_t)tokens * 2ull * token_bytes(t->g) *
                                 (uint64_t)t->n_local_layers);
         KVX_CUDA(cudaEventRecord(ev.first, t->stream));
-        if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
+        if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
+            kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
+                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
+                (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->has_peer_dst ? 1 : 0);
+        } else if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
             const uint64_t run_bytes = nseg > 0 ? (uint64_t)tokens * 2ull * token_bytes(t->g) / (uint64_t)nseg : 0;
             const int vi = t->bulk_variant >= 0 ? t->bulk_variant : (run_bytes >= 65536 ? 2 : 0);
             const BulkVariant& bv = kBulkVariants[vi];

@@ -31,7 +31,8 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libkvx.so")
 
 KVX_OK, KVX_EINVAL, KVX_ESTALE, KVX_ENOSPC, KVX_ECUDA, KVX_ESTATE = 0, -1, -2, -3, -4, -5
 ACT_DELTA, ACT_BARRIER_WAIT, ACT_FINAL = 0, 1, 2
-LAYOUT_BLOCKS, LAYOUT_KV_PLANES = 0, 1  # per layer [blocks][2][B][H][D] | [2][blocks][B][H][D]
+# per layer: [blocks][2][B][H][D] | [2][blocks][B][H][D] | [blocks][2][H][B][D] (HND, vLLM FlashInfer on B200)
+LAYOUT_BLOCKS, LAYOUT_KV_PLANES, LAYOUT_HEADS = 0, 1, 2
 IPC_HANDLE_BYTES = 64
 
 

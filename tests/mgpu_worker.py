@@ -138,9 +138,11 @@ def _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull, layouts=(
     for j, (b, e) in enumerate(W.stage_ranges(L, t.new_boundaries)):
         if new_dev[j] == rank:
             got = new_pools[j].read().reshape(e - b, -1)
-            want = dp.new_pools[j].reshape(e - b, dst_blocks, 2, -1)
-            if layouts[1] == kvx.LAYOUT_KV_PLANES:     # the oracle is in the block layout
-                want = want.transpose(0, 2, 1, 3)
+            want = dp.new_pools[j].reshape(e - b, dst_blocks, 2, 16, heads, -1)  # the oracle: block layout
+            if layouts[1] == kvx.LAYOUT_KV_PLANES:
+                want = want.transpose(0, 2, 1, 3, 4, 5)
+            elif layouts[1] == kvx.LAYOUT_HEADS:
+                want = want.transpose(0, 1, 2, 4, 3, 5)
             assert np.array_equal(got, np.ascontiguousarray(want).reshape(e - b, -1)), \
                 f"new stage {j} differs on rank {rank}"
             checked += 1

@@ -97,8 +97,9 @@ def test_two_gpu_controller_chain_bit_exact(gpu_count, mode):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("pull", [False, True], ids=["push", "pull"])
-@pytest.mark.parametrize("layouts", [(1, 0), (0, 1), (1, 1)], ids=["planes-to-blocks", "blocks-to-planes",
-                                                                     "planes"])
+@pytest.mark.parametrize("layouts", [(1, 0), (0, 1), (1, 1), (2, 2), (0, 2), (2, 1)],
+                         ids=["planes-to-blocks", "blocks-to-planes", "planes", "heads", "blocks-to-heads",
+                              "heads-to-planes"])
 def test_two_gpu_layout_conversion_bit_exact(gpu_count, layouts, pull):
     """Cross-GPU transitions between K/V-plane and block pools: peers map each
     other's pools with their layout (kvx_pool_import_layout); the moved
