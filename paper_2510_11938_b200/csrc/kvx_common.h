@@ -71,6 +71,10 @@ inline bool geometry_ok(const kvx_geometry* g, std::string* why) {
 inline bool layout_ok(int32_t layout) {
     return layout == KVX_LAYOUT_BLOCKS || layout == KVX_LAYOUT_KV_PLANES || layout == KVX_LAYOUT_HEADS;
 }
+// head-major rows are head_dim * elem_bytes long: 16-byte vectors / bulk-copy alignment
+inline bool layout_fits(int32_t layout, const kvx_geometry& g) {
+    return layout != KVX_LAYOUT_HEADS || ((int64_t)g.head_dim * g.elem_bytes) % 16 == 0;
+}
 
 inline uint64_t token_bytes(const kvx_geometry& g) {
     return (uint64_t)g.num_kv_heads * (uint64_t)g.head_dim * (uint64_t)g.elem_bytes;

@@ -27,6 +27,7 @@ int kvx_pool_create_layout(int32_t device, const kvx_geometry* g, int32_t num_la
     if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
     if (num_layers < 1 || num_blocks < 1) return fail(KVX_EINVAL, "num_layers/num_blocks must be >= 1");
     if (!layout_ok(layout)) return fail(KVX_EINVAL, "unknown layout");
+    if (!layout_fits(layout, *g)) return fail(KVX_EINVAL, "head-major layout needs head_dim * elem_bytes % 16 == 0");
     DeviceGuard dg(device);
     if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed for pool device");
     if (const int rc = ensure_loaded(device)) return rc;
@@ -80,6 +81,7 @@ int kvx_pool_wrap_layers(int32_t device, int32_t num_layers, void* const* layer_
     if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
     if (num_layers < 1 || num_blocks < 1) return fail(KVX_EINVAL, "num_layers/num_blocks must be >= 1");
     if (!layout_ok(layout)) return fail(KVX_EINVAL, "unknown layout");
+    if (!layout_fits(layout, *g)) return fail(KVX_EINVAL, "head-major layout needs head_dim * elem_bytes % 16 == 0");
     if (!layer_ptrs) return fail(KVX_EINVAL, "layer_ptrs is null");
     if (layer_bytes < (uint64_t)num_blocks * block_bytes(*g))
         return fail(KVX_EINVAL, "layer allocation smaller than num_blocks blocks");
@@ -130,6 +132,7 @@ int kvx_pool_import_layout(int32_t device, const uint8_t handle[KVX_IPC_HANDLE_B
     if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
     if (num_layers < 1 || num_blocks < 1) return fail(KVX_EINVAL, "num_layers/num_blocks must be >= 1");
     if (!layout_ok(layout)) return fail(KVX_EINVAL, "unknown layout");
+    if (!layout_fits(layout, *g)) return fail(KVX_EINVAL, "head-major layout needs head_dim * elem_bytes % 16 == 0");
     DeviceGuard dg(device);
     if (const int rc = ensure_loaded(device)) return rc;
     cudaIpcMemHandle_t h;

@@ -97,6 +97,8 @@ def test_layout_validation():
     g = kvx.geometry(4, 2, 64)
     h = C.c_void_p()
     assert L.kvx_pool_create_layout(0, C.byref(g), 2, 4, 7, C.byref(h)) == kvx.KVX_EINVAL   # unknown layout
+    g8 = kvx.geometry(4, 4, 4)                                # 8-byte head rows: no head-major layout
+    assert L.kvx_pool_create_layout(0, C.byref(g8), 2, 4, kvx.LAYOUT_HEADS, C.byref(h)) == kvx.KVX_EINVAL
     ok = (C.c_void_p * 2)(0x1000, 0x2000)
     bb = g.block_bytes
     W = L.kvx_pool_wrap_layers
