@@ -327,34 +327,56 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     if (fence_system) __threadfence_system();  // peer (NVLink) stores visible before host sync
 }
 
-// --------------------------------------------- layout-transposing mover
-// Moves between token-major (BLOCKS, KV_PLANES) and head-major (HEADS) pools:
-// every (K|V, token, head) row of head_bytes is its own piece, addressed
-// through both layouts' strides.  Consecutive threads take consecutive
-// 16-byte vectors of a row, then the next head of the same token, so one side
-// is read or written fully coalesced and the other in head_bytes pieces
-// (D*elem, 256 B at D=128 fp16: whole DRAM sectors).
+// --------------------------------------------- row-granular mover
+// Copies (K|V, token, head) rows of head_bytes, addressed through both
+// pools' strides -- any layout pair.  Used for moves between token-major
+// (BLOCKS, KV_PLANES) and head-major (HEADS) pools (tails_only = 0), and for
+// the partial blocks of head-major-to-head-major moves, whose 2*H short runs
+// would starve the bulk mover's single issuing thread (tails_only = 1: full
+// blocks are left to kvx_bulk_kernel).  Vectors of one row go to consecutive
+// threads; rows are ordered tokens-inner when the source is head-major (its
+// contiguous direction), heads-inner otherwise.  4 independent 16-byte loads
+// in flight per thread.
 static __global__ void __launch_bounds__(kMoveThreads)
 kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
-                    int32_t nlayers, int32_t heads, uint32_t head_bytes, int32_t fence_system) {
+                    int32_t nlayers, int32_t heads, uint32_t head_bytes, int32_t block_tokens,
+                    int32_t tails_only, int32_t fence_system) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int kU = 4;
     const int64_t units = (int64_t)nseg * nlayers;
-    const uint32_t vph = head_bytes >> 4;  // 16-byte vectors per head row
+    const uint32_t vph = head_bytes >> 4;  // 16-byte vectors per row
+    const uint32_t H = (uint32_t)heads;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         const int32_t layer = (int32_t)(u / nseg);
         const Seg sg = segs[u - (int64_t)layer * nseg];
         const LayerPtr lp = layers[layer];
+        if (tails_only && (lp.nh <= 1 || (sg.t0 == 0 && sg.t1 == block_tokens))) continue;
         const char* sb = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
         char* db = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
         const uint32_t ntok = (uint32_t)(sg.t1 - sg.t0);
-        const uint32_t per_kv = ntok * (uint32_t)heads * vph;
-        for (uint32_t i = threadIdx.x; i < 2 * per_kv; i += kMoveThreads) {
-            const uint32_t kv = i / per_kv, r = i - kv * per_kv;
-            const uint32_t w = r % vph, th = r / vph;
-            const uint32_t h = th % (uint32_t)heads, t = (uint32_t)sg.t0 + th / (uint32_t)heads;
-            const uint4* s = reinterpret_cast<const uint4*>(sb + kv * lp.src_kv + t * lp.src_ts + h * lp.src_hs) + w;
-            uint4* d = reinterpret_cast<uint4*>(db + kv * lp.dst_kv + t * lp.dst_ts + h * lp.dst_hs) + w;
-            st_stream(d, ld_stream(s));
+        const uint32_t per_kv = ntok * H * vph;
+        const bool tok_inner = lp.src_ts < lp.src_hs;  // head-major source
+        const uint32_t total = 2 * per_kv;
+        for (uint32_t base = threadIdx.x; base < total; base += kMoveThreads * kU) {
+            uint4 v[kU];
+            uint4* dp[kU];
+#pragma unroll
+            for (int k = 0; k < kU; ++k) {
+                const uint32_t i = base + (uint32_t)k * kMoveThreads;
+                dp[k] = nullptr;
+                if (i < total) {
+                    const uint32_t kv = i / per_kv, r = i - kv * per_kv;
+                    const uint32_t w = r % vph, row = r / vph;
+                    const uint32_t h = tok_inner ? row / ntok : row % H;
+                    const uint32_t t = (uint32_t)sg.t0 + (tok_inner ? row % ntok : row / H);
+                    v[k] = ld_stream(reinterpret_cast<const uint4*>(sb + kv * lp.src_kv + t * lp.src_ts +
+                                                                    h * lp.src_hs) + w);
+                    dp[k] = reinterpret_cast<uint4*>(db + kv * lp.dst_kv + t * lp.dst_ts + h * lp.dst_hs) + w;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kU; ++k)
+                if (dp[k]) st_stream(dp[k], v[k]);
         }
     }
     if (fence_system) __threadfence_system();
@@ -430,10 +452,12 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
     uint64_t src_kv, dst_kv, src_hs, dst_hs;  // of the current unit's layer
 
     __device__ bool load_unit() {
-        while (u < units) {
+        for (; u < units; u += ustep) {
             const int32_t layer = (int32_t)(u / nseg);
             const Seg sg = segs[u - (int64_t)layer * nseg];
             const LayerPtr lp = layers[layer];
+            const bool full = sg.t0 == 0 && sg.t1 == block_tokens;
+            if (lp.nh > 1 && !full) continue;  // head-major tail: kvx_move_any_kernel(tails_only)
             base_src = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
             base_dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
             src_kv = lp.src_kv;

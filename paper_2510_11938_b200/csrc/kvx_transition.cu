@@ -216,6 +216,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         // wave goes through the transposing mover (kvx_move_any_kernel)
         const bool heads_runs = src->head_major() && dst->head_major();
         if (src->head_major() != dst->head_major()) t->transpose = true;
+        if (heads_runs && g.num_kv_heads > 1) t->head_tails = true;
         layers.push_back({src->layer_base[(size_t)(l - stage_begin(ob, so))],
                           dst->layer_base[(size_t)(l - stage_begin(nb, sn))], src->blk_stride(), dst->blk_stride(),
                           src->kv_stride(), dst->kv_stride(), src->tok_stride(), dst->tok_stride(),
@@ -334,7 +335,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
             kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
-                (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->has_peer_dst ? 1 : 0);
+                (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0);
         } else if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
             const uint64_t run_bytes = nseg > 0 ? (uint64_t)tokens * 2ull * token_bytes(t->g) / (uint64_t)nseg : 0;
             const int vi = t->bulk_variant >= 0 ? t->bulk_variant : (run_bytes >= 65536 ? 2 : 0);
@@ -377,6 +378,12 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                                         (const kvx::LayerPtr*)t->d_layers, t->n_local_layers,
                                         block_bytes(t->g), token_bytes(t->g), t->g.block_tokens,
                                         t->n_peer_layers, peer_ctas));
+            if (t->head_tails) {  // head-major partial blocks: the row mover (bulk skipped them)
+                KVX_LAUNCHED();
+                kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
+                    t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
+                    (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 1, t->has_peer_dst ? 1 : 0);
+            }
         } else if (t->lsu256 && token_bytes(t->g) % 32 == 0) {
             kvx::kvx_move256_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
