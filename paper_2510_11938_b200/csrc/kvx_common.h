@@ -247,6 +247,8 @@ struct kvx_transition {
     int32_t n_pull_layers = 0;  // of which pulled (read from a peer's old pool)
     bool transpose = false;     // some layer pairs a token-major with a head-major pool
     bool head_tails = false;    // head-major to head-major layers (H > 1): partial blocks go to the row mover
+    cudaStream_t side = nullptr;  // ... launched on this side stream beside the bulk mover
+    cudaEvent_t ev_join = nullptr;
     bool has_peer_dst = false;
     // wave staging: pinned host ring of 2 + device buffer
     char* h_wave[2] = {nullptr, nullptr};

@@ -242,6 +242,11 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
                             cudaMemcpyHostToDevice, t->stream) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "layer table upload"));
     }
+    if (t->head_tails) {  // side stream for the head-major tail mover (see kvx_wave)
+        if (cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking) != cudaSuccess ||
+            A.event(&t->ev_join, false) != cudaSuccess)
+            return bail(fail(KVX_ECUDA, "side stream"));
+    }
     // No host sync: the uploads above were staged from pageable memory
     // (copied out before cudaMemcpyAsync returned) and are stream-ordered
     // before every wave.
@@ -378,11 +383,17 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                                         (const kvx::LayerPtr*)t->d_layers, t->n_local_layers,
                                         block_bytes(t->g), token_bytes(t->g), t->g.block_tokens,
                                         t->n_peer_layers, peer_ctas));
-            if (t->head_tails) {  // head-major partial blocks: the row mover (bulk skipped them)
+            if (t->head_tails) {
+                // head-major partial blocks (the bulk mover skips them): the row mover on a
+                // side stream forked after the plan kernel, so it runs beside the bulk
+                // mover (which holds only ~96 SMs) and joins before the wave's end event
                 KVX_LAUNCHED();
-                kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
+                KVX_CUDA(cudaStreamWaitEvent(t->side, t->h_wave_free[slot], 0));
+                kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->side>>>(
                     t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                     (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 1, t->has_peer_dst ? 1 : 0);
+                KVX_CUDA(cudaEventRecord(t->ev_join, t->side));
+                KVX_CUDA(cudaStreamWaitEvent(t->stream, t->ev_join, 0));
             }
         } else if (t->lsu256 && token_bytes(t->g) % 32 == 0) {
             kvx::kvx_move256_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
@@ -597,6 +608,11 @@ int kvx_destroy(kvx_transition* t) {
         A.event_free(ev.first, true);
         A.event_free(ev.second, true);
     }
+    if (t->side) {
+        cudaStreamSynchronize(t->side);
+        cudaStreamDestroy(t->side);
+    }
+    A.event_free(t->ev_join, false);
     if (t->stream && t->own_stream) cudaStreamDestroy(t->stream);
     delete t;
     return KVX_OK;
