@@ -340,7 +340,7 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
 static __global__ void __launch_bounds__(kMoveThreads)
 kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
                     int32_t nlayers, int32_t heads, uint32_t head_bytes, int32_t block_tokens,
-                    int32_t tails_only, int32_t fence_system, int32_t order_by_dst = 0) {
+                    int32_t tails_only, int32_t fence_system) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     constexpr int kU = 4;
     const int64_t units = (int64_t)nseg * nlayers;
@@ -355,7 +355,8 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
         char* db = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
         const uint32_t ntok = (uint32_t)(sg.t1 - sg.t0);
         const uint32_t per_kv = ntok * H * vph;
-        const bool tok_inner = order_by_dst ? lp.dst_ts < lp.dst_hs : lp.src_ts < lp.src_hs;
+        const bool tok_inner = lp.src_ts < lp.src_hs;  // head-major source (order barely matters:
+                                                        // profiles/r01_row_sweep.jsonl)
         const uint32_t total = 2 * per_kv;
         for (uint32_t base = threadIdx.x; base < total; base += kMoveThreads * kU) {
             uint4 v[kU];

@@ -338,14 +338,9 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                                 (uint64_t)t->n_local_layers);
         KVX_CUDA(cudaEventRecord(ev.first, t->stream));
         if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
-            static const int order_by_dst = getenv("KVX_ROW_ORDER_DST") ? atoi(getenv("KVX_ROW_ORDER_DST")) : 0;
-            static const int row_cps = getenv("KVX_ROW_CTAS_PER_SM") ? atoi(getenv("KVX_ROW_CTAS_PER_SM")) : 0;
-            const unsigned grid_r = row_cps > 0 ? (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)t->num_sms * row_cps))
-                                                : grid;
-            kvx::kvx_move_any_kernel<<<grid_r, kvx::kMoveThreads, 0, t->stream>>>(
+            kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
-                (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0,
-                order_by_dst);
+                (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0);
         } else if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
             const uint64_t run_bytes = nseg > 0 ? (uint64_t)tokens * 2ull * token_bytes(t->g) / (uint64_t)nseg : 0;
             const int vi = t->bulk_variant >= 0 ? t->bulk_variant : (run_bytes >= 65536 ? 2 : 0);
