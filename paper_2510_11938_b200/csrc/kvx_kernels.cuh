@@ -327,21 +327,6 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     if (fence_system) __threadfence_system();  // peer (NVLink) stores visible before host sync
 }
 
-// Division by a runtime divisor as multiply-high + add + shift (round-up
-// method, exact for every 32-bit numerator and 1 <= d < 2^31): the row mover
-// decomposes a flat vector index per 16-byte vector, and plain 32-bit
-// division (~20 instructions) would throttle the integer pipe.
-struct FastDiv {
-    uint32_t d, m, l;
-    __device__ __forceinline__ explicit FastDiv(uint32_t div) : d(div), l(0) {
-        while ((1u << l) < d) ++l;
-        m = (uint32_t)(((((uint64_t)1 << l) - d) << 32) / d + 1);
-    }
-    __device__ __forceinline__ uint32_t div(uint32_t n) const {
-        return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> l);
-    }
-};
-
 // --------------------------------------------- row-granular mover
 // Copies (K|V, token, head) rows of head_bytes, addressed through both
 // pools' strides -- any layout pair.  Used for moves between token-major
@@ -374,7 +359,6 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
         const bool tok_inner = lp.src_ts < lp.src_hs;  // head-major source (order barely matters:
                                                         // profiles/r01_row_sweep.jsonl)
         const uint32_t total = 2 * per_kv;
-        const FastDiv by_kv(per_kv), by_vec(vph), by_inner(tok_inner ? ntok : H);
         for (uint32_t base = threadIdx.x; base < total; base += kMoveThreads * kU) {
             uint4 v[kU];
             uint4* dp[kU];
@@ -383,11 +367,12 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
                 const uint32_t i = base + (uint32_t)k * kMoveThreads;
                 dp[k] = nullptr;
                 if (i < total) {
-                    const uint32_t kv = by_kv.div(i), r = i - kv * per_kv;
-                    const uint32_t row = by_vec.div(r), w = r - row * vph;
-                    const uint32_t q = by_inner.div(row), rem = row - q * by_inner.d;
-                    const uint32_t h = tok_inner ? q : rem;
-                    const uint32_t t = (uint32_t)sg.t0 + (tok_inner ? rem : q);
+                    // plain division: a multiply-shift variant measured slower on the
+                    // same box (its per-unit set-up dominates short tails)
+                    const uint32_t kv = i / per_kv, r = i - kv * per_kv;
+                    const uint32_t w = r % vph, row = r / vph;
+                    const uint32_t h = tok_inner ? row / ntok : row % H;
+                    const uint32_t t = (uint32_t)sg.t0 + (tok_inner ? row % ntok : row / H);
                     v[k] = ld_stream(reinterpret_cast<const uint4*>(sb + kv * lp.src_kv + t * lp.src_ts +
                                                                     h * lp.src_hs) + w);
                     dp[k] = reinterpret_cast<uint4*>(db + kv * lp.dst_kv + t * lp.dst_ts + h * lp.dst_hs) + w;
