@@ -355,7 +355,8 @@ def run_reference(args):
     plan = Plan(args.config)
     threads = os.cpu_count() or 1
     steps = args.steps
-    gbs, desc, step_bytes = cpu_sample_run(plan, steps, max(1, args.warmup), threads)
+    gbs, desc, step_bytes = cpu_sample_run(plan, steps, max(1, args.warmup), threads,
+                                           target_bytes=args.sample_gb * 1e9)
     ms = step_bytes / (gbs * 1e9) * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
@@ -488,6 +489,8 @@ def main():
                          "(shard.move_plan); push = the source GPU; pull = the destination GPU")
     ap.add_argument("--pull", action="store_true", help="alias of --move pull")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--sample-gb", type=float, default=2.0,
+                    help="KV bytes per step of the CPU samples (--impl reference, cpu_baseline)")
     ap.add_argument("--layouts", default="blocks,blocks",
                     help="old,new pool layouts: blocks (FlashInfer NHD [blocks][2][B][H][D]), planes "
                          "(FlashAttention [2][blocks][B][H][D]) or heads (FlashInfer HND [blocks][2][H][B][D], "
@@ -852,7 +855,7 @@ def main():
         line["not_a_measurement"] = "ranks share GPUs (KVX_BENCH_FOLD); functional check of the N-rank path"
     if n_gpus == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        gbs, desc, _ = cpu_sample_run(plan, None, 1, threads, seconds=8.0)
+        gbs, desc, _ = cpu_sample_run(plan, None, 1, threads, target_bytes=args.sample_gb * 1e9, seconds=8.0)
         gbs1, desc1, _ = cpu_sample_run(plan, None, 1, 1, target_bytes=0.5e9, seconds=3.0)
         line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                                 "sample": desc, "value_1_thread": round(gbs1, 3), "sample_1_thread": desc1,
