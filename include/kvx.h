@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define KVX_ABI_VERSION 2  /* 2: kvx_transition_desc.layer_pull */
+#define KVX_ABI_VERSION 3  /* 2: kvx_transition_desc.layer_pull; 3: .max_ctas */
 
 #define KVX_OK 0
 #define KVX_EINVAL (-1)  /* bad argument (null, out of range, unsorted wave) */
@@ -210,6 +210,9 @@ typedef struct kvx_transition_desc {
                                      (DESIGN.md 4); shard.py derives it from the placement.
                                      Layers whose old and new pools are both local always move
                                      here.  NULL = `pull` for every layer. */
+    int32_t max_ctas;             /* optional cap on the mover's CTAs per wave (0 = the tuned grid):
+                                     waves 0 / delta overlap serving, and fewer CTAs leave serving
+                                     more HBM bandwidth */
 } kvx_transition_desc;
 
 typedef struct kvx_transition kvx_transition;

@@ -248,6 +248,7 @@ struct kvx_transition {
     bool transpose = false;     // some layer pairs a token-major with a head-major pool
     bool head_tails = false;    // head-major to head-major layers (H > 1): partial blocks go to the row mover
     cudaStream_t side = nullptr;  // ... launched on this side stream beside the bulk mover
+    int32_t max_ctas = 0;         // cap on mover CTAs per wave (0 = tuned grid)
     cudaEvent_t ev_join = nullptr;
     bool has_peer_dst = false;
     // wave staging: pinned host ring of 2 + device buffer

@@ -43,6 +43,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     if (!plan_ok(d->new_plan, g.num_layers, &why, &nb)) return fail(KVX_EINVAL, "new plan: " + why);
     if (d->max_requests < 1 || d->max_blocks < 1 || d->dst_num_blocks < 1)
         return fail(KVX_EINVAL, "max_requests/max_blocks/dst_num_blocks must be >= 1");
+    if (d->max_ctas < 0) return fail(KVX_EINVAL, "max_ctas must be >= 0");
     if (!d->src_block_table) return fail(KVX_EINVAL, "src_block_table is null");
     for (int k = 0; k < d->new_plan.num_stages; ++k) {
         const kvx_pool* p = d->new_plan.pools[k];
@@ -101,6 +102,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     t->max_blocks = d->max_blocks;
     t->dst_num_blocks = d->dst_num_blocks;
     t->bm = static_cast<kvx_blockmgr*>(d->dst_blockmgr);
+    t->max_ctas = d->max_ctas;
     t->epoch = d->epoch;
     t->synced_hi.assign((size_t)d->max_requests, 0);
     t->src_bt.assign(d->src_block_table, d->src_block_table + cells);
@@ -328,7 +330,8 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     if (t->bm && new_blocks > 0) KVX_CUDA(bm_order_after(t->bm, t->stream));
     if (t->n_local_layers > 0) {
         const int64_t units = nseg * t->n_local_layers;
-        const int64_t full = (int64_t)t->num_sms * t->move_ctas_per_sm;
+        int64_t full = (int64_t)t->num_sms * t->move_ctas_per_sm;
+        if (t->max_ctas > 0) full = std::min<int64_t>(full, t->max_ctas);  // sharing HBM with serving
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full));
         std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
         KVX_CUDA(kvx::Arena::of(t->device).event(&ev.first, true));
@@ -366,6 +369,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                 full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], local_grid + peer_ctas);
             if (const char* cap = getenv("KVX_BULK_GRID"))
                 full_b = std::max<int64_t>(1, std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], atoll(cap)));
+            if (t->max_ctas > 0) full_b = std::min<int64_t>(full_b, t->max_ctas);
             const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full_b));
             // programmatic dependent launch: the mover's launch overlaps the
             // plan kernel; it waits (griddepcontrol.wait) for its segments

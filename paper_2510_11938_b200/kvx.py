@@ -81,7 +81,8 @@ class _Desc(C.Structure):
                 ("dst_num_blocks", C.c_int32), ("src_block_table", C.POINTER(C.c_int32)),
                 ("epoch", C.c_uint64), ("max_sync_rounds", C.c_int32),
                 ("kv_bytes_per_token", C.c_double), ("stream", C.c_void_p),
-                ("dst_blockmgr", C.c_void_p), ("pull", C.c_int32), ("layer_pull", C.POINTER(C.c_uint8))]
+                ("dst_blockmgr", C.c_void_p), ("pull", C.c_int32), ("layer_pull", C.POINTER(C.c_uint8)),
+                ("max_ctas", C.c_int32)]
 
 
 class _CommitResult(C.Structure):
@@ -408,7 +409,7 @@ class Transition(_Handle):
                  src_block_table: np.ndarray, epoch: int = 1, max_sync_rounds: int = 8,
                  kv_bytes_per_token: float = 0.0, stream: int = 0,
                  dst_blockmgr: Optional["BlockManager"] = None, pull: bool = False,
-                 layer_pull: Optional[Sequence[int]] = None):
+                 layer_pull: Optional[Sequence[int]] = None, max_ctas: int = 0):
         self.geom = geom
         self.max_requests, self.max_blocks = max_requests, max_blocks
         self._ob = _i32(list(old_boundaries))
@@ -434,6 +435,7 @@ class Transition(_Handle):
         d.dst_blockmgr = dst_blockmgr.handle.value if dst_blockmgr is not None else None
         self._bm = dst_blockmgr
         d.pull = 1 if pull else 0
+        d.max_ctas = max_ctas
         if layer_pull is not None:   # per layer: 1 = destination pulls, 0 = source pushes
             self._layer_pull = np.ascontiguousarray(layer_pull, dtype=np.uint8)
             if self._layer_pull.shape != (geom.num_layers,):

@@ -78,6 +78,11 @@ def test_missing_new_pool_rejected_in_push_mode():
     assert b"new-stage pool" in L.kvx_last_error()
 
 
+def test_negative_max_ctas_rejected():
+    d, keep = desc(max_ctas=-1)
+    assert begin_rc(d) == kvx.KVX_EINVAL
+
+
 def test_error_message_is_thread_local_and_set():
     d, keep = desc(max_blocks=0)
     begin_rc(d)
