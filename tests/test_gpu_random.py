@@ -38,7 +38,7 @@ def one_case(seed):
 
 
 @pytest.mark.parametrize("seed", range(40))
-def test_random_transition_bit_exact(gpu_count, seed):
+def test_random_transition_bit_exact(gpu_count, seed, max_ctas=0):
     rng, L, heads, dim, elem, B, ob, nb, N, final, max_blocks, use_bm = one_case(seed)
     g, og = kvx.geometry(L, heads, dim, elem, B), O.geo(L, heads, dim, elem, B)
     src_bt, cap0 = W.fragmented_block_table(final, max_blocks, B, seed=seed, slack=float(rng.random()))
@@ -69,7 +69,8 @@ def test_random_transition_bit_exact(gpu_count, seed):
     dp = O.DataPlane(og, ob, nb, cap0, cap1, N, max_blocks, src_bt, bm=ref_bm)
     if len(live):
         dp.fill_source(seed, live, final[live])
-    tr = kvx.Transition(g, ob, old, nb, new, 0, N, max_blocks, cap1, src_bt, epoch=1, dst_blockmgr=bm)
+    tr = kvx.Transition(g, ob, old, nb, new, 0, N, max_blocks, cap1, src_bt, epoch=1, dst_blockmgr=bm,
+                        max_ctas=max_ctas)
     try:
         synced = np.zeros(N, np.int64)
         waves = int(rng.integers(1, 5))
@@ -110,3 +111,10 @@ def test_movers_agree_on_random_case(gpu_count, impl, monkeypatch):
     """Both movers (KVX_MOVE_IMPL, read at kvx_begin) produce the same bytes."""
     monkeypatch.setenv("KVX_MOVE_IMPL", impl)
     test_random_transition_bit_exact(gpu_count, 101)
+
+
+@pytest.mark.parametrize("max_ctas", [1, 3, 7])
+def test_capped_mover_grid_bit_exact(gpu_count, max_ctas):
+    """desc.max_ctas (sharing HBM with serving) only narrows the grid."""
+    for seed in (5, 17, 23):
+        test_random_transition_bit_exact(gpu_count, seed, max_ctas=max_ctas)
