@@ -343,3 +343,69 @@ def random_worker(rank, world, port, seed, out):
         out.put((rank, "ok", {"checked": checked, "pull": pull, "bm": use_bm}))
     except Exception:
         out.put((rank, "err", traceback.format_exc()))
+
+
+def mapping_worker(rank, world, port, out):
+    """shard.setup_rank_pools with a fake kvx over gloo: for every placement
+    and mover policy, every layer this rank moves (kvx_begin's selection) has
+    both of its pools here, local or mapped from the owning peer."""
+    try:
+        dist = _init(rank, world, port)
+        from paper_2510_11938_b200 import shard as S
+        from paper_2510_11938_b200 import workload as W
+
+        class FakePool:
+            def __init__(self, device, g, layers, blocks, layout=0, owner=None, stage=None):
+                self.device, self.layers, self.blocks, self.layout = device, layers, blocks, layout
+                self.imported, self.owner = owner is not None, owner if owner is not None else rank
+
+            def zero(self):
+                pass
+
+            def fill_pattern(self, *a):
+                pass
+
+            def export_ipc(self):
+                return bytes([rank]) * 64
+
+            @classmethod
+            def import_ipc(cls, device, h, g, layers, blocks, layout=0):
+                return cls(device, g, layers, blocks, layout, owner=h[0])
+
+        class FakeKvx:
+            Pool = FakePool
+
+        class G:
+            num_layers = 40
+
+        scn = W.load_golden("llama13b_8to4")
+        t = scn.transitions[0]
+        ob, nb, L = t.old_boundaries, t.new_boundaries, 40
+        checked = 0
+        for mode in ("affinity", "disjoint", "spread", "oneway"):
+            old_dev, new_dev = S.placement(L, ob, nb, world, mode)
+            for policy in ("push", "pull", "auto"):
+                lp = S.move_plan(L, ob, nb, old_dev, new_dev, policy)
+
+                def gather(obj):
+                    o = [None] * world
+                    dist.all_gather_object(o, obj)
+                    return o
+
+                old, new = S.setup_rank_pools(FakeKvx, G, ob, nb, old_dev, new_dev, rank, rank, 8, 8,
+                                              all_gather=gather, layer_pull=lp, new_layout=2)
+                for l in range(L):
+                    so, sn = S.stage_of(ob, l), S.stage_of(nb, l)
+                    s, d = old_dev[so], new_dev[sn]
+                    moves_here = (s == rank and d == rank) or (s != d and ((lp[l] and d == rank) or
+                                                                           (not lp[l] and s == rank)))
+                    if moves_here:
+                        assert old[so] is not None and new[sn] is not None, (mode, policy, l)
+                        assert old[so].owner == s and new[sn].owner == d
+                        assert new[sn].layout == 2          # peers map pools with their layout
+                        checked += 1
+        dist.barrier()
+        dist.destroy_process_group()
+        out.put((rank, "ok", {"checked": checked}))
+    except Exception:
+        out.put((rank, "err", traceback.format_exc()))

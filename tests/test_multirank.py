@@ -46,6 +46,14 @@ def test_ranks_shard_every_layer_once_cpu(world):
         assert old_dev == list(range(8)) and new_dev == [0, 2, 4, 6]   # half of each stage crosses NVLink
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_rank_pool_mapping_for_every_mover_policy_cpu(world):
+    """The real shard.setup_rank_pools across gloo ranks: every layer a rank
+    moves has both pools there (local or IPC-mapped from its owner)."""
+    res = _run(mgpu_worker.mapping_worker, world)
+    assert sum(r["checked"] for r in res.values()) == 4 * 3 * 40   # each layer moved once per case
+
+
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 @pytest.mark.parametrize("placement", ["affinity", "disjoint", "spread", "oneway"])
 @pytest.mark.parametrize("policy", ["auto", "push", "pull"])
