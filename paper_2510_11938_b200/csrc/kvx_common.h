@@ -246,7 +246,6 @@ struct kvx_transition {
     int32_t n_peer_layers = 0;  // layers [0, n_peer_layers) of d_layers cross NVLink (pushed or pulled)
     int32_t n_pull_layers = 0;  // of which pulled (read from a peer's old pool)
     bool transpose = false;     // some layer pairs a token-major with a head-major pool
-    bool trans_staged = true;   // ... and its full blocks go through kvx_transpose_kernel
     bool head_tails = false;    // head-major to head-major layers (H > 1): partial blocks go to the row mover
     cudaStream_t side = nullptr;  // ... launched on this side stream beside the bulk mover
     int32_t max_ctas = 0;         // cap on mover CTAs per wave (0 = tuned grid)

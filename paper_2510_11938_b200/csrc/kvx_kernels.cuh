@@ -350,10 +350,7 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
         const int32_t layer = (int32_t)(u / nseg);
         const Seg sg = segs[u - (int64_t)layer * nseg];
         const LayerPtr lp = layers[layer];
-        const bool full = sg.t0 == 0 && sg.t1 == block_tokens;
-        if (tails_only == 1 && (lp.nh <= 1 || full)) continue;           // head-major tails only
-        if (tails_only == 2 && full && ((lp.src_ts < lp.src_hs) != (lp.dst_ts < lp.dst_hs)))
-            continue;                                                     // kvx_transpose_kernel's
+        if (tails_only && (lp.nh <= 1 || (sg.t0 == 0 && sg.t1 == block_tokens))) continue;
         const char* sb = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
         char* db = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
         const uint32_t ntok = (uint32_t)(sg.t1 - sg.t0);
@@ -810,154 +807,6 @@ kvx_verify_kernel(PoolAddr pa, int32_t first_layer,
     }
     for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatches, bad);
-}
-
-// ------------------------------------------------------ block transposer
-// Full blocks of layers that pair a token-major pool with a head-major one.
-// One elected thread bulk-loads a contiguous chunk of the source block into
-// shared memory (tokens [t0, t0+n) x all heads from a token-major source, or
-// heads [h0, h0+n) x all tokens from a head-major one) through a 2-buffer
-// ring; all threads then write it in the destination's order, so every head
-// (or token) of the chunk becomes one contiguous run -- instead of the row
-// mover's scattered D*elem rows.  Partial blocks stay with the row mover.
-constexpr int kTransThreads = 512;
-constexpr uint32_t kTransChunk = 81920;  // bytes per staging buffer (2 buffers = 160 KiB)
-
-struct TransJob {
-    const char* src;   // contiguous source chunk
-    char* dst;         // destination block + K/V offset
-    uint64_t dst_ts, dst_hs;
-    uint32_t bytes;
-    uint32_t first;    // first token (token chunk) or first head (head chunk)
-    uint32_t count;    // tokens or heads in the chunk
-    int32_t heads_chunk;
-    int32_t valid;
-};
-
-struct TransIter {  // elected thread only: this CTA's chunk sequence
-    const Seg* segs;
-    const LayerPtr* layers;
-    int32_t nseg;
-    int64_t u, units, ustep;
-    int kv;
-    uint32_t c;
-    uint32_t H, hb, B;
-    __device__ bool transposing(const LayerPtr& lp) const {
-        return (lp.src_ts < lp.src_hs) != (lp.dst_ts < lp.dst_hs);
-    }
-    __device__ void next(TransJob* j) {
-        while (u < units) {
-            const int32_t layer = (int32_t)(u / nseg);
-            const Seg sg = segs[u - (int64_t)layer * nseg];
-            const LayerPtr lp = layers[layer];
-            if (!transposing(lp) || sg.t0 != 0 || sg.t1 != (int32_t)B) {  // not ours
-                u += ustep;
-                continue;
-            }
-            const bool src_hm = lp.src_ts < lp.src_hs;
-            // chunk = n tokens x all heads (token-major source) or n heads x all tokens
-            const uint32_t per = src_hm ? B * hb : H * hb, dim = src_hm ? H : B;
-            uint32_t n = kTransChunk / per;
-            n = n > dim ? dim : (n < 1 ? 1 : n);
-            const uint32_t nchunks = (dim + n - 1) / n;
-            if (c >= nchunks) {  // this half done: V half next, or the next unit
-                c = 0;
-                if (kv == 0) {
-                    kv = 1;
-                } else {
-                    kv = 0;
-                    u += ustep;
-                    continue;
-                }
-            }
-            const uint32_t first = c * n, cnt = first + n > dim ? dim - first : n;
-            const char* sb = lp.src + (uint64_t)sg.src_blk * lp.src_bs + (uint64_t)kv * lp.src_kv;
-            j->src = sb + (uint64_t)first * (src_hm ? lp.src_hs : lp.src_ts);
-            j->dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs + (uint64_t)kv * lp.dst_kv;
-            j->dst_ts = lp.dst_ts;
-            j->dst_hs = lp.dst_hs;
-            j->bytes = cnt * per;
-            j->first = first;
-            j->count = cnt;
-            j->heads_chunk = src_hm ? 1 : 0;
-            j->valid = 1;
-            ++c;
-            return;
-        }
-        j->valid = 0;
-    }
-};
-
-static __global__ void __launch_bounds__(kTransThreads)
-kvx_transpose_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
-                     int32_t nlayers, int32_t heads, uint32_t head_bytes, int32_t block_tokens,
-                     int32_t fence_system) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[2];
-    __shared__ TransJob jobs[2];
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint32_t H = (uint32_t)heads, hb = head_bytes, vph = hb >> 4, B = (uint32_t)block_tokens;
-    const uint32_t tb = H * hb;
-    TransIter it;
-    if (threadIdx.x == 0) {
-        it.segs = segs;
-        it.layers = layers;
-        it.nseg = nseg;
-        it.u = blockIdx.x;
-        it.units = (int64_t)nseg * nlayers;
-        it.ustep = gridDim.x;
-        it.kv = 0;
-        it.c = 0;
-        it.H = H;
-        it.hb = hb;
-        it.B = B;
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < 2; ++s) {
-            it.next(&jobs[s]);
-            if (jobs[s].valid) {
-                mbar_expect_tx(&bars[s], jobs[s].bytes);
-                bulk_g2s(smem + (size_t)s * kTransChunk, jobs[s].src, jobs[s].bytes, &bars[s]);
-            }
-        }
-    }
-    __syncthreads();
-    uint32_t phase[2] = {0, 0};
-    for (int i = 0;; ++i) {
-        const int s = i & 1;
-        if (!jobs[s].valid) break;
-        mbar_wait(&bars[s], phase[s]);
-        phase[s] ^= 1;
-        const TransJob j = jobs[s];
-        const unsigned char* buf = smem + (size_t)s * kTransChunk;
-        const uint32_t n = j.count;
-        const uint32_t total = (j.heads_chunk ? B : H) * n * vph;
-        for (uint32_t x = threadIdx.x; x < total; x += kTransThreads) {
-            const uint32_t w = x % vph, r = x / vph;
-            uint32_t so;
-            char* d;
-            if (!j.heads_chunk) {  // smem [n tokens][H][vph] -> dst per head: tokens contiguous
-                const uint32_t tl = r % n, h = r / n;
-                so = tl * tb + h * hb;
-                d = j.dst + (uint64_t)h * j.dst_hs + (uint64_t)(j.first + tl) * j.dst_ts;
-            } else {               // smem [n heads][B][vph] -> dst per token: heads contiguous
-                const uint32_t hl = r % n, t = r / n;
-                so = hl * B * hb + t * hb;
-                d = j.dst + (uint64_t)t * j.dst_ts + (uint64_t)(j.first + hl) * j.dst_hs;
-            }
-            st_stream(reinterpret_cast<uint4*>(d) + w, *reinterpret_cast<const uint4*>(buf + so + w * 16u));
-        }
-        __syncthreads();  // buffer s fully read; jobs[s] may be replaced
-        if (threadIdx.x == 0) {
-            it.next(&jobs[s]);
-            if (jobs[s].valid) {
-                mbar_expect_tx(&bars[s], jobs[s].bytes);
-                bulk_g2s(smem + (size_t)s * kTransChunk, jobs[s].src, jobs[s].bytes, &bars[s]);
-            }
-        }
-    }
-    if (fence_system) __threadfence_system();
 }
 
 }  // namespace kvx

@@ -25,9 +25,6 @@ cudaError_t preload_transition_kernels() {
         if ((e = cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       bv.stages * (int)bv.chunk)) != cudaSuccess)
             return e;
-    if ((e = cudaFuncSetAttribute(kvx::kvx_transpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  2 * (int)kvx::kTransChunk)) != cudaSuccess)
-        return e;
     return e;
 }
 }  // namespace kvx_host
@@ -220,12 +217,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         // run copies need both sides token-major or both head-major; otherwise the
         // wave goes through the transposing mover (kvx_move_any_kernel)
         const bool heads_runs = src->head_major() && dst->head_major();
-        if (src->head_major() != dst->head_major()) {
-            t->transpose = true;
-            // the block transposer stages a chunk of >= 1 token (or head) per buffer
-            const uint64_t unit = src->head_major() ? (uint64_t)g.block_tokens * src->head_bytes() : token_bytes(g);
-            if (unit > kvx::kTransChunk) t->trans_staged = false;
-        }
+        if (src->head_major() != dst->head_major()) t->transpose = true;
         if (heads_runs && g.num_kv_heads > 1) t->head_tails = true;
         layers.push_back({src->layer_base[(size_t)(l - stage_begin(ob, so))],
                           dst->layer_base[(size_t)(l - stage_begin(nb, sn))], src->blk_stride(), dst->blk_stride(),
@@ -252,12 +244,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
                             cudaMemcpyHostToDevice, t->stream) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "layer table upload"));
     }
-    {
-        const char* tp = getenv("KVX_TRANSPOSE");  // 0: the row mover alone (A/B)
-        if (tp && std::string(tp) == "0") t->trans_staged = false;
-        if (!t->transpose) t->trans_staged = false;
-    }
-    if (t->head_tails || t->trans_staged) {  // side stream for the row mover (see kvx_wave)
+    if (t->head_tails) {  // side stream for the head-major tail mover (see kvx_wave)
         if (cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking) != cudaSuccess ||
             A.event(&t->ev_join, false) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "side stream"));
@@ -353,24 +340,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         t->move_bytes.push_back(2ull * (uint64_t)tokens * 2ull * token_bytes(t->g) *
                                 (uint64_t)t->n_local_layers);
         KVX_CUDA(cudaEventRecord(ev.first, t->stream));
-        if (t->transpose && t->trans_staged) {
-            // token-major <-> head-major: full blocks through the staged block transposer,
-            // everything else (partial blocks, compatible layers) through the row mover on
-            // the side stream beside it
-            const unsigned grid_t = (unsigned)std::max<int64_t>(
-                1, std::min<int64_t>(units, t->max_ctas > 0 ? std::min<int64_t>(t->max_ctas, t->num_sms)
-                                                             : (int64_t)t->num_sms));
-            kvx::kvx_transpose_kernel<<<grid_t, kvx::kTransThreads, 2 * kvx::kTransChunk, t->stream>>>(
-                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
-                (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, t->has_peer_dst ? 1 : 0);
-            KVX_LAUNCHED();
-            KVX_CUDA(cudaStreamWaitEvent(t->side, t->h_wave_free[slot], 0));
-            kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->side>>>(
-                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
-                (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 2, t->has_peer_dst ? 1 : 0);
-            KVX_CUDA(cudaEventRecord(t->ev_join, t->side));
-            KVX_CUDA(cudaStreamWaitEvent(t->stream, t->ev_join, 0));
-        } else if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
+        if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
             kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                 (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0);
