@@ -1,0 +1,870 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native inflight-refactor KV transition.
+
+One "step" = one complete inflight refactor of the BASELINE config-3 workload
+(Llama-2-13B shape, 8->4 stage merge, ~17 GB live paged KV), driven by the
+reference engine's OWN wave plan for it (tests/golden/llama13b_8to4.jsonl,
+extracted from the unmodified reference): wave 0 over every live token, the
+barrier / drain decision, the final post-barrier wave, commit (Eq. 10 check +
+block-table compaction).  All through the kvx C-ABI (include/kvx.h).
+
+  value     KV-refactor GB/s = reference-accounted KV bytes of the step
+            (kv_synced_bytes, engine.cpp:644-684) / device time per step,
+            KV resident in HBM (CUDA events on the transition stream).
+  e2e       same metric through the public API with the control inputs in
+            host memory: kvx_begin (grant + source block table H2D), the wave
+            descriptors H2D, the commit result (violations + compacted block
+            table + free list) D2H, host wall clock.
+  stall_ms  barrier -> commit done (final wave + commit), engine.cpp:676-686.
+  roofline  dominant kernel = the TMA bulk mover (kvx_bulk_kernel) of wave 0:
+            algorithmic read+write bytes / its CUDA-event duration vs
+            MEASURED_PEAKS hbm_gbs (N>1: vs the HBM / NVLink bound of the
+            busiest GPU); traffic from the committed ncu capture.
+
+`--impl reference` times the reference's CPU path for the same metric: the
+oracle restatement (oracle/kvx_oracle.c, all host threads) on a bounded
+sample, since the reference itself moves no bytes.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; N>1 via
+torch.distributed.run (one rank per GPU, NVLink P2P through CUDA IPC pools).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2510_11938_b200 import shard as S  # noqa: E402
+from paper_2510_11938_b200 import workload as W  # noqa: E402
+
+CONFIGS = {
+    # name: (golden, shape, description)
+    "c3": ("llama13b_8to4", "llama2-13b",
+           "Llama-2-13B shape (40 layers, 40 KV heads, d=128, fp16), 8->4 stage merge, "
+           "256 live requests, ~17 GB paged KV (16-token blocks)"),
+    "c1": ("llama7b_4to2", "llama2-7b",
+           "Llama-2-7B shape (32 layers, 32 KV heads), 4->2 merge, 16 requests, ~4k tokens"),
+    "c2": ("llama7b_2to8", "llama2-7b",
+           "Llama-2-7B shape, 2->8 split, 1024 live requests"),
+    "c4": ("llama70b_8to2to8", "llama2-70b",
+           "Llama-2-70B GQA shape (80 layers, 8 KV heads), 8->2 and 2->8"),
+    "c4r": ("llama70b_8to2to8", "llama2-70b",
+            "Llama-2-70B GQA shape (80 layers, 8 KV heads), same-K re-placement of all 8 stages "
+            "(10 layers each), ~64k live tokens = 21 GB; wave plan of the reference's 2->8 transition"),
+}
+SEED = 0xB200
+METRIC = "KV-refactor GB/s (% of HBM/NVLink roofline); refactor stall ms at 1/2/4/8 B200"
+
+
+def ncu_traffic(cfg: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the wave-0 mover launch
+    from the newest committed ncu capture of this config (scripts/run_ncu.sh
+    -> profiles/*_traffic_<cfg>.csv), or None."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*bulk_traffic_{cfg}.csv")))
+    if not files:
+        return None, None
+    total = 0.0
+    with open(files[-1]) as f:
+        for row in csv.reader(f):
+            if len(row) > 14 and row[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                total += float(row[14].replace(",", ""))
+    return (total or None), os.path.relpath(files[-1], ROOT)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------- clocks
+class ClockSampler:
+    """SM clock + throttle reasons sampled in-process through NVML (one call
+    per 20 ms from a thread) while the timed region runs."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int, period_s: float = 0.02):
+        self.index, self.period = index, period_s
+        self.rows = []
+        self.err = None
+        self._stop = threading.Event()
+        self._thr = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # NVML absent
+            self.err = f"nvml: {e}"
+            return
+        self._thr = threading.Thread(target=self._run, daemon=True)
+        self._thr.start()
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.rows.append((time.time(), sm, rs))
+            except Exception as e:
+                self.err = str(e)
+                return
+            self._stop.wait(self.period)
+
+    def stop(self):
+        self._stop.set()
+        if self._thr:
+            self._thr.join(timeout=2)
+
+    def summary(self, t0: float, t1: float):
+        sel = [r for r in self.rows if t0 - 0.025 <= r[0] <= t1 + 0.025] or self.rows[-3:]
+        if not sel:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": self.err or "no samples"}
+        reasons = set()
+        for _, _, rs in sel:
+            for bit, name in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r[1] for r in sel), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sel), "source": "nvml"}
+
+
+# ------------------------------------------------------------------ workload
+class Plan:
+    """The golden transition and everything derived from it."""
+
+    def __init__(self, cfg: str):
+        golden, shape, self.desc = CONFIGS[cfg]
+        self.golden = golden
+        self.scn = W.load_golden(golden)
+        self.t = [t for t in self.scn.transitions if t.outcome == "commit"][-1] if cfg in ("c4", "c4r") \
+            else self.scn.transitions[0]
+        if cfg == "c4r":
+            # BASELINE C4: same-K re-placement.  The reference drops same-plan
+            # directives (engine.cpp:562) -- parity unpinned; its last wave
+            # plan is reused with the old 8-stage cut on both sides.
+            import copy
+            self.t = copy.copy(self.t)
+            self.t.old_boundaries = list(self.t.new_boundaries)
+        self.L, self.H, self.D = W.SHAPES[shape]
+        self.N = self.scn.num_requests
+        self.tokens = self.t.max_tokens(self.N)
+        self.max_blocks = int(max(1, (self.tokens.max() + 15) // 16))
+        self.src_bt, self.old_blocks = W.fragmented_block_table(self.tokens, self.max_blocks, 16, seed=7)
+        self.dst_blocks = int(((self.tokens + 15) // 16).sum())
+        self.live = np.nonzero(self.tokens)[0].astype(np.int32)
+        self.token_bytes = self.H * self.D * 2
+        self.kv_bytes_per_token = self.scn.kv_bytes_per_token
+        self.step_tokens = sum(int((w.hi - w.lo).clip(min=0).sum()) for w in self.t.waves)
+        self.step_bytes = self.step_tokens * self.kv_bytes_per_token  # reference-accounted
+        w0 = self.t.waves[0]
+        self.wave0_tokens = int((w0.hi - w0.lo).clip(min=0).sum())
+
+
+def run_step(tr, t, stall_ev=None, wait=True):
+    """One transition through the reference-shaped handlers, in the order the
+    reference engine issued them (engine.cpp:637-713).  stall_ev = (start,
+    end, stream): start is recorded right before the call that issues the
+    final post-barrier wave, end after commit -- the B200 refactor stall."""
+    from paper_2510_11938_b200 import kvx
+    ev = list(t.events)
+    w0 = ev.pop(0)
+    tr.begin_refactor((w0.req, w0.hi))
+    while ev:
+        e = ev.pop(0)
+        if isinstance(e, W.Barrier):
+            if e.inflight_batches > 0:
+                act, _ = tr.on_kv_sync_complete((e.req, e.kv), e.inflight_batches)
+                assert act == kvx.ACT_BARRIER_WAIT, act
+                continue
+            if stall_ev is not None:
+                stall_ev[0].record(stall_ev[2])
+            act, _ = tr.on_kv_sync_complete((e.req, e.kv), 0)
+            assert act == kvx.ACT_FINAL, act
+            ev.pop(0)  # the final wave this handler just issued
+        elif e.final:
+            if stall_ev is not None:
+                stall_ev[0].record(stall_ev[2])
+            act, _ = tr.on_kv_sync_complete((e.req, e.hi), 0)
+            assert act == kvx.ACT_FINAL, act
+        else:
+            act, _ = tr.on_kv_sync_complete((e.req, e.hi), 1)
+            assert act == kvx.ACT_DELTA, act
+    res = tr.on_refactor_commit((t.live_req, t.live_kv), wait=wait)
+    if stall_ev is not None:
+        stall_ev[1].record(stall_ev[2])  # device time at which the commit result is on the host
+    return res
+
+
+# ------------------------------------------------------------ NCCL baseline
+def nccl_baseline(kvx, torch, dist, plan, g, old_pools, old_dev, new_dev, rank, world, dev, stream,
+                  reps=5):
+    """Wave 0 the library-call way: gather every local-source layer into a
+    local copy of the destination layout (the same kvx mover, local HBM
+    only), then ship each remote layer region with NCCL send/recv (grouped,
+    batch_isend_irecv) straight into the owner's pool.  Returns device ms
+    (gather, nccl, total), max over ranks, or None if nothing crosses GPUs."""
+    t, L = plan.t, plan.L
+    ob, nb = t.old_boundaries, t.new_boundaries
+    cross = [l for l in range(L) if old_dev[S.stage_of(ob, l)] != new_dev[S.stage_of(nb, l)]]
+    if not cross:
+        return None
+    bb = g.block_bytes
+    ranges = W.stage_ranges(L, nb)
+    bufs, pools = [], []
+    for j, (b, e) in enumerate(ranges):
+        n = (e - b) * plan.dst_blocks * bb
+        buf = torch.empty(n, dtype=torch.uint8, device=dev)
+        bufs.append(buf)
+        pools.append(kvx.Pool.wrap(dev, buf.data_ptr(), n, g, e - b, plan.dst_blocks))
+    w0 = t.waves[0]
+    alloc0 = int(((w0.hi + 15) // 16).sum())  # fresh pools: wave 0 fills blocks [0, alloc0) per layer
+    ops_spec = []
+    for l in cross:
+        src, dst = old_dev[S.stage_of(ob, l)], new_dev[S.stage_of(nb, l)]
+        j = S.stage_of(nb, l)
+        off = (l - ranges[j][0]) * plan.dst_blocks * bb
+        if rank == src:
+            ops_spec.append(("send", j, off, dst))
+        elif rank == dst:
+            ops_spec.append(("recv", j, off, src))
+    sp = stream.cuda_stream
+    res = []
+    for rep in range(reps + 1):
+        tr = kvx.Transition(g, ob, old_pools, nb, pools, dev, plan.N, plan.max_blocks, plan.dst_blocks,
+                            plan.src_bt, epoch=t.epoch, stream=sp)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            tr.wave(w0.req, w0.lo, w0.hi)
+            e1.record(stream)
+            ops = [dist.P2POp(dist.isend if k == "send" else dist.irecv,
+                              bufs[j][off:off + alloc0 * bb], peer) for k, j, off, peer in ops_spec]
+            for r in dist.batch_isend_irecv(ops) if ops else []:
+                r.wait()
+            e2.record(stream)
+        torch.cuda.synchronize(dev)
+        tr.close()
+        if rep:
+            res.append((e0.elapsed_time(e1), e1.elapsed_time(e2), e0.elapsed_time(e2)))
+    med = [statistics.median(x[i] for x in res) for i in range(3)]
+    tm = torch.tensor(med, dtype=torch.float64, device=dev)
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    for p in pools:
+        p.close()
+    del bufs
+    return [float(x) for x in tm.tolist()]
+
+
+# -------------------------------------------------------------- CPU baseline
+def cpu_sample_run(plan: Plan, steps, warmup: int, threads: int, target_bytes: float = 2.0e9,
+                   seconds: float = 8.0):
+    """The oracle executor (oracle/kvx_oracle.c, pthreads) on a bounded sample
+    of the same transition: the first requests whose KV totals ~target_bytes.
+    steps=None: as many steps as fill ~`seconds` of CPU work (at least 2),
+    sized from the warm-up step.  Returns (GB/s, sample description, bytes
+    per step)."""
+    from oracle import pyoracle as O
+    per_req = plan.tokens * plan.kv_bytes_per_token
+    order = plan.live
+    csum = np.cumsum(per_req[order])
+    nsel = int(np.searchsorted(csum, target_bytes) + 1)
+    sel = np.sort(order[:max(1, nsel)])
+    tokens = np.zeros_like(plan.tokens)
+    tokens[sel] = plan.tokens[sel]
+    src_bt, old_blocks = W.fragmented_block_table(tokens, plan.max_blocks, 16, seed=7)
+    dst_blocks = int(((tokens + 15) // 16).sum())
+    g = O.geo(plan.L, plan.H, plan.D)
+    t = plan.t
+    waves = []
+    for w in t.waves:
+        m = np.isin(w.req, sel)
+        waves.append((w.req[m], w.lo[m], w.hi[m]))
+    step_bytes = sum(int((hi - lo).clip(min=0).sum()) for _, lo, hi in waves) * plan.kv_bytes_per_token
+    dp = O.DataPlane(g, t.old_boundaries, t.new_boundaries, old_blocks, dst_blocks, plan.N,
+                     plan.max_blocks, src_bt)
+    for p in dp.old_pools:  # touch every page (a real KV cache is resident)
+        p.fill(0x5A)
+    for p in dp.new_pools:
+        p[:] = 0
+    live_m = np.isin(t.live_req, sel)
+
+    def one_step():
+        dp.bt[:] = -1
+        dp.synced_hi[:] = 0
+        dp.d.next_block = 0
+        t0 = time.perf_counter()
+        for req, lo, hi in waves:
+            assert dp.wave(req, lo, hi, threads=threads) == 0
+        dp.commit(t.live_req[live_m], t.live_kv[live_m])
+        return time.perf_counter() - t0
+
+    warm = [one_step() for _ in range(max(1, warmup))]
+    if steps is None:
+        steps = int(min(500, max(2, round(seconds / max(1e-6, min(warm))))))
+    times = [one_step() for _ in range(steps)]
+    gbs = step_bytes * len(times) / sum(times) / 1e9
+    desc = (f"{len(sel)} of {len(plan.live)} live requests of {plan.golden} "
+            f"({step_bytes / 1e9:.2f} GB of KV per step, real geometry), same wave plan, "
+            f"oracle run-granular memcpy on {threads} threads, {len(times)} steps")
+    return gbs, desc, step_bytes
+
+
+def reference_control_plane(golden: str):
+    """The reference's OWN transition handlers (oracle/_ref/extract_waves, the
+    unmodified reference library) timed on this host for the same scenario:
+    refactor_begin / kv_sync_complete / refactor_commit wall us (median).  The
+    reference moves no bytes, so this is its whole CPU path for the
+    transition; None when the prebuilt binary is absent."""
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "extract_waves")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe, "--time", golden, "5"], capture_output=True, text=True, timeout=120)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # report, never fail the bench on it
+        return {"error": str(e)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    plan = Plan(args.config)
+    threads = os.cpu_count() or 1
+    steps = args.steps
+    gbs, desc, step_bytes = cpu_sample_run(plan, steps, max(1, args.warmup), threads,
+                                           target_bytes=args.sample_gb * 1e9)
+    ms = step_bytes / (gbs * 1e9) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16 (u16 words)",
+        "data": "synthetic", "config": {"workload": plan.desc, "golden_wave_plan": plan.golden},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": desc,
+                         "reference_control_plane": reference_control_plane(plan.golden)},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (pipesim) is a simulator that moves no bytes; its CPU path for this "
+                "metric is the oracle restatement executing the identical byte plan",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------- repeated refactors (C5)
+def run_chain(args):
+    """BASELINE config 5: the reference's bursty, mixed-length trace
+    (tests/golden/bursty_repeated.jsonl: gamma arrivals CV=4) drives two
+    consecutive inflight refactors, 8->4 then 4->8, at the Llama-2-13B shape.
+    The second reads the first one's destination pools through its block
+    table; destination blocks come from device block managers; the serving
+    pipeline's decode appends between the two are emulated (untimed).  One
+    step = both transitions; value = their reference-accounted KV bytes / the
+    transitions' device time."""
+    import torch
+    from paper_2510_11938_b200 import kvx
+    dev = 0
+    torch.cuda.set_device(dev)
+    scn = W.load_golden("bursty_repeated")
+    t1, t2 = [t for t in scn.transitions if t.outcome == "commit"][:2]
+    N = scn.num_requests
+    L, H, D = W.SHAPES["llama2-13b"]
+    g = kvx.geometry(L, H, D)
+    tok1, tok2 = t1.max_tokens(N), t2.max_tokens(N)
+    max_blocks = int((max(tok1.max(), tok2.max()) + 15) // 16)
+    need2 = int(((tok2 + 15) // 16).sum())
+    src_bt1, capA = W.fragmented_block_table(tok1, max_blocks, 16, seed=7)
+    capA = max(capA, need2 + 16)
+    capB = int(((np.maximum(tok1, tok2) + 15) // 16).sum()) + 16
+    live1 = np.nonzero(tok1)[0].astype(np.int32)
+    poolsA = [kvx.Pool(dev, g, e - b, capA) for b, e in W.stage_ranges(L, t1.old_boundaries)]
+    poolsB = [kvx.Pool(dev, g, e - b, capB) for b, e in W.stage_ranges(L, t1.new_boundaries)]
+    bmA, bmB = kvx.BlockManager(dev, capA), kvx.BlockManager(dev, capB)
+    stream = torch.cuda.Stream(device=dev)
+    sp = stream.cuda_stream
+    bytes1 = sum(int((w.hi - w.lo).clip(min=0).sum()) for w in t1.waves) * scn.kv_bytes_per_token
+    bytes2 = sum(int((w.hi - w.lo).clip(min=0).sum()) for w in t2.waves) * scn.kv_bytes_per_token
+    times, stalls, bad = [], [], 0
+    for s in range(args.warmup + args.steps):
+        for k, (b, e) in enumerate(W.stage_ranges(L, t1.old_boundaries)):
+            poolsA[k].fill_pattern(SEED, b, live1, tok1[live1], src_bt1)
+        bmA.reset()
+        bmB.reset()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        st1 = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), stream)
+        st2 = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), stream)
+        tr1 = kvx.Transition(g, t1.old_boundaries, poolsA, t1.new_boundaries, poolsB, dev, N, max_blocks, capB,
+                             src_bt1, epoch=t1.epoch, max_sync_rounds=scn.max_sync_rounds,
+                             kv_bytes_per_token=scn.kv_bytes_per_token, stream=sp, dst_blockmgr=bmB)
+        torch.cuda.synchronize(dev)
+        ev[0].record(stream)
+        run_step(tr1, t1, st1)
+        ev[1].record(stream)
+        torch.cuda.synchronize(dev)
+        table = tr1.dst_block_table()
+        tr1.close()
+        # serving between the refactors: decode appends into the 4-stage pools
+        grown = W.serving_append(bmB.pop, table, t1.live_kv_map(N), tok2)
+        if len(grown):
+            for k, (b, e) in enumerate(W.stage_ranges(L, t1.new_boundaries)):
+                poolsB[k].fill_pattern(SEED, b, grown, tok2[grown], table)
+        tr2 = kvx.Transition(g, t2.old_boundaries, poolsB, t2.new_boundaries, poolsA, dev, N, max_blocks, capA,
+                             table, epoch=t2.epoch, max_sync_rounds=scn.max_sync_rounds,
+                             kv_bytes_per_token=scn.kv_bytes_per_token, stream=sp, dst_blockmgr=bmA)
+        torch.cuda.synchronize(dev)
+        ev[2].record(stream)
+        run_step(tr2, t2, st2)
+        ev[3].record(stream)
+        torch.cuda.synchronize(dev)
+        if s == args.warmup + args.steps - 1:
+            bad = tr2.verify_pattern(SEED, t2.live_req, t2.live_kv)
+        tr2.close()
+        if s >= args.warmup:
+            times.append((ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])))
+            stalls.append((st1[0].elapsed_time(st1[1]), st2[0].elapsed_time(st2[1])))
+    if bad:
+        raise SystemExit(f"bench c5: final KV differs from the payload ({bad} words)")
+    ms1 = statistics.median(x[0] for x in times)
+    ms2 = statistics.median(x[1] for x in times)
+    value = (bytes1 + bytes2) / ((ms1 + ms2) * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms1 + ms2, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp16 (u16 words)", "data": "synthetic",
+        "config": {"workload": "BASELINE C5: bursty gamma trace (CV=4), mixed lengths, repeated inflight "
+                               "refactors 8->4->8 at the Llama-2-13B shape, chained through device block "
+                               "managers", "golden_wave_plan": "bursty_repeated",
+                   "transitions": [{"stages": f"{t1.old_stages}->{t1.new_stages}", "bytes": bytes1,
+                                    "ms": round(ms1, 4), "stall_ms": round(statistics.median(x[0] for x in stalls), 4)},
+                                   {"stages": f"{t2.old_stages}->{t2.new_stages}", "bytes": bytes2,
+                                    "ms": round(ms2, 4), "stall_ms": round(statistics.median(x[1] for x in stalls), 4)}]},
+        "verified_words_mismatched": int(bad),
+    }
+    print(json.dumps(line), flush=True)
+    for p in poolsA + poolsB:
+        p.close()
+    bmA.close()
+    bmB.close()
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="kvx", choices=["kvx", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS) + ["c5"])
+    ap.add_argument("--placement", default="affinity", choices=["affinity", "disjoint", "spread", "oneway"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-weights", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--move", default="auto", choices=["auto", "push", "pull"],
+                    help="who moves a cross-GPU layer: auto = pull on one-way traffic, push on two-way "
+                         "(shard.move_plan); push = the source GPU; pull = the destination GPU")
+    ap.add_argument("--pull", action="store_true", help="alias of --move pull")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--sample-gb", type=float, default=2.0,
+                    help="KV bytes per step of the CPU samples (--impl reference, cpu_baseline)")
+    ap.add_argument("--layouts", default="blocks,blocks",
+                    help="old,new pool layouts: blocks (FlashInfer NHD [blocks][2][B][H][D]), planes "
+                         "(FlashAttention [2][blocks][B][H][D]) or heads (FlashInfer HND [blocks][2][H][B][D], "
+                         "vLLM's FlashInfer layout on B200); unequal = the refactor converts")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.config == "c5":
+        return run_chain(args)
+    if args.warmup < 3:
+        args.warmup = 3
+
+    import torch
+    import torch.distributed as dist
+    from paper_2510_11938_b200 import kvx
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = world
+    # KVX_BENCH_FOLD=n (functional testing only): fold the ranks onto n
+    # physical GPUs, e.g. the N=8 placement on a 4-GPU box.  NCCL refuses two
+    # ranks on one GPU, so the host plumbing goes over gloo, the NCCL baseline
+    # is skipped and the line is marked as not a measurement.
+    fold = int(os.environ.get("KVX_BENCH_FOLD", "0"))
+    dev = (local % fold if fold else local) if world > 1 else 0
+    if fold:
+        args.no_nccl = True
+    if world > 1:
+        torch.cuda.set_device(dev)
+        if fold:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+
+    plan = Plan(args.config)
+    t = plan.t
+    L = plan.L
+    layouts = [{"blocks": kvx.LAYOUT_BLOCKS, "planes": kvx.LAYOUT_KV_PLANES, "heads": kvx.LAYOUT_HEADS}[x]
+               for x in args.layouts.split(",")]
+    g = kvx.geometry(L, plan.H, plan.D)
+    old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, n_gpus, args.placement)
+    if args.pull:
+        args.move = "pull"
+    layer_pull = S.move_plan(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev, args.move)
+
+    # ---- pools on this GPU; new-stage pools of peers mapped through CUDA IPC
+    def gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    old_pools, new_pools = S.setup_rank_pools(
+        kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, dev, plan.old_blocks,
+        plan.dst_blocks, all_gather=gather if world > 1 else None,
+        fill=(SEED, plan.live, plan.tokens[plan.live], plan.src_bt), layer_pull=layer_pull,
+        old_layout=layouts[0], new_layout=layouts[1])
+    if world > 1:
+        dist.barrier()
+
+    stream = torch.cuda.Stream(device=dev)
+    sp = stream.cuda_stream
+
+    def make():
+        return kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, dev,
+                              plan.N, plan.max_blocks, plan.dst_blocks, plan.src_bt, epoch=t.epoch,
+                              max_sync_rounds=plan.scn.max_sync_rounds,
+                              kv_bytes_per_token=plan.kv_bytes_per_token, stream=sp, layer_pull=layer_pull)
+
+    K, Wm = args.steps, args.warmup
+    trs = [make() for _ in range(Wm + K)]
+
+    # ---- warm-up
+    for s in range(Wm):
+        run_step(trs[s], t)
+    torch.cuda.synchronize(dev)
+
+    # ---- correctness gate on the warm-up output (device-side payload check);
+    #      peers push into our pools, so every rank must be done first
+    if world > 1:
+        dist.barrier()
+    bad = 0
+    if not args.no_verify:
+        bad = trs[Wm - 1].verify_pattern(SEED, t.live_req, t.live_kv)
+    if world > 1:
+        tb = torch.tensor([bad], dtype=torch.int64, device=dev)
+        dist.all_reduce(tb)
+        bad = int(tb.item())
+    if bad:
+        raise SystemExit(f"bench: destination KV differs from the source payload ({bad} words)")
+
+    # ---- timed region (device-resident KV): K steps
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.3)
+    stall_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), stream)
+                   for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = kvx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    ev0.record(stream)
+    for s in range(K):
+        # commit without a host sync: the next transition's waves queue right
+        # behind it; every result is collected (and checked) after the loop
+        run_step(trs[Wm + s], t, stall_pairs[s], wait=False)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    wall1 = time.time()
+    launches = kvx.launch_count() - launches0
+    for s in range(K):
+        res = trs[Wm + s].collect_commit()
+        if res.violations != t.violations:
+            raise SystemExit(f"bench: step {s} commit reported {res.violations} Eq. 10 violations")
+    if world > 1:
+        dist.barrier()
+    sampler.stop()
+    dev_ms = ev0.elapsed_time(ev1)
+    stalls = sorted(a.elapsed_time(b) for a, b, _ in stall_pairs)
+    stall_med = statistics.median(stalls)
+    # dominant kernel: wave-0 move of each timed step
+    mv = [trs[Wm + s].move_timings() for s in range(K)]
+    w0_ms = [m[0][0] for m in mv if m]
+    w0_bytes = mv[0][0][1] if mv and mv[0] else 0
+    w0_avg = sum(w0_ms) / len(w0_ms) if w0_ms else float("nan")
+    all_move_ms = sum(x[0] for m in mv for x in m)
+    n_waves = max((len(m) for m in mv), default=0)
+    wave_ms = [round(statistics.median(m[i][0] for m in mv if len(m) > i), 4) for i in range(n_waves)]
+
+    tm = torch.tensor([dev_ms, stall_med, float(launches), w0_avg, float(w0_bytes)], dtype=torch.float64,
+                      device=dev)
+    rank_ms = [round(dev_ms / K, 4)]
+    rank_w0 = [round(w0_avg, 4)]
+    if world > 1:
+        allv = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(world)]
+        dist.all_gather(allv, torch.tensor([dev_ms / K, w0_avg], dtype=torch.float64, device=dev))
+        rank_ms = [round(float(v[0]), 4) for v in allv]
+        rank_w0 = [round(float(v[1]), 4) for v in allv]
+        mx = tm.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tm.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_ms, stall_med, w0_avg = float(mx[0]), float(mx[1]), float(mx[3])
+        launches = int(sm[2])
+        w0_bytes_total = int(sm[4])
+    else:
+        w0_bytes_total = w0_bytes
+    for tr in trs:
+        tr.close()
+
+    # ---- e2e through the public API (host inputs, results back to host)
+    e2e_steps = args.e2e_steps or K
+    h2d = d2h = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = time.perf_counter()
+    for s in range(e2e_steps):
+        tr = make()  # grant: device state + source block table H2D
+        res = run_step(tr, t)
+        tr.close()
+        if s == 0:
+            n_entries = sum(len(w.req) for w in t.waves)
+            h2d = plan.src_bt.nbytes + n_entries * (4 + 8 + 8) + len(t.live_req) * (4 + 8)
+            d2h = 3 * 8 + res.row_ptr.nbytes + res.blocks.nbytes + res.free_list.nbytes
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - e0
+    if world > 1:
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+
+    # ---- drain-free stall: at the reference's barrier the
+    #      in-flight micro-batches are handed to their new owners (hidden x
+    #      fp16 rows) instead of drained, the final wave goes out at once over
+    #      the barrier's live set, then commit.  Device time barrier -> commit.
+    handoff = None
+    bar = next((e for e in t.events if isinstance(e, W.Barrier) and e.microbatches), None)
+    if bar is not None:
+        row = {"llama2-13b": 5120, "llama2-7b": 4096, "llama2-70b": 8192}[CONFIGS[args.config][1]] * 2
+        srcs = [torch.full((max(m.tokens, 1) * row,), m.batch % 251, dtype=torch.uint8, device=dev)
+                for m in bar.microbatches]
+        cap = sum(m.tokens * row + 256 for m in bar.microbatches) + 256
+        arenas = [torch.zeros(cap, dtype=torch.uint8, device=dev) for _ in range(len(t.new_boundaries) + 1)]
+        htimes, stimes = [], []
+        for rep in range(6):
+            tr = make()
+            tr.set_handoff(True)
+            wave0 = t.waves[0]
+            tr.begin_refactor((wave0.req, wave0.hi))
+            for e in t.events[1:]:  # delta waves before the barrier, as the reference ran them
+                if isinstance(e, W.Barrier):
+                    break
+                tr.on_kv_sync_complete((e.req, e.hi), 1)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a0.record(stream)
+            act, _ = tr.on_kv_sync_complete((bar.req, bar.kv), bar.inflight_batches)
+            assert act == kvx.ACT_FINAL, act
+            slots = tr.handoff(row, [(m.batch, m.after, m.tokens, s_.data_ptr())
+                                     for m, s_ in zip(bar.microbatches, srcs)],
+                               [x.data_ptr() for x in arenas], [cap] * len(arenas))
+            a1.record(stream)
+            res = tr.on_refactor_commit((bar.req, bar.kv))
+            a2.record(stream)
+            torch.cuda.synchronize(dev)
+            assert res.violations == 0
+            if rep > 0:
+                htimes.append(a0.elapsed_time(a1))
+                stimes.append(a0.elapsed_time(a2))
+            tr.close()
+        hbytes = sum(sl[4] for sl in slots)
+        hms, sms = statistics.median(htimes), statistics.median(stimes)
+        if world > 1:
+            tt = torch.tensor([hms, sms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            hms, sms = [float(x) for x in tt.tolist()]
+        handoff = {"batches": len(bar.microbatches), "bytes": int(hbytes),
+                   "final_wave_plus_handoff_ms": round(hms, 4), "stall_handoff_ms": round(sms, 4),
+                   "note": "drain-free mode: in-flight micro-batches of the reference's barrier moved "
+                           "to their new owners (hidden x fp16 rows), final wave over the barrier's "
+                           "live set, commit; device time barrier -> commit result on host"}
+
+    # ---- stage weight migration: the new stages' parameters
+    #      gathered by layer range on the device (N=1; fp16 weights of the shape)
+    weights = None
+    if world == 1 and not args.no_weights:
+        params = {"llama2-13b": 26.0e9, "llama2-7b": 13.5e9, "llama2-70b": 138.0e9}[CONFIGS[args.config][1]]
+        lb = int(params / L) // 4096 * 4096
+        if lb * L * 2 < 120e9:
+            wold = [torch.empty((e - b) * lb, dtype=torch.uint8, device=dev)
+                    for b, e in W.stage_ranges(L, t.old_boundaries)]
+            wnew = [torch.empty((e - b) * lb, dtype=torch.uint8, device=dev)
+                    for b, e in W.stage_ranges(L, t.new_boundaries)]
+            wt = []
+            for rep in range(4):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                kvx.weights_migrate(dev, L, lb, t.old_boundaries, [x.data_ptr() for x in wold],
+                                    t.new_boundaries, [x.data_ptr() for x in wnew], stream=sp)
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                if rep:
+                    wt.append(a.elapsed_time(b))
+            wms = statistics.median(wt)
+            wbytes = lb * L
+            weights = {"bytes": wbytes, "ms": round(wms, 3), "GB_s": round(wbytes / (wms * 1e-3) / 1e9, 1),
+                       "hbm_frac": round(2 * wbytes / (wms * 1e-3) / 1e9 / peaks()[0], 4),
+                       "reference_load_ms": plan.t.load_ready_ms - plan.t.t_ms,
+                       "note": "device-to-device layer-range gather of the new stages' weights; the "
+                               "reference models this as host/storage loads (load_ready_ms)"}
+            del wold, wnew
+
+    # ---- NCCL baseline of the cross-GPU path (N > 1, when bytes cross GPUs)
+    nccl = None
+    if world > 1 and not args.no_nccl:
+        nb_ms = nccl_baseline(kvx, torch, dist, plan, g, old_pools, old_dev, new_dev, rank, world, dev,
+                              stream)
+        if nb_ms is not None:
+            nccl = {"gather_ms": round(nb_ms[0], 4), "nccl_ms": round(nb_ms[1], 4),
+                    "total_ms": round(nb_ms[2], 4), "fused_p2p_ms": round(w0_avg, 4),
+                    "fused_speedup": round(nb_ms[2] / w0_avg, 3),
+                    "note": "wave 0: local gather into a copy of the destination layout + grouped "
+                            "NCCL send/recv of each remote layer region, vs the fused gather+push "
+                            "kernel over NVLink P2P (max over ranks)"}
+
+    # ---- the roofline denominator re-measured live on this GPU: the same
+    #      torch copy MEASURED_PEAKS.json uses (b.copy_(a), 1 Gi bf16, read+write)
+    copy_ref = None
+    if world == 1:
+        a_t = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+        b_t = torch.empty_like(a_t)
+        best = float("inf")
+        for _ in range(10):
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record()
+            b_t.copy_(a_t)
+            c1.record()
+            torch.cuda.synchronize(dev)
+            best = min(best, c0.elapsed_time(c1))
+        copy_ref = {"torch_copy_GBps": round(2 * a_t.numel() * 2 / (best * 1e-3) / 1e9, 1),
+                    "note": "b.copy_(a) over 1 Gi bf16 (read+write), best of 10, this run"}
+        del a_t, b_t
+
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = peaks()
+    layer_bytes = plan.wave0_tokens * 2 * plan.token_bytes  # K+V bytes per layer in wave 0
+    hbm, out, inn = S.link_bytes(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev, layer_bytes,
+                               n_gpus)
+    nvl_peak = 770.0  # measured peer copy GB/s per direction (B200_PROFILING.md)
+    t_roof = max(max(h / (peak * 1e9) for h in hbm), max(o / (nvl_peak * 1e9) for o in out),
+                 max(i / (nvl_peak * 1e9) for i in inn))
+    if n_gpus == 1:
+        achieved = w0_bytes / (w0_avg * 1e-3) / 1e9
+        traffic, traffic_src = ncu_traffic(args.config)
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "live_copy_reference": copy_ref,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": "kvx_bulk_kernel<3,64K> (wave 0, TMA bulk mover)", "bytes_per_launch": w0_bytes,
+                "launch_ms": round(w0_avg, 4), "peak_source": peak_kind}
+    else:
+        frac = t_roof * 1e3 / w0_avg
+        bound = "nvlink" if max(out + inn) / nvl_peak > max(hbm) / peak else "hbm"
+        roof = {"bound": bound, "achieved": round(frac * (peak if bound == "hbm" else nvl_peak), 1),
+                "peak": peak if bound == "hbm" else nvl_peak, "unit": "GB/s", "frac": round(frac, 4),
+                "traffic": None, "kernel": "kvx_bulk_kernel (wave 0, slowest rank)",
+                "t_roof_ms": round(t_roof * 1e3, 4), "launch_ms": round(w0_avg, 4),
+                "peak_source": f"hbm {peak_kind}; nvlink 770 GB/s measured peer copy"}
+
+    # ordered teardown: unmap peers' pools, then free our own
+    for p in old_pools + new_pools:
+        if p is not None and p.imported:
+            p.close()
+    if world > 1:
+        dist.barrier()
+    for p in old_pools + new_pools:
+        if p is not None and not p.imported:
+            p.close()
+    if world > 1:
+        dist.barrier()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    value = plan.step_bytes * K / (dev_ms * 1e-3) / 1e9
+    e2e_value = plan.step_bytes * e2e_steps / e2e_s / 1e9
+    clocks = sampler.summary(wall0, wall1)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": n_gpus, "steps": K,
+        "warmup": Wm, "ms_per_step": round(dev_ms / K, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp16 (u16 words)", "data": "synthetic",
+        "config": {"workload": plan.desc, "golden_wave_plan": plan.golden,
+                   "bytes_per_step": plan.step_bytes, "tokens_per_step": plan.step_tokens,
+                   "placement": {"mode": args.placement, "old_stage_gpu": old_dev, "new_stage_gpu": new_dev},
+                   "kv_layouts": args.layouts,
+                   "movers": {"policy": args.move, "pulled_layers": int(sum(layer_pull)),
+                              "cross_gpu_layers": sum(1 for l in range(L) if old_dev[S.stage_of(t.old_boundaries, l)]
+                                                      != new_dev[S.stage_of(t.new_boundaries, l)])},
+                   "l2": "inputs (17 GB) larger than L2 (126 MB); no flush needed"},
+        "stall_ms": round(stall_med, 4), "stall_ms_all": [round(x, 4) for x in (stalls[0], stalls[-1])],
+        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+                "ms_per_step": round(e2e_s * 1e3 / e2e_steps, 4)},
+        "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "handoff": handoff,
+        "weights": weights, "nccl_baseline": nccl,
+        "move_kernel_ms_per_step": round(all_move_ms / K, 4), "move_ms_by_wave": wave_ms,
+        "rank_ms_per_step": rank_ms, "rank_wave0_move_ms": rank_w0,
+        "mover": os.environ.get("KVX_MOVE_IMPL", "bulk") + ":" + os.environ.get("KVX_BULK_CFG", "auto"),
+    }
+    sim = plan.t.simulated_stall_ms()
+    line["stall_reference_simulated_ms"] = round(sim, 3) if sim is not None else None
+    if fold:
+        line["folded_onto_gpus"] = fold
+        line["not_a_measurement"] = "ranks share GPUs (KVX_BENCH_FOLD); functional check of the N-rank path"
+    if n_gpus == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        gbs, desc, _ = cpu_sample_run(plan, None, 1, threads, target_bytes=args.sample_gb * 1e9, seconds=8.0)
+        gbs1, desc1, _ = cpu_sample_run(plan, None, 1, 1, target_bytes=0.5e9, seconds=3.0)
+        line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                                "sample": desc, "value_1_thread": round(gbs1, 3), "sample_1_thread": desc1,
+                                "reference_control_plane": reference_control_plane(plan.golden)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -91,28 +91,10 @@ public:
         (timing ? ev_t_ : ev_n_).push_back(e);
     }
 
-    cudaError_t stream(cudaStream_t* s) {  // non-blocking streams, cached
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            if (!streams_.empty()) {
-                *s = streams_.back();
-                streams_.pop_back();
-                return cudaSuccess;
-            }
-        }
-        return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
-    }
-    void stream_free(cudaStream_t s) {  // the caller has drained it
-        if (!s) return;
-        std::lock_guard<std::mutex> lk(mu_);
-        streams_.push_back(s);
-    }
-
 private:
     std::mutex mu_;
     std::unordered_map<size_t, std::vector<void*>> dev_, host_;
     std::vector<cudaEvent_t> ev_t_, ev_n_;
-    std::vector<cudaStream_t> streams_;
 };
 
 }  // namespace kvx

@@ -247,9 +247,7 @@ struct kvx_transition {
     int32_t n_pull_layers = 0;  // of which pulled (read from a peer's old pool)
     bool transpose = false;     // some layer pairs a token-major with a head-major pool
     bool head_tails = false;    // head-major to head-major layers (H > 1): partial blocks go to the row mover
-    cudaStream_t side = nullptr;  // side stream (arena-cached): head-major tails, the commit kernel
-    cudaEvent_t ev_side_commit = nullptr;
-    int last_plan_slot = -1;      // h_wave_free[slot] recorded after the most recent plan kernel
+    cudaStream_t side = nullptr;  // ... launched on this side stream beside the bulk mover
     int32_t max_ctas = 0;         // cap on mover CTAs per wave (0 = tuned grid)
     cudaEvent_t ev_join = nullptr;
     bool has_peer_dst = false;

@@ -1,0 +1,812 @@
+// kvx_kernels.cuh -- sm_100a device code of the inflight-refactor KV transition.
+//
+// Kernels (launched on the transition's stream):
+//   kvx_plan_kernel      one CTA: destination block allocation (block-wide
+//                        exclusive scan of per-request new-block counts; bump
+//                        rule or pops off the block manager's free stack),
+//                        block-table rewrite, synced high-water marks, the
+//                        per-block copy segments of the wave, and a bounds
+//                        check of every segment.  Reads the wave entries
+//                        straight from mapped pinned memory.  Restates the
+//                        "which tokens move" half of engine.cpp:637-687.
+//   kvx_bulk_kernel      THE mover (default): persistent, one elected thread
+//                        per CTA streams (segment, layer) slabs global ->
+//                        shared -> global through a cp.async.bulk ring with
+//                        mbarrier tx counts (SASS UBLKCP / SYNCS); local HBM
+//                        or NVLink-peer destinations; optional CTA split
+//                        between peer and local layers.  Launched with PDL
+//                        behind the plan kernel (griddepcontrol.wait).
+//   kvx_move_kernel      LSU mover (16-byte ld.global.nc / st.global, 8 in
+//                        flight per thread); kvx_move256_kernel its 256-bit
+//                        variant.  KVX_MOVE_IMPL=lsu|lsu256.
+//   kvx_copy_list_kernel bulk engine over a (src, dst, bytes) list: activation
+//                        handoff and stage weight migration.
+//   kvx_commit_kernel    one CTA: Eq. 10 check per live request
+//                        (engine.cpp:707-713) with warp ballots, CSR
+//                        compaction of live rows, free list of rows no longer
+//                        live (scans); results written into mapped pinned
+//                        memory.
+//   kvx_bm_init_kernel   block-manager stack initialisation.
+//   kvx_fill_kernel / kvx_verify_kernel   synthetic payload (tests + bench).
+#pragma once
+// Included by several translation units: non-template kernels have internal
+// linkage (static), templates are instantiated where used.
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kvx {
+
+struct Seg {  // one logical block of one request inside one wave
+    int32_t src_blk;
+    int32_t dst_blk;
+    int32_t t0;  // first token inside the block
+    int32_t t1;  // one past the last token
+};
+
+struct LayerPtr {  // layer l in the old / new pool (address of block b, K|V k, token t, head h:
+                   //   base + b*bs + k*kv + t*ts + h*hs)
+    char* src;
+    char* dst;
+    uint64_t src_bs, dst_bs;  // bytes between consecutive blocks (layout-dependent)
+    uint64_t src_kv, dst_kv;  // bytes from a block's K rows to its V rows
+    uint64_t src_ts, dst_ts;  // token stride
+    uint64_t src_hs, dst_hs;  // head stride
+    uint32_t run_tok;         // run copies: bytes per token of one run (token_bytes or head bytes)
+    uint32_t nh;              // run copies: runs per K/V of a partial block (1 token-major, H head-major)
+};
+
+struct PoolAddr {  // one pool for the payload kernels: per-layer bases + strides
+    char* const* layer;  // device array, one base per layer
+    uint64_t blk_stride, kv_stride, tok_stride, head_stride;
+    uint32_t head_bytes;
+};
+
+// ---------------------------------------------------------------- payload
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t token_hash(uint64_t seed, int32_t req, int32_t layer,
+                                                        int32_t kv, int64_t tok) {
+    uint64_t h = mix64(seed ^ (uint64_t)(uint32_t)req);
+    h = mix64(h ^ (((uint64_t)(uint32_t)layer << 1) | (uint64_t)(kv & 1)));
+    return mix64(h ^ (uint64_t)tok);
+}
+__host__ __device__ __forceinline__ uint32_t word(uint64_t th, uint32_t w) {
+    return (uint32_t)(((th + (uint64_t)w * 0x9E3779B97F4A7C15ull) * 0xBF58476D1CE4E5B9ull) >> 48);
+}
+__device__ __forceinline__ uint4 pattern_vec(uint64_t th, uint32_t vec) {
+    const uint32_t w = vec * 8u;
+    uint4 v;
+    v.x = word(th, w + 0) | (word(th, w + 1) << 16);
+    v.y = word(th, w + 2) | (word(th, w + 3) << 16);
+    v.z = word(th, w + 4) | (word(th, w + 5) << 16);
+    v.w = word(th, w + 6) | (word(th, w + 7) << 16);
+    return v;
+}
+
+// ------------------------------------------------------------ scan helper
+// Block-wide exclusive scan of two int32 counters at once (1024 threads).
+template <int kThreads>
+__device__ __forceinline__ int2 block_exclusive_scan2(int2 v, int2* total) {
+    static_assert(kThreads % 32 == 0 && kThreads <= 1024, "threads");
+    __shared__ int2 warp_sums[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int2 inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int ax = __shfl_up_sync(0xffffffffu, inc.x, d);
+        const int ay = __shfl_up_sync(0xffffffffu, inc.y, d);
+        if (lane >= d) {
+            inc.x += ax;
+            inc.y += ay;
+        }
+    }
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int2 s = lane < kThreads / 32 ? warp_sums[lane] : make_int2(0, 0);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int ax = __shfl_up_sync(0xffffffffu, s.x, d);
+            const int ay = __shfl_up_sync(0xffffffffu, s.y, d);
+            if (lane >= d) {
+                s.x += ax;
+                s.y += ay;
+            }
+        }
+        warp_sums[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const int2 before = wid > 0 ? warp_sums[wid - 1] : make_int2(0, 0);
+    *total = warp_sums[kThreads / 32 - 1];
+    __syncthreads();  // warp_sums reused by the next call
+    return make_int2(before.x + inc.x - v.x, before.y + inc.y - v.y);
+}
+
+__device__ __forceinline__ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// -------------------------------------------------------------- planning
+constexpr int kPlanThreads = 1024;
+
+// Wave entries are strictly ascending request ids (validated on the host),
+// so rows never collide.  Destination rule: the new blocks of a request are
+// logical blocks [ceil(synced_hi/B), ceil(hi/B)); their ids are the bump
+// pointer plus the exclusive scan of the per-entry counts, in entry order.
+static __global__ void __launch_bounds__(kPlanThreads, 1)
+kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
+                const int64_t* __restrict__ hi, int32_t n, const int32_t* __restrict__ src_bt,
+                int32_t* __restrict__ dst_bt, int64_t* __restrict__ synced_hi, int32_t max_blocks,
+                int32_t block_tokens, int32_t alloc_base, const int32_t* __restrict__ pop_stack,
+                Seg* __restrict__ segs, int32_t src_cap, int32_t dst_cap, int32_t* __restrict__ err) {
+    const int64_t B = block_tokens;
+    int2 carry = make_int2(0, 0);
+    for (int32_t base = 0; base < n; base += kPlanThreads) {
+        const int32_t i = base + (int32_t)threadIdx.x;
+        int32_t r = -1;
+        int64_t l = 0, h = 0, s = 0;
+        int2 cnt = make_int2(0, 0);  // (new blocks, segments)
+        if (i < n) {
+            r = req[i];
+            l = lo[i];
+            h = hi[i];
+            s = synced_hi[r];
+            if (h > l) {
+                const int64_t have = cdiv(s, B), need = cdiv(h, B);
+                cnt.x = need > have ? (int32_t)(need - have) : 0;
+                cnt.y = (int32_t)(need - l / B);
+            }
+        }
+        int2 tot;
+        const int2 off = block_exclusive_scan2<kPlanThreads>(cnt, &tot);
+        if (i < n && h > l) {
+            int32_t* row = dst_bt + (int64_t)r * max_blocks;
+            const int32_t* srow = src_bt + (int64_t)r * max_blocks;
+            const int64_t have = cdiv(s, B);
+            // bump pointer, or pops off the block manager's free stack
+            // (alloc_base = its top): the j-th pop of the wave is stack[top-1-j]
+            for (int32_t k = 0; k < cnt.x; ++k) {
+                const int32_t j = carry.x + off.x + k;
+                row[have + k] = pop_stack ? pop_stack[alloc_base - 1 - j] : alloc_base + j;
+            }
+            if (h > s) synced_hi[r] = h;
+            const int64_t b0 = l / B;
+            Seg* out = segs + carry.y + off.y;
+            for (int32_t k = 0; k < cnt.y; ++k) {
+                const int64_t b = b0 + k;
+                const int64_t t0 = l > b * B ? l - b * B : 0;
+                const int64_t t1 = h < (b + 1) * B ? h - b * B : B;
+                Seg sg{srow[b], row[b], (int32_t)t0, (int32_t)t1};
+                // bounds check on every segment (defence in depth behind the host
+                // validation): an id outside its pool becomes an empty run, so the
+                // mover never touches memory out of range; the error word reports it
+                if (sg.src_blk < 0 || sg.src_blk >= src_cap || sg.dst_blk < 0 || sg.dst_blk >= dst_cap) {
+                    *reinterpret_cast<volatile int32_t*>(err) = 1;  // idempotent; err is host-mapped
+                    sg.t0 = sg.t1 = 0;
+                }
+                out[k] = sg;
+            }
+        }
+        carry.x += tot.x;
+        carry.y += tot.y;
+    }
+}
+
+// Block-manager helper: stack[i] = capacity - 1 - i (pops yield 0, 1, 2, ...).
+static __global__ void kvx_bm_init_kernel(int32_t* __restrict__ stack, int32_t capacity) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < capacity; i += gridDim.x * blockDim.x)
+        stack[i] = capacity - 1 - i;
+}
+
+// ------------------------------------------------------------ LSU mover
+constexpr int kMoveThreads = 512;
+constexpr int kMoveUnroll = 8;
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// CTA-cooperative copy of nvec 16-byte vectors.
+__device__ __forceinline__ void cta_copy(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                         uint32_t nvec) {
+    uint32_t i = threadIdx.x;
+    const uint32_t step = kMoveThreads * kMoveUnroll;
+    for (; i + (kMoveUnroll - 1) * kMoveThreads < nvec; i += step) {
+        uint4 v[kMoveUnroll];
+#pragma unroll
+        for (int u = 0; u < kMoveUnroll; ++u) v[u] = ld_stream(src + i + u * kMoveThreads);
+#pragma unroll
+        for (int u = 0; u < kMoveUnroll; ++u) st_stream(dst + i + u * kMoveThreads, v[u]);
+    }
+    for (; i < nvec; i += kMoveThreads) st_stream(dst + i, ld_stream(src + i));
+}
+
+// 256-bit variant (sm_100: LDG/STG.256): half the memory instructions per
+// byte; needs 32-byte-aligned runs (token_bytes % 32 == 0, checked on host).
+struct alignas(32) V8 {
+    uint32_t w[8];
+};
+__device__ __forceinline__ V8 ld_stream256(const V8* p) {
+    V8 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]),
+                   "=r"(v.w[6]), "=r"(v.w[7])
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream256(V8* p, const V8& v) {
+    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+                 "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                 : "memory");
+}
+__device__ __forceinline__ void cta_copy256(V8* __restrict__ dst, const V8* __restrict__ src, uint32_t n) {
+    constexpr int kU = 4;
+    uint32_t i = threadIdx.x;
+    const uint32_t step = kMoveThreads * kU;
+    for (; i + (kU - 1) * kMoveThreads < n; i += step) {
+        V8 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = ld_stream256(src + i + u * kMoveThreads);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) st_stream256(dst + i + u * kMoveThreads, v[u]);
+    }
+    for (; i < n; i += kMoveThreads) st_stream256(dst + i, ld_stream256(src + i));
+}
+
+static __global__ void __launch_bounds__(kMoveThreads)
+kvx_move256_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
+                   int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
+                   int32_t fence_system) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int64_t units = (int64_t)nseg * nlayers;
+    const uint64_t half = block_bytes >> 1;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t layer = (int32_t)(u / nseg);
+        const Seg sg = segs[u - (int64_t)layer * nseg];
+        const LayerPtr lp = layers[layer];
+        const char* src = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
+        char* dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
+        if (sg.t0 == 0 && sg.t1 == block_tokens && lp.src_kv == half && lp.dst_kv == half) {
+            cta_copy256(reinterpret_cast<V8*>(dst), reinterpret_cast<const V8*>(src), (uint32_t)(block_bytes >> 5));
+        } else {  // K then V rows; per head for head-major pools
+            const uint64_t off = (uint64_t)sg.t0 * lp.run_tok;
+            const uint32_t n = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * lp.run_tok) >> 5);
+            for (uint32_t r = 0; r < 2 * lp.nh; ++r) {
+                const uint32_t kv = r / lp.nh, h = r % lp.nh;
+                cta_copy256(reinterpret_cast<V8*>(dst + kv * lp.dst_kv + h * lp.dst_hs + off),
+                            reinterpret_cast<const V8*>(src + kv * lp.src_kv + h * lp.src_hs + off), n);
+            }
+        }
+    }
+    if (fence_system) __threadfence_system();
+}
+
+// Work unit u -> (layer = u / nseg, segment = u % nseg): consecutive CTAs walk
+// consecutive destination blocks of one layer (the dense rule makes them
+// contiguous), sources are wherever the old block table points.
+static __global__ void __launch_bounds__(kMoveThreads)
+kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
+                int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
+                int32_t fence_system) {
+    // launched with programmatic dependent launch behind the plan kernel:
+    // wait until its segment list is complete and visible (no-op otherwise)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int64_t units = (int64_t)nseg * nlayers;
+    const uint64_t half = block_bytes >> 1;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t layer = (int32_t)(u / nseg);
+        const Seg sg = segs[u - (int64_t)layer * nseg];
+        const LayerPtr lp = layers[layer];
+        const char* src = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
+        char* dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
+        if (sg.t0 == 0 && sg.t1 == block_tokens && lp.src_kv == half && lp.dst_kv == half) {
+            cta_copy(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src),
+                     (uint32_t)(block_bytes >> 4));
+        } else {  // K then V rows; per head for head-major pools
+            const uint64_t off = (uint64_t)sg.t0 * lp.run_tok;
+            const uint32_t nvec = (uint32_t)(((uint64_t)(sg.t1 - sg.t0) * lp.run_tok) >> 4);
+            for (uint32_t r = 0; r < 2 * lp.nh; ++r) {
+                const uint32_t kv = r / lp.nh, h = r % lp.nh;
+                cta_copy(reinterpret_cast<uint4*>(dst + kv * lp.dst_kv + h * lp.dst_hs + off),
+                         reinterpret_cast<const uint4*>(src + kv * lp.src_kv + h * lp.src_hs + off), nvec);
+            }
+        }
+    }
+    if (fence_system) __threadfence_system();  // peer (NVLink) stores visible before host sync
+}
+
+// --------------------------------------------- row-granular mover
+// Copies (K|V, token, head) rows of head_bytes, addressed through both
+// pools' strides -- any layout pair.  Used for moves between token-major
+// (BLOCKS, KV_PLANES) and head-major (HEADS) pools (tails_only = 0), and for
+// the partial blocks of head-major-to-head-major moves, whose 2*H short runs
+// would starve the bulk mover's single issuing thread (tails_only = 1: full
+// blocks are left to kvx_bulk_kernel).  Vectors of one row go to consecutive
+// threads; rows are ordered tokens-inner when the source is head-major (its
+// contiguous direction), heads-inner otherwise.  4 independent 16-byte loads
+// in flight per thread.
+static __global__ void __launch_bounds__(kMoveThreads)
+kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
+                    int32_t nlayers, int32_t heads, uint32_t head_bytes, int32_t block_tokens,
+                    int32_t tails_only, int32_t fence_system) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int kU = 4;
+    const int64_t units = (int64_t)nseg * nlayers;
+    const uint32_t vph = head_bytes >> 4;  // 16-byte vectors per row
+    const uint32_t H = (uint32_t)heads;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int32_t layer = (int32_t)(u / nseg);
+        const Seg sg = segs[u - (int64_t)layer * nseg];
+        const LayerPtr lp = layers[layer];
+        if (tails_only && (lp.nh <= 1 || (sg.t0 == 0 && sg.t1 == block_tokens))) continue;
+        const char* sb = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
+        char* db = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
+        const uint32_t ntok = (uint32_t)(sg.t1 - sg.t0);
+        if (ntok == 0) continue;  // emptied by the plan kernel's bounds check
+        const uint32_t per_kv = ntok * H * vph;
+        const bool tok_inner = lp.src_ts < lp.src_hs;  // head-major source (order barely matters:
+                                                        // profiles/r01_row_sweep.jsonl)
+        const uint32_t total = 2 * per_kv;
+        for (uint32_t base = threadIdx.x; base < total; base += kMoveThreads * kU) {
+            uint4 v[kU];
+            uint4* dp[kU];
+#pragma unroll
+            for (int k = 0; k < kU; ++k) {
+                const uint32_t i = base + (uint32_t)k * kMoveThreads;
+                dp[k] = nullptr;
+                if (i < total) {
+                    // plain division: a multiply-shift variant measured slower on the
+                    // same box (its per-unit set-up dominates short tails)
+                    const uint32_t kv = i / per_kv, r = i - kv * per_kv;
+                    const uint32_t w = r % vph, row = r / vph;
+                    const uint32_t h = tok_inner ? row / ntok : row % H;
+                    const uint32_t t = (uint32_t)sg.t0 + (tok_inner ? row % ntok : row / H);
+                    v[k] = ld_stream(reinterpret_cast<const uint4*>(sb + kv * lp.src_kv + t * lp.src_ts +
+                                                                    h * lp.src_hs) + w);
+                    dp[k] = reinterpret_cast<uint4*>(db + kv * lp.dst_kv + t * lp.dst_ts + h * lp.dst_hs) + w;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kU; ++k)
+                if (dp[k]) st_stream(dp[k], v[k]);
+        }
+    }
+    if (fence_system) __threadfence_system();
+}
+
+// ------------------------------------------------------- TMA bulk mover
+// One elected thread per CTA streams the CTA's (segment, layer) work through
+// a kBulkStages-deep shared-memory ring with the bulk-copy engine:
+//   cp.async.bulk global->shared (completes on an mbarrier with tx bytes),
+//   cp.async.bulk shared->global (bulk_group; .read completion frees the slot).
+// No registers carry payload; the SM's LSU pipe is idle.  Same work list and
+// unit order as kvx_move_kernel.
+constexpr int kBulkStages = 6;           // default ring depth
+constexpr uint32_t kBulkChunk = 32768;   // default bytes per stage (16-byte multiple)
+constexpr int kBulkThreads = 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
+                 "r"(smem_u32(smem)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
+    const Seg* segs;
+    const LayerPtr* layers;
+    int32_t nseg;
+    int64_t units, u, ustep;
+    uint64_t block_bytes, token_bytes;
+    int32_t block_tokens;
+    uint32_t chunk;
+    // current run
+    const char* src;
+    char* dst;
+    uint64_t left;
+    int run, nrun;  // current run / runs of the unit: 1 (whole block), 2 (K, V) or 2*nh
+    uint32_t nh;    // runs per K/V (head-major pools: one per head)
+    uint64_t run_bytes, off0;
+    const char* base_src;
+    char* base_dst;
+    uint64_t src_kv, dst_kv, src_hs, dst_hs;  // of the current unit's layer
+
+    __device__ bool load_unit() {
+        for (; u < units; u += ustep) {
+            const int32_t layer = (int32_t)(u / nseg);
+            const Seg sg = segs[u - (int64_t)layer * nseg];
+            const LayerPtr lp = layers[layer];
+            const bool full = sg.t0 == 0 && sg.t1 == block_tokens;
+            if (lp.nh > 1 && !full) continue;  // head-major tail: kvx_move_any_kernel(tails_only)
+            base_src = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
+            base_dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
+            src_kv = lp.src_kv;
+            dst_kv = lp.dst_kv;
+            src_hs = lp.src_hs;
+            dst_hs = lp.dst_hs;
+            const uint64_t half = block_bytes >> 1;
+            run = 0;
+            if (sg.t0 == 0 && sg.t1 == block_tokens && src_kv == half && dst_kv == half) {
+                nrun = 1;  // the whole block is one run on both sides (BLOCKS, HEADS)
+                nh = 1;
+                off0 = 0;
+                run_bytes = block_bytes;
+            } else {  // K rows then V rows; per head for head-major pools
+                nh = lp.nh;
+                nrun = 2 * (int)nh;
+                off0 = (uint64_t)sg.t0 * lp.run_tok;
+                run_bytes = (uint64_t)(sg.t1 - sg.t0) * lp.run_tok;
+            }
+            src = base_src + off0;
+            dst = base_dst + off0;
+            left = run_bytes;
+            return true;
+        }
+        return false;
+    }
+    __device__ bool next(const char** s, char** d, uint32_t* n) {
+        while (left == 0) {
+            if (++run < nrun) {  // next (K|V, head) run of the unit
+                const uint32_t kv = (uint32_t)run / nh, h = (uint32_t)run % nh;
+                src = base_src + kv * src_kv + h * src_hs + off0;
+                dst = base_dst + kv * dst_kv + h * dst_hs + off0;
+                left = run_bytes;
+                break;
+            }
+            u += ustep;
+            if (!load_unit()) return false;
+        }
+        const uint32_t c = left > chunk ? chunk : (uint32_t)left;
+        *s = src;
+        *d = dst;
+        *n = c;
+        src += c;
+        dst += c;
+        left -= c;
+        return true;
+    }
+};
+
+// Generic single-thread bulk streaming loop over any chunk iterator with
+// `bool next(const char**, char**, uint32_t*)`.
+template <int kStages, uint32_t kChunk, class Iter>
+__device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint64_t* bars) {
+    for (int i = 0; i < kStages; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    char* pend_dst[kStages];
+    uint32_t pend_n[kStages];
+    int64_t issued = 0, stored = 0;
+    bool more = true;
+    for (int st = 0; st < kStages && more; ++st) {  // prologue: fill the ring
+        const char* s;
+        char* d;
+        uint32_t n;
+        more = it.next(&s, &d, &n);
+        if (!more) break;
+        mbar_expect_tx(&bars[st], n);
+        bulk_g2s(smem + (size_t)st * kChunk, s, n, &bars[st]);
+        pend_dst[st] = d;
+        pend_n[st] = n;
+        ++issued;
+    }
+    while (stored < issued) {
+        const int st = (int)(stored % kStages);
+        const uint32_t parity = (uint32_t)((stored / kStages) & 1);
+        mbar_wait(&bars[st], parity);
+        bulk_s2g(pend_dst[st], smem + (size_t)st * kChunk, pend_n[st]);
+        bulk_commit();
+        ++stored;
+        // refill the slot stored one iteration ago once its store has read smem
+        if (more && stored >= 2) {
+            const int rs = (int)((stored - 2) % kStages);
+            const char* s;
+            char* d;
+            uint32_t n;
+            more = it.next(&s, &d, &n);
+            if (more) {
+                bulk_wait_read<1>();
+                mbar_expect_tx(&bars[rs], n);
+                bulk_g2s(smem + (size_t)rs * kChunk, s, n, &bars[rs]);
+                pend_dst[rs] = d;
+                pend_n[rs] = n;
+                ++issued;
+            }
+        }
+    }
+    bulk_wait_all();
+}
+
+// The first n_peer layers of `layers` have a peer (NVLink) destination.  When
+// a wave mixes them with local layers, CTAs [0, peer_ctas) stream only the
+// peer units and the rest only the local ones, so the NVLink-bound and the
+// HBM-bound traffic overlap instead of running layer after layer.
+template <int kStages, uint32_t kChunk>
+__global__ void __launch_bounds__(kBulkThreads)
+kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
+                int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
+                int32_t n_peer, int32_t peer_ctas) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[kStages];
+    if (threadIdx.x != 0) return;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the plan kernel's segments
+    ChunkIter it;
+    it.segs = segs;
+    it.layers = layers;
+    it.nseg = nseg;
+    const int64_t split = (int64_t)nseg * n_peer;
+    if (peer_ctas > 0 && n_peer > 0 && n_peer < nlayers && (int)gridDim.x > peer_ctas) {
+        if ((int)blockIdx.x < peer_ctas) {
+            it.u = blockIdx.x;
+            it.ustep = peer_ctas;
+            it.units = split;
+        } else {
+            it.u = split + (blockIdx.x - peer_ctas);
+            it.ustep = gridDim.x - peer_ctas;
+            it.units = (int64_t)nseg * nlayers;
+        }
+    } else {
+        it.u = blockIdx.x;
+        it.ustep = gridDim.x;
+        it.units = (int64_t)nseg * nlayers;
+    }
+    it.block_bytes = block_bytes;
+    it.token_bytes = token_bytes;
+    it.block_tokens = block_tokens;
+    it.chunk = kChunk;
+    it.left = 0;
+    it.run = 1;
+    if (!it.load_unit()) return;
+    bulk_stream<kStages, kChunk>(it, smem, bars);
+}
+
+// ------------------------------------------------- generic copy list
+// Activation handoff (and any batched device copy): a list of (src, dst,
+// bytes) pieces, 16-byte aligned, streamed by the same bulk engine loop.
+struct Piece {
+    const char* src;
+    char* dst;
+    uint64_t bytes;
+};
+
+struct PieceIter {
+    const Piece* p;
+    int64_t n, i, step;
+    const char* src;
+    char* dst;
+    uint64_t left;
+    uint32_t chunk;
+    __device__ bool next(const char** s, char** d, uint32_t* c) {
+        while (left == 0) {
+            i += step;
+            if (i >= n) return false;
+            src = p[i].src;
+            dst = p[i].dst;
+            left = p[i].bytes;
+        }
+        const uint32_t k = left > chunk ? chunk : (uint32_t)left;
+        *s = src;
+        *d = dst;
+        *c = k;
+        src += k;
+        dst += k;
+        left -= k;
+        return true;
+    }
+};
+
+template <int kStages, uint32_t kChunk>
+__global__ void __launch_bounds__(kBulkThreads)
+kvx_copy_list_kernel(const Piece* __restrict__ pieces, int64_t n) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[kStages];
+    if (threadIdx.x != 0 || (int64_t)blockIdx.x >= n) return;
+    PieceIter it;
+    it.p = pieces;
+    it.n = n;
+    it.step = gridDim.x;
+    it.i = (int64_t)blockIdx.x - it.step;
+    it.left = 0;
+    it.chunk = kChunk;
+    bulk_stream<kStages, kChunk>(it, smem, bars);
+}
+
+// ------------------------------------------------------------- commit
+constexpr int kCommitThreads = 1024;
+
+// Phase A (this kernel, one CTA): live flags, Eq. 10 violations, CSR row
+// pointers and free-list offsets; phase B writes the blocks (same kernel,
+// after the scans).  live_flag is a scratch [max_requests] array.
+static __global__ void __launch_bounds__(kCommitThreads, 1)
+kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ kv, int32_t n,
+                  const int32_t* __restrict__ dst_bt, const int64_t* __restrict__ synced_hi,
+                  uint8_t* __restrict__ live_flag, int32_t max_requests, int32_t max_blocks,
+                  int32_t block_tokens, int32_t* __restrict__ row_ptr,
+                  int32_t* __restrict__ blocks, int32_t* __restrict__ free_list,
+                  int64_t* __restrict__ out /* [0]=violations [1]=n_blocks [2]=n_free */,
+                  int32_t* __restrict__ free_list_dev /* optional device copy (block-manager push) */,
+                  const int32_t* __restrict__ err = nullptr /* plan-kernel error word -> out[3] */) {
+    __shared__ unsigned long long s_viol;
+    if (threadIdx.x == 0) s_viol = 0;
+    for (int32_t r = threadIdx.x; r < max_requests; r += kCommitThreads) live_flag[r] = 0;
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < n; i += kCommitThreads) live_flag[req[i]] = 1;
+    __syncthreads();
+    const int64_t B = block_tokens;
+
+    // Live rows: violation ballot + CSR of the allocated blocks.
+    int2 carry = make_int2(0, 0);
+    for (int32_t base = 0; base < n; base += kCommitThreads) {
+        const int32_t i = base + (int32_t)threadIdx.x;
+        int32_t nb = 0;
+        bool bad = false;
+        int32_t r = -1;
+        if (i < n) {
+            r = req[i];
+            const int64_t s = synced_hi[r];
+            bad = s != kv[i];  // engine.cpp:712
+            nb = (int32_t)cdiv(s, B);
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, bad);
+        if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(&s_viol, (unsigned long long)__popc(ballot));
+        int2 tot;
+        const int2 off = block_exclusive_scan2<kCommitThreads>(make_int2(nb, 0), &tot);
+        if (i < n) {
+            const int32_t o = carry.x + off.x;
+            if (row_ptr) row_ptr[i] = o;
+            if (blocks)
+                for (int32_t k = 0; k < nb; ++k) blocks[o + k] = dst_bt[(int64_t)r * max_blocks + k];
+        }
+        carry.x += tot.x;
+    }
+    if (threadIdx.x == 0 && row_ptr) row_ptr[n] = carry.x;
+    const int32_t n_blocks = carry.x;
+
+    // Dead rows (allocated but no longer live): ballot-compacted free list.
+    carry = make_int2(0, 0);
+    for (int32_t base = 0; base < max_requests; base += kCommitThreads) {
+        const int32_t r = base + (int32_t)threadIdx.x;
+        int32_t nb = 0;
+        if (r < max_requests && !live_flag[r]) nb = (int32_t)cdiv(synced_hi[r], B);
+        int2 tot;
+        const int2 off = block_exclusive_scan2<kCommitThreads>(make_int2(nb, 0), &tot);
+        if (nb > 0 && (free_list || free_list_dev))
+            for (int32_t k = 0; k < nb; ++k) {
+                const int32_t id = dst_bt[(int64_t)r * max_blocks + k];
+                if (free_list) free_list[carry.x + off.x + k] = id;
+                if (free_list_dev) free_list_dev[carry.x + off.x + k] = id;
+            }
+        carry.x += tot.x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        out[0] = (int64_t)s_viol;
+        out[1] = n_blocks;
+        out[2] = carry.x;
+        out[3] = err ? (int64_t)*err : 0;
+    }
+}
+
+// ---------------------------------------------------- payload kernels
+// grid = (entries, max logical blocks); one CTA per (request, logical block),
+// looping over the pool's layers and the block's K/V token rows.
+// from == nullptr: tokens [0, tokens[i]); else [from[i], tokens[i]) (decode appends).
+static __global__ void __launch_bounds__(256)
+kvx_fill_kernel(PoolAddr pa, int32_t first_layer,
+                int32_t num_layers, const int32_t* __restrict__ req,
+                const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
+                int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed,
+                const int64_t* __restrict__ from = nullptr) {
+    const int32_t i = blockIdx.x;
+    const int32_t r = req[i];
+    const uint32_t vecs = (uint32_t)(token_bytes >> 4);
+    for (int32_t b = blockIdx.y; (int64_t)b * block_tokens < tokens[i]; b += gridDim.y) {  // grid.y <= 65535
+        int64_t t_begin = (int64_t)b * block_tokens;
+        const int64_t t_end = min(tokens[i], t_begin + block_tokens);
+        if (from) {
+            if (t_end <= from[i]) continue;
+            t_begin = max(t_begin, from[i]);
+        }
+        const int32_t blk = bt[(int64_t)r * max_blocks + b];
+        const int32_t rows = (int32_t)(t_end - t_begin);
+        const int32_t row0 = (int32_t)(t_begin - (int64_t)b * block_tokens);  // first row inside the block
+        for (int32_t l = 0; l < num_layers; ++l) {
+            char* slab = pa.layer[l] + (uint64_t)blk * pa.blk_stride;
+            for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
+                const int32_t kvi = kvr / rows, t = kvr % rows;
+                const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
+                char* row = slab + (uint64_t)kvi * pa.kv_stride + (uint64_t)(row0 + t) * pa.tok_stride;
+                const uint32_t vph = pa.head_bytes >> 4;  // vector v of the token lies in head v / vph
+                for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x)
+                    *reinterpret_cast<uint4*>(row + (uint64_t)(v / vph) * pa.head_stride + (v % vph) * 16u) =
+                        pattern_vec(th, v);
+            }
+        }
+    }
+}
+
+static __global__ void __launch_bounds__(256)
+kvx_verify_kernel(PoolAddr pa, int32_t first_layer,
+                  int32_t num_layers, const int32_t* __restrict__ req,
+                  const int64_t* __restrict__ tokens, const int32_t* __restrict__ bt,
+                  int32_t max_blocks, int32_t block_tokens, uint64_t token_bytes, uint64_t seed,
+                  unsigned long long* __restrict__ mismatches) {
+    const int32_t i = blockIdx.x;
+    const int32_t r = req[i];
+    const uint32_t vecs = (uint32_t)(token_bytes >> 4);
+    unsigned long long bad = 0;
+    for (int32_t b = blockIdx.y; (int64_t)b * block_tokens < tokens[i]; b += gridDim.y) {  // grid.y <= 65535
+        const int64_t t_begin = (int64_t)b * block_tokens;
+        const int64_t t_end = min(tokens[i], t_begin + block_tokens);
+        const int32_t blk = bt[(int64_t)r * max_blocks + b];
+        const int32_t rows = (int32_t)(t_end - t_begin);
+        if (blk < 0) {
+            bad += threadIdx.x == 0 ? (unsigned long long)num_layers * 2 * rows * vecs * 8 : 0;
+            continue;
+        }
+        for (int32_t l = 0; l < num_layers; ++l) {
+            const char* slab = pa.layer[l] + (uint64_t)blk * pa.blk_stride;
+            for (int32_t kvr = 0; kvr < 2 * rows; ++kvr) {
+                const int32_t kvi = kvr / rows, t = kvr % rows;
+                const uint64_t th = token_hash(seed, r, first_layer + l, kvi, t_begin + t);
+                const char* row = slab + (uint64_t)kvi * pa.kv_stride + (uint64_t)t * pa.tok_stride;
+                const uint32_t vph = pa.head_bytes >> 4;
+                for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) {
+                    const uint4 want = pattern_vec(th, v);
+                    const uint4 got =
+                        *reinterpret_cast<const uint4*>(row + (uint64_t)(v / vph) * pa.head_stride + (v % vph) * 16u);
+                    const uint32_t d[4] = {want.x ^ got.x, want.y ^ got.y, want.z ^ got.z, want.w ^ got.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) bad += ((d[q] & 0xffffu) != 0) + ((d[q] >> 16) != 0);
+                }
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatches, bad);
+}
+
+}  // namespace kvx

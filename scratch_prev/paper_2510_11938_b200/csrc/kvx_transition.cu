@@ -244,11 +244,11 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
                             cudaMemcpyHostToDevice, t->stream) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "layer table upload"));
     }
-    // side stream: the head-major tail mover beside the bulk mover, and the commit
-    // kernel beside the last wave's mover (see kvx_wave / kvx_commit_async)
-    if (A.stream(&t->side) != cudaSuccess || A.event(&t->ev_join, false) != cudaSuccess ||
-        A.event(&t->ev_side_commit, false) != cudaSuccess)
-        return bail(fail(KVX_ECUDA, "side stream"));
+    if (t->head_tails) {  // side stream for the head-major tail mover (see kvx_wave)
+        if (cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking) != cudaSuccess ||
+            A.event(&t->ev_join, false) != cudaSuccess)
+            return bail(fail(KVX_ECUDA, "side stream"));
+    }
     // No host sync: the uploads above were staged from pageable memory
     // (copied out before cudaMemcpyAsync returned) and are stream-ordered
     // before every wave.
@@ -327,7 +327,6 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         t->src_cap, t->dst_num_blocks, t->d_err);
     KVX_LAUNCHED();
     KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
-    t->last_plan_slot = slot;  // this event now marks the table / synced marks as final
     if (t->bm && new_blocks > 0) KVX_CUDA(bm_order_after(t->bm, t->stream));
     if (t->n_local_layers > 0) {
         const int64_t units = nseg * t->n_local_layers;
@@ -483,27 +482,14 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
     // staging slot and writes its results straight into the pinned landing
     // zone h_commit = [int64 x4 | row_ptr | blocks | free]: no copies on the
     // stream.  A device copy of the free list feeds the block-manager push.
-    // The commit kernel reads only the block table, the synced marks and the
-    // plan error word -- final once the last plan kernel ran -- not the KV bytes:
-    // it runs on the side stream beside the last wave's mover, and the commit
-    // event below joins both (the stall is plan + max(mover, commit)).
-    cudaStream_t cs = t->stream;
-    if (t->last_plan_slot >= 0 && t->side) {
-        KVX_CUDA(cudaStreamWaitEvent(t->side, t->h_wave_free[t->last_plan_slot], 0));
-        cs = t->side;
-    }
     int32_t* h32 = reinterpret_cast<int32_t*>(t->h_commit + 32);
-    kvx::kvx_commit_kernel<<<1, kvx::kCommitThreads, 0, cs>>>(
+    kvx::kvx_commit_kernel<<<1, kvx::kCommitThreads, 0, t->stream>>>(
         reinterpret_cast<const int32_t*>(h), reinterpret_cast<const int64_t*>(h + off_kv), n_live, t->d_dst_bt,
         t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens, h32, h32 + (n_live + 1),
         h32 + (n_live + 1) + nb_live, reinterpret_cast<int64_t*>(t->h_commit), t->bm ? d_free : nullptr,
         t->d_err);
     KVX_LAUNCHED();
-    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], cs));
-    if (cs != t->stream) {
-        KVX_CUDA(cudaEventRecord(t->ev_side_commit, cs));
-        KVX_CUDA(cudaStreamWaitEvent(t->stream, t->ev_side_commit, 0));
-    }
+    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     (void)d_row_ptr;
     (void)d_blocks;
     if (t->bm && nb_free > 0) {  // free-list update: dead rows' blocks back on the stack
@@ -628,10 +614,9 @@ int kvx_destroy(kvx_transition* t) {
     }
     if (t->side) {
         cudaStreamSynchronize(t->side);
-        A.stream_free(t->side);
+        cudaStreamDestroy(t->side);
     }
     A.event_free(t->ev_join, false);
-    A.event_free(t->ev_side_commit, false);
     if (t->stream && t->own_stream) cudaStreamDestroy(t->stream);
     delete t;
     return KVX_OK;

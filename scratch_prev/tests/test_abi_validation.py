@@ -1,0 +1,134 @@
+"""C-ABI argument validation (CPU): malformed descriptors and arrays are
+rejected with KVX_EINVAL (or KVX_ESTALE/ESTATE) before any CUDA call, never
+by a crash -- the boundary never throws and never dereferences NULL."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2510_11938_b200 import kvx
+
+L = kvx.lib()
+
+
+def desc(**over):
+    d = kvx._Desc()
+    d.geometry = kvx.geometry(4, 2, 64)
+    ob = (C.c_int32 * 1)(2)
+    nb = (C.c_int32 * 1)(1)
+    pools = (C.c_void_p * 2)(None, None)
+    d.old_plan = kvx._Plan(2, ob, C.cast(pools, C.POINTER(C.c_void_p)))
+    d.new_plan = kvx._Plan(2, nb, C.cast(pools, C.POINTER(C.c_void_p)))
+    d.max_requests, d.max_blocks, d.dst_num_blocks = 4, 4, 16
+    bt = (C.c_int32 * 16)(*([-1] * 16))
+    d.src_block_table = C.cast(bt, C.POINTER(C.c_int32))
+    d.epoch = 1
+    keep = (ob, nb, pools, bt)
+    for k, v in over.items():
+        setattr(d, k, v)
+    return d, keep
+
+
+def begin_rc(d):
+    h = C.c_void_p()
+    return L.kvx_begin(C.byref(d), C.byref(h))
+
+
+def test_null_arguments():
+    h = C.c_void_p()
+    assert L.kvx_begin(None, C.byref(h)) == kvx.KVX_EINVAL
+    assert L.kvx_wave(None, 1, 0, None, None, None) == kvx.KVX_EINVAL
+    assert L.kvx_wait(None, 1, None) == kvx.KVX_EINVAL
+    assert L.kvx_commit(None, 1, 0, None, None, None) == kvx.KVX_EINVAL
+    assert L.kvx_abort(None) == kvx.KVX_EINVAL
+    assert L.kvx_destroy(None) == kvx.KVX_OK
+    assert L.kvx_pool_destroy(None) == kvx.KVX_OK
+    assert L.kvx_bm_destroy(None) == kvx.KVX_OK
+    assert L.kvx_handoff(None, 1, 16, 0, None, None, None, None) == kvx.KVX_EINVAL
+    assert L.kvx_ctl_begin(None, 0, None, None, None) == kvx.KVX_EINVAL
+
+
+@pytest.mark.parametrize("field,value", [
+    ("max_requests", 0), ("max_blocks", 0), ("dst_num_blocks", 0),
+])
+def test_bad_sizes(field, value):
+    d, keep = desc(**{field: value})
+    assert begin_rc(d) == kvx.KVX_EINVAL
+
+
+def test_bad_geometry_and_plans():
+    d, keep = desc()
+    d.geometry = kvx.geometry(4, 1, 4)           # token_bytes 8: not a 16-byte multiple
+    assert begin_rc(d) == kvx.KVX_EINVAL
+    d, keep = desc()
+    bad = (C.c_int32 * 1)(4)                      # boundary == L
+    d.old_plan = kvx._Plan(2, bad, d.old_plan.pools)
+    assert begin_rc(d) == kvx.KVX_EINVAL
+    d, keep = desc()
+    d.new_plan = kvx._Plan(9, d.new_plan.boundaries, d.new_plan.pools)  # more stages than layers
+    assert begin_rc(d) == kvx.KVX_EINVAL
+    d, keep = desc()
+    d.src_block_table = None
+    assert begin_rc(d) == kvx.KVX_EINVAL
+
+
+def test_missing_new_pool_rejected_in_push_mode():
+    d, keep = desc()                               # new_plan pools are NULL
+    assert begin_rc(d) == kvx.KVX_EINVAL
+    assert b"new-stage pool" in L.kvx_last_error()
+
+
+def test_negative_max_ctas_rejected():
+    d, keep = desc(max_ctas=-1)
+    assert begin_rc(d) == kvx.KVX_EINVAL
+
+
+def test_error_message_is_thread_local_and_set():
+    d, keep = desc(max_blocks=0)
+    begin_rc(d)
+    msg = L.kvx_last_error()
+    assert isinstance(msg, bytes) and len(msg) > 0
+
+
+def test_pool_wrap_validation():
+    g = kvx.geometry(4, 2, 64)
+    h = C.c_void_p()
+    assert L.kvx_pool_wrap(0, None, 1 << 20, C.byref(g), 2, 4, C.byref(h)) == kvx.KVX_EINVAL
+    assert L.kvx_pool_wrap(0, C.c_void_p(0x1001), 1 << 20, C.byref(g), 2, 4, C.byref(h)) == kvx.KVX_EINVAL  # misaligned
+    assert L.kvx_pool_wrap(0, C.c_void_p(0x1000), 16, C.byref(g), 2, 4, C.byref(h)) == kvx.KVX_EINVAL      # too small
+
+
+def test_layout_validation():
+    g = kvx.geometry(4, 2, 64)
+    h = C.c_void_p()
+    assert L.kvx_pool_create_layout(0, C.byref(g), 2, 4, 7, C.byref(h)) == kvx.KVX_EINVAL   # unknown layout
+    g8 = kvx.geometry(4, 4, 4)                                # 8-byte head rows: no head-major layout
+    assert L.kvx_pool_create_layout(0, C.byref(g8), 2, 4, kvx.LAYOUT_HEADS, C.byref(h)) == kvx.KVX_EINVAL
+    ok = (C.c_void_p * 2)(0x1000, 0x2000)
+    bb = g.block_bytes
+    W = L.kvx_pool_wrap_layers
+    assert W(0, 2, None, 4 * bb, C.byref(g), 4, kvx.LAYOUT_KV_PLANES, C.byref(h)) == kvx.KVX_EINVAL
+    assert W(0, 2, ok, 4 * bb, C.byref(g), 4, 9, C.byref(h)) == kvx.KVX_EINVAL               # unknown layout
+    assert W(0, 2, ok, 4 * bb - 16, C.byref(g), 4, 1, C.byref(h)) == kvx.KVX_EINVAL          # layer too small
+    assert W(0, 2, (C.c_void_p * 2)(0x1000, None), 4 * bb, C.byref(g), 4, 1, C.byref(h)) == kvx.KVX_EINVAL
+    assert W(0, 2, (C.c_void_p * 2)(0x1000, 0x2008), 4 * bb, C.byref(g), 4, 1, C.byref(h)) == kvx.KVX_EINVAL
+    # bookkeeping only: a valid per-layer wrap needs no GPU; it cannot be read or exported
+    assert W(0, 2, ok, 4 * bb, C.byref(g), 4, kvx.LAYOUT_KV_PLANES, C.byref(h)) == kvx.KVX_OK
+    lay = C.c_int32(-1)
+    assert L.kvx_pool_layout(h, C.byref(lay)) == kvx.KVX_OK and lay.value == kvx.LAYOUT_KV_PLANES
+    buf = (C.c_uint8 * 16)()
+    assert L.kvx_pool_read(h, 0, 16, buf) == kvx.KVX_EINVAL
+    assert L.kvx_pool_export(h, (C.c_char * 64)()) == kvx.KVX_EINVAL
+    assert L.kvx_pool_destroy(h) == kvx.KVX_OK
+
+
+def test_weights_validation():
+    ob = (C.c_int32 * 1)(2)
+    ptrs = (C.c_void_p * 2)(None, None)
+    db, hb = C.c_uint64(), C.c_uint64()
+    # layer_bytes not a 16-byte multiple
+    assert L.kvx_weights_migrate(0, None, 4, 10, 2, ob, ptrs, 2, ob, ptrs, None, None,
+                                 C.byref(db), C.byref(hb)) == kvx.KVX_EINVAL
+    # missing new-stage buffer
+    assert L.kvx_weights_migrate(0, None, 4, 16, 2, ob, ptrs, 2, ob, ptrs, None, None,
+                                 C.byref(db), C.byref(hb)) == kvx.KVX_EINVAL
