@@ -250,6 +250,7 @@ struct kvx_transition {
     cudaStream_t side = nullptr;  // side stream (arena-cached): head-major tails, the commit kernel
     cudaEvent_t ev_side_commit = nullptr;
     int last_plan_slot = -1;      // h_wave_free[slot] recorded after the most recent plan kernel
+    bool handoff_since_plan = false;
     int32_t max_ctas = 0;         // cap on mover CTAs per wave (0 = tuned grid)
     cudaEvent_t ev_join = nullptr;
     bool has_peer_dst = false;

@@ -81,6 +81,7 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
             pieces.push_back({src + o, dst + o, std::min<uint64_t>(65536, b - o)});
     }
     if (pieces.empty()) return KVX_OK;
+    t->handoff_since_plan = true;  // the commit then stays on the main stream (kvx_commit_async)
     DeviceGuard dg(t->device);
     kvx::Arena& A = kvx::Arena::of(t->device);
     if (!t->pieces_free) KVX_CUDA(A.event(&t->pieces_free, false));

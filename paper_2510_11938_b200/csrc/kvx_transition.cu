@@ -328,6 +328,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     KVX_LAUNCHED();
     KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     t->last_plan_slot = slot;  // this event now marks the table / synced marks as final
+    t->handoff_since_plan = false;
     if (t->bm && new_blocks > 0) KVX_CUDA(bm_order_after(t->bm, t->stream));
     if (t->n_local_layers > 0) {
         const int64_t units = nseg * t->n_local_layers;
@@ -487,8 +488,10 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
     // plan error word -- final once the last plan kernel ran -- not the KV bytes:
     // it runs on the side stream beside the last wave's mover, and the commit
     // event below joins both (the stall is plan + max(mover, commit)).
+    // (not after a handoff: there the fork/join cost more than they hid, same-box A/B
+    // profiles/r01_ab_stall.txt)
     cudaStream_t cs = t->stream;
-    if (t->last_plan_slot >= 0 && t->side) {
+    if (t->last_plan_slot >= 0 && t->side && !t->handoff_since_plan) {
         KVX_CUDA(cudaStreamWaitEvent(t->side, t->h_wave_free[t->last_plan_slot], 0));
         cs = t->side;
     }
