@@ -262,3 +262,46 @@ def test_request_longer_than_grid_y(gpu_count):
         tr.close()
         for p in old + new:
             p.close()
+
+
+def test_many_requests(gpu_count):
+    """200,000 live requests in two waves (the single-CTA plan and commit
+    kernels loop over entries and blocks): tables, bytes, compaction and the
+    free list equal the oracle's."""
+    L, N = 2, 200_000
+    rng = np.random.default_rng(42)
+    g, og = kvx.geometry(L, 1, 8), O.geo(L, 1, 8)
+    final = rng.integers(1, 40, N).astype(np.int64)
+    mb = int((final.max() + 15) // 16)
+    src_bt, cap0 = W.fragmented_block_table(final, mb, 16, seed=9, slack=0.1)
+    cap1 = int(((final + 15) // 16).sum())
+    live = np.arange(N, dtype=np.int32)
+    old = [kvx.Pool(0, g, 1, cap0) for _ in range(2)]
+    for k, p in enumerate(old):
+        p.zero()
+        p.fill_pattern(SEED, k, live, final, src_bt)
+    new = [kvx.Pool(0, g, L, cap1)]
+    new[0].zero()
+    tr = kvx.Transition(g, [1], old, [], new, 0, N, mb, cap1, src_bt)
+    dp = O.DataPlane(og, [1], [], cap0, cap1, N, mb, src_bt)
+    dp.fill_source(SEED, live, final)
+    try:
+        half = final // 2
+        tr.wave(live, np.zeros(N, np.int64), half)
+        assert dp.wave(live, np.zeros(N, np.int64), half) == 0
+        tr.wave(live, half, final)
+        assert dp.wave(live, half, final) == 0
+        tr.wait()
+        np.testing.assert_array_equal(tr.dst_block_table(), dp.bt)
+        np.testing.assert_array_equal(new[0].read(), dp.new_pools[0])
+        alive = live[rng.random(N) < 0.7]
+        res = tr.commit(alive, final[alive])
+        v, row_ptr, blocks, free = dp.commit(alive, final[alive])
+        assert res.violations == v == 0
+        np.testing.assert_array_equal(res.row_ptr, row_ptr)
+        np.testing.assert_array_equal(res.blocks, blocks)
+        np.testing.assert_array_equal(res.free_list, free)
+    finally:
+        tr.close()
+        for p in old + new:
+            p.close()
