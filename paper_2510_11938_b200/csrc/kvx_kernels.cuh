@@ -16,16 +16,22 @@
 //                        or NVLink-peer destinations; optional CTA split
 //                        between peer and local layers.  Launched with PDL
 //                        behind the plan kernel (griddepcontrol.wait).
+//                        Pools of any layout (per-layer base, block / K-V /
+//                        token / head strides); NVLink-peer sources (pull) too.
 //   kvx_move_kernel      LSU mover (16-byte ld.global.nc / st.global, 8 in
 //                        flight per thread); kvx_move256_kernel its 256-bit
 //                        variant.  KVX_MOVE_IMPL=lsu|lsu256.
+//   kvx_move_any_kernel  row mover: (K|V, token, head) rows through both pools'
+//                        strides -- token-major <-> head-major (HND) transposes,
+//                        and head-major tails beside the bulk mover.
 //   kvx_copy_list_kernel bulk engine over a (src, dst, bytes) list: activation
 //                        handoff and stage weight migration.
 //   kvx_commit_kernel    one CTA: Eq. 10 check per live request
 //                        (engine.cpp:707-713) with warp ballots, CSR
 //                        compaction of live rows, free list of rows no longer
 //                        live (scans); results written into mapped pinned
-//                        memory.
+//                        memory.  Runs beside the last wave's mover (side
+//                        stream): it needs the table, not the bytes.
 //   kvx_bm_init_kernel   block-manager stack initialisation.
 //   kvx_fill_kernel / kvx_verify_kernel   synthetic payload (tests + bench).
 #pragma once
