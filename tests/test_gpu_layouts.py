@@ -8,6 +8,8 @@ allocations or one caller-owned tensor per layer (kvx_pool_wrap_layers).  A
 refactor then also converts the cache between backends.  The oracle works in
 the block layout; a layout is a permutation of the same bytes, so every pool
 is compared with the oracle's pool permuted into its layout, bit for bit."""
+import os
+
 import numpy as np
 import pytest
 
@@ -53,7 +55,7 @@ def make_pool(torch, rng, g, layers, blocks, allow_wrap, layout=None):
     return p, (lambda p=p: p.read().reshape(layers, -1)), layout, None
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVX_LAYOUT_SEEDS", "24"))))  # soak: more seeds
 def test_random_layouts_bit_exact(gpu_count, seed, uniform=None):
     """uniform = (old layout, new layout) for every stage; None = random per stage."""
     import torch

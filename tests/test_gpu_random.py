@@ -37,7 +37,7 @@ def one_case(seed):
     return rng, L, heads, dim, elem, B, ob, nb, N, final, max_blocks, use_bm
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVX_RANDOM_SEEDS", "40"))))  # soak: more seeds
 def test_random_transition_bit_exact(gpu_count, seed, max_ctas=0):
     rng, L, heads, dim, elem, B, ob, nb, N, final, max_blocks, use_bm = one_case(seed)
     g, og = kvx.geometry(L, heads, dim, elem, B), O.geo(L, heads, dim, elem, B)
