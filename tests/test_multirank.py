@@ -1,6 +1,7 @@
 """Multi-process transitions: world_size-2 host logic on CPU (gloo), and the
 NVLink P2P push path on 2 GPUs (-m gpu; skipped on a 1-GPU box)."""
 import multiprocessing as mp
+import os
 import random
 
 import pytest
@@ -128,7 +129,7 @@ def test_two_gpu_activation_handoff(gpu_count):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVX_MGPU_SEEDS", "6"))))  # soak: more seeds
 def test_two_gpu_random_bit_exact(gpu_count, seed):
     if gpu_count < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
