@@ -218,10 +218,17 @@ typedef struct kvx_transition_desc {
 typedef struct kvx_transition kvx_transition;
 
 /* Grants the destination: allocates the transition state on `device`.
- * No bytes move until the first kvx_wave. */
+ * No bytes move until the first kvx_wave.
+ * Replaces: the data-plane side of Engine::begin_refactor once the grant
+ * succeeded -- RefactorCtx creation, engine.cpp:633-635 (grant and binding
+ * :584-619 stay the engine's).  KVX_ENOSPC maps to a refactor hold
+ * (engine.cpp:563,592-593). */
 int kvx_begin(const kvx_transition_desc* d, kvx_transition** out);
 
-/* Enqueues one wave: for each entry, tokens [lo[i], hi[i]) of request req[i]
+/* Replaces: the simulated sync charge sync_ms = tokens * bpt / kv_bw of
+ * wave 0 (engine.cpp:637-647), delta waves (:665-674) and the final wave
+ * (:680-687) -- the bytes move instead of being charged.
+ * Enqueues one wave: for each entry, tokens [lo[i], hi[i]) of request req[i]
  * across every layer.  req must be strictly ascending (the std::map order of
  * RefactorCtx::sync_target, engine.hpp:153-154); entries with lo == hi are
  * allowed (the reference snapshots zero-delta requests too, engine.cpp:548).
@@ -230,7 +237,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out);
 int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
              const int64_t* lo, const int64_t* hi);
 /* Blocks until every enqueued wave finished; *measured_ms = device time of
- * the waves since the previous wait (CUDA events on the handle's stream). */
+ * the waves since the previous wait (CUDA events on the handle's stream).
+ * Replaces: the modelled arrival of KvSyncComplete (engine.cpp:646,651). */
 int kvx_wait(kvx_transition* t, uint64_t epoch, double* measured_ms);
 
 typedef struct kvx_commit_result {
@@ -246,7 +254,9 @@ typedef struct kvx_commit_result {
 
 /* Final apply + consistency check + block-table compaction for the live
  * (req, kv_tokens) set, ascending req.  After a successful commit the
- * destination pools with the returned block table are the stage's KV. */
+ * destination pools with the returned block table are the stage's KV.
+ * Replaces: Engine::on_refactor_commit's final apply and Eq. 10 check,
+ * engine.cpp:697-713 (violations == the host loop's count). */
 int kvx_commit(kvx_transition* t, uint64_t epoch, int32_t n_live, const int32_t* req,
                const int64_t* kv_tokens, kvx_commit_result* out);
 /* The same commit split in two: _async enqueues the check + compaction and
@@ -258,8 +268,11 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
                      const int64_t* kv_tokens);
 int kvx_commit_collect(kvx_transition* t, kvx_commit_result* out);
 /* Drops every destination allocation, invalidates the epoch (++epoch,
- * engine.cpp:769).  The source pools were never modified. */
+ * engine.cpp:769).  The source pools were never modified.
+ * Replaces: abort_refactor, engine.cpp:759-772. */
 int kvx_abort(kvx_transition* t);
+/* Frees the handle (after its stream drained).  Replaces: inst.refactor.reset(),
+ * engine.cpp:750. */
 int kvx_destroy(kvx_transition* t);
 
 /* Introspection: current epoch, and the dense destination block table
