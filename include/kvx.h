@@ -362,11 +362,19 @@ typedef struct kvx_ctl_state {
     int64_t last_wave_tokens;
 } kvx_ctl_state;
 
+/* Replaces begin_refactor's snapshot + wave 0 + byte accounting,
+ * engine.cpp:637-647 (snapshot_sync_targets :548-556).  (n, req, kv) = the
+ * live homed requests and their kv_tokens, ascending. */
 int kvx_ctl_begin(kvx_transition* t, int32_t n, const int32_t* req, const int64_t* kv,
                   int64_t* tokens_out);
+/* Replaces on_kv_sync_complete, engine.cpp:651-688: apply, then a delta wave
+ * (kv_tokens_unsynced :534-546, max_sync_rounds), the barrier, or the final
+ * wave once inflight_batches == 0 (or at once in handoff mode). */
 int kvx_ctl_sync_complete(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
                           const int64_t* kv, int32_t inflight_batches, int32_t* action_out,
                           int64_t* tokens_out);
+/* Replaces on_refactor_commit's apply + Eq. 10, engine.cpp:697-713; the
+ * device count must equal the mirror's (else KVX_ECUDA). */
 int kvx_ctl_commit(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
                    const int64_t* kv, kvx_commit_result* out);
 int kvx_ctl_commit_async(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
