@@ -65,3 +65,12 @@ def test_product_never_imports_the_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "kvx_oracle" not in txt, f
+
+
+def test_python_face_binds_every_declared_symbol():
+    """kvx.py gives every header entry point a typed ctypes signature (a
+    missing one would silently default to int arguments)."""
+    src = open(os.path.join(ROOT, "paper_2510_11938_b200", "kvx.py")).read()
+    bound = set(re.findall(r'"(kvx_\w+)":\s*\(', src))
+    missing = [n for n in declared() if n not in bound]
+    assert not missing, missing
