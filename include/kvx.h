@@ -196,7 +196,8 @@ typedef struct kvx_transition_desc {
     int32_t dst_num_blocks;       /* block capacity of every new-stage pool */
     const int32_t* src_block_table; /* host [max_requests * max_blocks], the old pipeline's */
     uint64_t epoch;               /* InstanceRt::epoch after ++ (engine.cpp:634) */
-    int32_t max_sync_rounds;      /* EngineConfig::max_sync_rounds (engine.hpp:75), kvx_ctl_* */
+    int32_t max_sync_rounds;      /* EngineConfig::max_sync_rounds (engine.hpp:75; default 8), kvx_ctl_*;
+                                     taken as given: 0 = no delta wave, wave 0 then the barrier */
     double kv_bytes_per_token;    /* accounting of kvx_ctl_* (engine.cpp:644); 0 = from geometry */
     void* stream;                 /* cudaStream_t to run on (not owned); NULL = a private stream */
     void* dst_blockmgr;           /* kvx_blockmgr* of the new pools; NULL = bump rule from id 0 */

@@ -178,6 +178,67 @@ void kvo_fill(const kvo_geometry* g, uint64_t seed, int32_t num_stages, const in
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+/* kvo_fill restricted to ONE model layer of one pool, on a zeroed image,
+ * striped over `threads` pthreads: phase 1 zeroes a slice of the layer per
+ * thread, phase 2 writes the rows of every (tid + k * threads)-th request. */
+typedef struct {
+    const kvo_geometry* g;
+    uint64_t seed;
+    int32_t layer, blocks_per_pool, n, max_blocks, tid, nthreads;
+    uint8_t* buf;
+    const int32_t *req, *bt;
+    const int64_t* tokens;
+} fill_job;
+
+static void* fill_zero_worker(void* arg) {
+    const fill_job* j = (const fill_job*)arg;
+    const uint64_t bytes = (uint64_t)j->blocks_per_pool * kvo_block_bytes(j->g);
+    const uint64_t per = (bytes + (uint64_t)j->nthreads - 1) / (uint64_t)j->nthreads;
+    const uint64_t b0 = per * (uint64_t)j->tid;
+    if (b0 < bytes) memset(j->buf + b0, 0, b0 + per < bytes ? per : bytes - b0);
+    return NULL;
+}
+
+static void* fill_rows_worker(void* arg) {
+    const fill_job* j = (const fill_job*)arg;
+    const kvo_geometry* g = j->g;
+    const uint32_t words = (uint32_t)(kvo_token_bytes(g) / 2);
+    for (int32_t i = j->tid; i < j->n; i += j->nthreads) {
+        const int32_t r = j->req[i];
+        for (int64_t t = 0; t < j->tokens[i]; ++t) {
+            const int32_t blk = j->bt[(int64_t)r * j->max_blocks + t / g->block_tokens];
+            for (int32_t kv = 0; kv < 2; ++kv) {
+                uint16_t* row = (uint16_t*)(j->buf + row_offset(g, j->blocks_per_pool, 0, blk, kv,
+                                                                (int32_t)(t % g->block_tokens)));
+                const uint64_t th = kvo_token_hash(j->seed, r, j->layer, kv, t);
+                for (uint32_t w = 0; w < words; ++w) row[w] = kvo_word(th, w);
+            }
+        }
+    }
+    return NULL;
+}
+
+static void run_fill_phase(void* (*fn)(void*), fill_job* jobs, int32_t threads) {
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+    for (int32_t t = 0; t < threads; ++t)
+        if (threads == 1 || pthread_create(&th[t], NULL, fn, &jobs[t]) != 0) fn(&jobs[t]), th[t] = 0;
+    for (int32_t t = 0; t < threads; ++t)
+        if (th[t]) pthread_join(th[t], NULL);
+    free(th);
+}
+
+void kvo_fill_layer(const kvo_geometry* g, uint64_t seed, int32_t layer, uint8_t* layer_buf,
+                    int32_t blocks_per_pool, int32_t n, const int32_t* req, const int64_t* tokens,
+                    const int32_t* bt, int32_t max_blocks, int32_t threads) {
+    if (threads < 1) threads = 1;
+    fill_job* jobs = (fill_job*)malloc(sizeof(fill_job) * (size_t)threads);
+    for (int32_t t = 0; t < threads; ++t)
+        jobs[t] = (fill_job){g, seed, layer, blocks_per_pool, n, max_blocks, t, threads, layer_buf, req, bt, tokens};
+    run_fill_phase(fill_zero_worker, jobs, threads);
+    run_fill_phase(fill_rows_worker, jobs, threads);
+    free(jobs);
+}
+
 /* Destination block rule: a wave entry must start inside the already-copied
  * prefix (lo <= synced_hi; the reference guarantees lo == synced,
  * engine.cpp:548-556,657-661).  For the entries in the order given (ascending

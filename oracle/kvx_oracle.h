@@ -103,6 +103,18 @@ void kvo_fill(const kvo_geometry* g, uint64_t seed, int32_t num_stages, const in
               uint8_t* const* pools, int32_t blocks_per_pool, int32_t n, const int32_t* req,
               const int64_t* tokens, const int32_t* bt, int32_t max_blocks);
 
+/* The expected image of ONE layer (model layer `layer`) of a block-layout
+ * pool: zero everywhere except tokens [0, tokens[i]) of each request req[i],
+ * which hold the payload, placed through bt -- i.e. kvo_fill restricted to
+ * one layer on a zeroed buffer.  Given the oracle's destination table and
+ * synced high-water marks it is the oracle's destination layer after a
+ * transition (rows never written stay zero), so a full-size pool can be
+ * compared byte for byte one layer at a time.  layer_buf holds
+ * blocks_per_pool * kvo_block_bytes(g) bytes; `threads` pthreads. */
+void kvo_fill_layer(const kvo_geometry* g, uint64_t seed, int32_t layer, uint8_t* layer_buf,
+                    int32_t blocks_per_pool, int32_t n, const int32_t* req, const int64_t* tokens,
+                    const int32_t* bt, int32_t max_blocks, int32_t threads);
+
 typedef struct kvo_dst {
     int32_t max_requests;
     int32_t max_blocks;    /* per request */

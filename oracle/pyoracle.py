@@ -65,6 +65,7 @@ def lib() -> C.CDLL:
             "kvo_ctx_begin": (I64, [P(Ctx), I32, P(I32), P(I64), P(I64), P(I64)]),
             "kvo_ctx_on_sync_complete": (I32, [P(Ctx), I32, P(I32), P(I64), I32, P(I64), P(I64), P(I64)]),
             "kvo_fill": (None, [P(Geo), U64, I32, P(I32), PP, I32, I32, P(I32), P(I64), P(I32), I32]),
+            "kvo_fill_layer": (None, [P(Geo), U64, I32, VP, I32, I32, P(I32), P(I64), P(I32), I32, I32]),
             "kvo_apply_wave": (C.c_int, [P(Geo), P(Dst), I32, P(I32), PP, I32, P(I32), I32, P(I32), PP,
                                          I32, P(I32), P(I64), P(I64)]),
             "kvo_apply_wave_mt": (C.c_int, [P(Geo), P(Dst), I32, P(I32), PP, I32, P(I32), I32, P(I32), PP,
@@ -242,6 +243,22 @@ class DataPlane:
         return int(lib().kvo_verify(C.byref(self.g), seed, C.byref(self.d), len(self.nb) + 1,
                                     _p(self.nb, C.c_int32), _pp(self.new_pools), len(req),
                                     _p(req, C.c_int32), _p(kv, C.c_int64)))
+
+
+def fill_layer(g: Geo, seed: int, layer: int, blocks_per_pool: int, req, tokens, bt: np.ndarray,
+               out: Optional[np.ndarray] = None, threads: int = 0) -> np.ndarray:
+    """kvo_fill_layer: the expected block-layout image of model layer `layer`
+    of a pool with blocks_per_pool blocks, rows [0, tokens[i]) of req[i]
+    through bt ([max_requests, max_blocks]), zeros elsewhere."""
+    req, tokens, bt = _i32(req), _i64(tokens), _i32(bt)
+    bb = 2 * g.block_tokens * g.num_kv_heads * g.head_dim * g.elem_bytes
+    if out is None:
+        out = np.empty(blocks_per_pool * bb, np.uint8)
+    assert out.nbytes == blocks_per_pool * bb and out.flags.c_contiguous
+    lib().kvo_fill_layer(C.byref(g), seed, layer, out.ctypes.data, blocks_per_pool, len(req),
+                         _p(req, C.c_int32), _p(tokens, C.c_int64), _p(bt, C.c_int32), bt.shape[-1],
+                         threads if threads > 0 else (os.cpu_count() or 1))
+    return out
 
 
 def activation_owner(old_b, new_b, from_old_stage: int) -> int:

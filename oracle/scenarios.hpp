@@ -249,6 +249,18 @@ inline std::vector<Scenario> scenarios() {
         s.forced = {{600.0, 8}};
         out.push_back(s);
     }
+    {
+        // EngineConfig::max_sync_rounds = 0 is a valid setting: wave 0 goes
+        // straight to the barrier (engine.cpp:666 never issues a delta wave).
+        Scenario s = engine_fixture({4, 8}, 4);
+        s.name = "delta_rounds_zero";
+        s.note = "max_sync_rounds=0: wave 0, then the barrier at once (no delta wave)";
+        s.kv_sync_bw = 2.0e4;
+        s.max_sync_rounds = 0;
+        s.reqs = steady(24, 2.0, 40, 200);
+        s.forced = {{150.0, 8}};
+        out.push_back(s);
+    }
     return out;
 }
 

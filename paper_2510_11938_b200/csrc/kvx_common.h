@@ -131,20 +131,30 @@ cudaError_t preload_pool_kernels();
 cudaError_t preload_extras_kernels();
 int ensure_loaded(int device);
 
-// (ring depth, chunk bytes) of the TMA bulk mover; KVX_BULK_CFG=<index> pins one.
+// (ring depth, chunk bytes, store lag, pieces per slot) of the TMA bulk
+// mover (kvx_kernels.cuh bulk_stream).  Slab-sized waves (mostly full
+// blocks) use kSlabVariant, token-granular waves (delta / final: a token's K
+// or V row per run) kTokVariant; KVX_BULK_CFG pins one variant for both,
+// KVX_BULK_CFG_SLAB / KVX_BULK_CFG_TOK one kind.
 using BulkFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, uint64_t, int32_t,
                         int32_t, int32_t);
 struct BulkVariant {
     int stages;
     uint32_t chunk;
+    int lag, pack;
     BulkFn fn;
 };
+#define KVX_BV(S, C, G, P) {S, C, G, P, kvx::kvx_bulk_kernel<S, C, G, P>}
 inline const BulkVariant kBulkVariants[] = {
-    {6, 32768, kvx::kvx_bulk_kernel<6, 32768>},  {4, 49152, kvx::kvx_bulk_kernel<4, 49152>},
-    {3, 65536, kvx::kvx_bulk_kernel<3, 65536>},  {12, 16384, kvx::kvx_bulk_kernel<12, 16384>},
-    {3, 32768, kvx::kvx_bulk_kernel<3, 32768>},  {8, 16384, kvx::kvx_bulk_kernel<8, 16384>},
-    {2, 65536, kvx::kvx_bulk_kernel<2, 65536>},  {4, 16384, kvx::kvx_bulk_kernel<4, 16384>},
+    KVX_BV(6, 32768, 2, 1),  KVX_BV(4, 49152, 2, 1),  KVX_BV(3, 65536, 2, 1),  KVX_BV(12, 16384, 2, 1),
+    KVX_BV(3, 32768, 2, 1),  KVX_BV(8, 16384, 2, 1),  KVX_BV(2, 65536, 1, 1),  KVX_BV(4, 16384, 2, 1),
+    // packed rings for token-granular waves
+    KVX_BV(6, 32768, 3, 4),  KVX_BV(12, 16384, 6, 2), KVX_BV(8, 24576, 4, 3),  KVX_BV(6, 32768, 2, 4),
+    KVX_BV(3, 32768, 1, 4),  KVX_BV(6, 16384, 3, 2),  KVX_BV(12, 16384, 4, 2), KVX_BV(4, 49152, 2, 4),
 };
+#undef KVX_BV
+constexpr int kSlabVariant = 2;  // 3 x 64 KiB, one chunk per slot
+constexpr int kTokVariant = 0;   // 6 x 32 KiB (round 1 default; sweeps in profiles/)
 constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
 
 }  // namespace kvx_host
@@ -223,8 +233,9 @@ struct kvx_transition {
     bool own_stream = true;
     int num_sms = 0;
     int move_ctas_per_sm = 1;
-    int bulk_ctas[16] = {};  // resident CTAs per SM of each bulk variant
-    int bulk_variant = -1;   // -1: chosen per wave from the average run size
+    int bulk_ctas[32] = {};  // resident CTAs per SM of each bulk variant
+    int bulk_variant_slab = kvx_host::kSlabVariant;  // ring of slab-sized waves (KVX_BULK_CFG[_SLAB])
+    int bulk_variant_tok = kvx_host::kTokVariant;    // ring of token-granular waves (KVX_BULK_CFG[_TOK])
     bool use_bulk = false;   // TMA bulk mover for local destinations
     bool peer_bulk = false;  // ... and for peer (NVLink) destinations
     bool lsu256 = false;     // LSU mover with 256-bit accesses (KVX_MOVE_IMPL=lsu256)

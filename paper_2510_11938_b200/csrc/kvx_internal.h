@@ -34,7 +34,10 @@ struct CtlState {
         target.assign((size_t)max_requests, 0);
         in_target.assign((size_t)max_requests, 0);
         target_keys.clear();
-        max_sync_rounds = max_rounds > 0 ? max_rounds : 8;
+        // kept as given: 0 is valid (wave 0, then the barrier; engine.cpp:666),
+        // and a negative cap behaves like 0 there too.  The default of 8
+        // (engine.hpp:75) lives in the callers (kvx.py, the engine's config).
+        max_sync_rounds = max_rounds;
         kv_bytes_per_token = bpt;
     }
 };

@@ -467,6 +467,7 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
             const Seg sg = segs[u - (int64_t)layer * nseg];
             const LayerPtr lp = layers[layer];
             const bool full = sg.t0 == 0 && sg.t1 == block_tokens;
+            if (sg.t1 <= sg.t0) continue;      // emptied by the plan kernel's bounds check
             if (lp.nh > 1 && !full) continue;  // head-major tail: kvx_move_any_kernel(tails_only)
             base_src = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
             base_dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
@@ -495,13 +496,13 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
         return false;
     }
     __device__ bool next(const char** s, char** d, uint32_t* n) {
-        while (left == 0) {
+        while (left == 0) {  // (load_unit never yields an empty run, so this ends)
             if (++run < nrun) {  // next (K|V, head) run of the unit
                 const uint32_t kv = (uint32_t)run / nh, h = (uint32_t)run % nh;
                 src = base_src + kv * src_kv + h * src_hs + off0;
                 dst = base_dst + kv * dst_kv + h * dst_hs + off0;
                 left = run_bytes;
-                break;
+                continue;
             }
             u += ustep;
             if (!load_unit()) return false;
@@ -519,48 +520,72 @@ struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
 
 // Generic single-thread bulk streaming loop over any chunk iterator with
 // `bool next(const char**, char**, uint32_t*)`.
-template <int kStages, uint32_t kChunk, class Iter>
+//   ring:  kStages slots of kChunk bytes; slot st completes on mbarrier st.
+//   pack:  a slot takes up to kPack consecutive pieces (each <= kChunk) while
+//          they fit, so short runs (a token's K or V row, a few KiB) do not
+//          leave most of a slot empty -- the loads of a slot complete on its
+//          mbarrier together (expect_tx = their sum), its stores form one
+//          bulk group.
+//   lag:   a slot is refilled once the store issued kLag slots earlier has
+//          read shared memory (cp.async.bulk.wait_group.read kLag-1), so up to
+//          kLag store groups drain while kStages - kLag slots load.
+// kPack = 1, kLag = 2 is the slab configuration (one 64 KiB chunk per slot).
+template <int kStages, uint32_t kChunk, int kLag = 2, int kPack = 1, class Iter>
 __device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint64_t* bars) {
+    static_assert(kLag >= 1 && kLag < kStages, "lag");
+    static_assert(kPack >= 1, "pack");
     for (int i = 0; i < kStages; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    char* pend_dst[kStages];
-    uint32_t pend_n[kStages];
+    char* pend_dst[kStages][kPack];
+    uint32_t pend_n[kStages][kPack];
+    int pend_k[kStages];
+    // one piece of look-ahead: the next piece is only taken into a slot if it fits
+    const char* ns = nullptr;
+    char* nd = nullptr;
+    uint32_t nn = 0;
+    bool have = it.next(&ns, &nd, &nn);
+    auto fill = [&](int st) -> bool {
+        if (!have) return false;
+        const char* src[kPack];
+        uint32_t used = 0, k = 0;
+        while (have && k < (uint32_t)kPack && used + nn <= kChunk) {
+            src[k] = ns;
+            pend_dst[st][k] = nd;
+            pend_n[st][k] = nn;
+            used += nn;
+            ++k;
+            have = it.next(&ns, &nd, &nn);
+        }
+        pend_k[st] = (int)k;
+        mbar_expect_tx(&bars[st], used);
+        uint32_t off = 0;
+        for (uint32_t q = 0; q < k; ++q) {
+            bulk_g2s(smem + (size_t)st * kChunk + off, src[q], pend_n[st][q], &bars[st]);
+            off += pend_n[st][q];
+        }
+        return true;
+    };
     int64_t issued = 0, stored = 0;
-    bool more = true;
-    for (int st = 0; st < kStages && more; ++st) {  // prologue: fill the ring
-        const char* s;
-        char* d;
-        uint32_t n;
-        more = it.next(&s, &d, &n);
-        if (!more) break;
-        mbar_expect_tx(&bars[st], n);
-        bulk_g2s(smem + (size_t)st * kChunk, s, n, &bars[st]);
-        pend_dst[st] = d;
-        pend_n[st] = n;
+    for (int st = 0; st < kStages; ++st) {  // prologue: fill the ring
+        if (!fill(st)) break;
         ++issued;
     }
     while (stored < issued) {
         const int st = (int)(stored % kStages);
         const uint32_t parity = (uint32_t)((stored / kStages) & 1);
         mbar_wait(&bars[st], parity);
-        bulk_s2g(pend_dst[st], smem + (size_t)st * kChunk, pend_n[st]);
+        uint32_t off = 0;
+        for (int q = 0; q < pend_k[st]; ++q) {
+            bulk_s2g(pend_dst[st][q], smem + (size_t)st * kChunk + off, pend_n[st][q]);
+            off += pend_n[st][q];
+        }
         bulk_commit();
         ++stored;
-        // refill the slot stored one iteration ago once its store has read smem
-        if (more && stored >= 2) {
-            const int rs = (int)((stored - 2) % kStages);
-            const char* s;
-            char* d;
-            uint32_t n;
-            more = it.next(&s, &d, &n);
-            if (more) {
-                bulk_wait_read<1>();
-                mbar_expect_tx(&bars[rs], n);
-                bulk_g2s(smem + (size_t)rs * kChunk, s, n, &bars[rs]);
-                pend_dst[rs] = d;
-                pend_n[rs] = n;
-                ++issued;
-            }
+        // refill the slot stored kLag slots ago once its store has read smem
+        if (have && stored >= kLag) {
+            const int rs = (int)((stored - kLag) % kStages);
+            bulk_wait_read<kLag - 1>();
+            if (fill(rs)) ++issued;
         }
     }
     bulk_wait_all();
@@ -570,7 +595,7 @@ __device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint6
 // a wave mixes them with local layers, CTAs [0, peer_ctas) stream only the
 // peer units and the rest only the local ones, so the NVLink-bound and the
 // HBM-bound traffic overlap instead of running layer after layer.
-template <int kStages, uint32_t kChunk>
+template <int kStages, uint32_t kChunk, int kLag = 2, int kPack = 1>
 __global__ void __launch_bounds__(kBulkThreads)
 kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
                 int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
@@ -606,7 +631,7 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     it.left = 0;
     it.run = 1;
     if (!it.load_unit()) return;
-    bulk_stream<kStages, kChunk>(it, smem, bars);
+    bulk_stream<kStages, kChunk, kLag, kPack>(it, smem, bars);
 }
 
 // ------------------------------------------------- generic copy list

@@ -122,11 +122,16 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         return bail(fail(KVX_ECUDA, "occupancy query"));
     t->move_ctas_per_sm = std::max(1, occ);
     {
-        // -1 = per wave: 3 x 64 KiB ring for slab-sized runs (>= 64 KiB on
-        // average, e.g. full 320 KiB 13B blocks), 6 x 32 KiB otherwise
-        // (token-sized delta / final waves).  KVX_BULK_CFG pins one variant.
-        const char* cfg = getenv("KVX_BULK_CFG");
-        t->bulk_variant = cfg ? std::max(0, std::min(kNumBulkVariants - 1, atoi(cfg))) : -1;
+        // Ring per wave kind (kvx_wave): slab waves (mostly full blocks) and
+        // token-granular waves.  KVX_BULK_CFG pins one variant for both,
+        // KVX_BULK_CFG_SLAB / _TOK one kind (sweeps).
+        static_assert(kNumBulkVariants <= (int)(sizeof(t->bulk_ctas) / sizeof(t->bulk_ctas[0])), "variants");
+        auto pick = [](const char* name, int dflt) {
+            const char* v = getenv(name);
+            return v ? std::max(0, std::min(kNumBulkVariants - 1, atoi(v))) : dflt;
+        };
+        t->bulk_variant_slab = pick("KVX_BULK_CFG_SLAB", pick("KVX_BULK_CFG", kSlabVariant));
+        t->bulk_variant_tok = pick("KVX_BULK_CFG_TOK", pick("KVX_BULK_CFG", kTokVariant));
         for (int v = 0; v < kNumBulkVariants; ++v) {
             const BulkVariant& bv = kBulkVariants[v];
             const int smem = bv.stages * (int)bv.chunk;
@@ -266,7 +271,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     // Validate against the host mirror of the destination rule.
     const int64_t B = t->g.block_tokens;
     static const bool skip_host_checks = getenv("KVX_TEST_SKIP_HOST_CHECKS") != nullptr;
-    int64_t nseg = 0, new_blocks = 0, tokens = 0;
+    int64_t nseg = 0, new_blocks = 0, tokens = 0, full_tokens = 0;
     for (int32_t i = 0; i < n; ++i) {
         const int32_t r = req[i];
         if (r < 0 || r >= t->max_requests) return fail(KVX_EINVAL, "req out of range");
@@ -282,6 +287,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         new_blocks += std::max<int64_t>(0, cdiv64(hi[i], B) - cdiv64(s, B));
         nseg += cdiv64(hi[i], B) - lo[i] / B;
         tokens += hi[i] - lo[i];
+        full_tokens += std::max<int64_t>(0, hi[i] / B - cdiv64(lo[i], B)) * B;  // tokens in whole blocks
     }
     if (t->bm ? new_blocks > t->bm->top : (int64_t)t->alloc + new_blocks > t->dst_num_blocks)
         return fail(KVX_ENOSPC, "destination pools full");
@@ -347,8 +353,13 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                 (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0);
         } else if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
-            const uint64_t run_bytes = nseg > 0 ? (uint64_t)tokens * 2ull * token_bytes(t->g) / (uint64_t)nseg : 0;
-            const int vi = t->bulk_variant >= 0 ? t->bulk_variant : (run_bytes >= 65536 ? 2 : 0);
+            // A wave is slab-sized when most of its bytes sit in whole blocks
+            // (each one contiguous run of 2 * block_tokens * token_bytes), else
+            // token-granular.  (Round 1 used the average run >= 64 KiB, which put
+            // the 70B-GQA slab waves -- 64 KiB blocks, partial tails pulling the
+            // average to 65,015 B -- on the token ring.)
+            const bool slab = 2 * full_tokens >= tokens;
+            const int vi = slab ? t->bulk_variant_slab : t->bulk_variant_tok;
             const BulkVariant& bv = kBulkVariants[vi];
             // Grid: measured on B200 across boxes (profiles/grid_cross_box/): 96
             // one-CTA-per-SM streams are the best HBM-bound grid on every chip tried
@@ -361,9 +372,9 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             // (C3 final wave: 148 -> 73.8 us, 128 -> 75.8, 96 -> 86.0;
             // profiles/grid_cross_box/grid_tok.jsonl; KVX_BULK_GRID_TOK overrides).
             constexpr int64_t kLocalGrid = 96, kLocalGridTok = 148, kPushCtas = 32, kPullCtas = 64;
-            static const int64_t grid_tok = getenv("KVX_BULK_GRID_TOK") ? atoll(getenv("KVX_BULK_GRID_TOK"))
-                                                                          : kLocalGridTok;
-            const int64_t local_grid = run_bytes >= 65536 ? kLocalGrid : grid_tok;
+            const char* gt = getenv("KVX_BULK_GRID_TOK");
+            const int64_t grid_tok = gt ? std::max<int64_t>(1, atoll(gt)) : kLocalGridTok;
+            const int64_t local_grid = slab ? kLocalGrid : grid_tok;
             int32_t peer_ctas = (int32_t)(t->n_pull_layers > 0 ? kPullCtas : kPushCtas);
             if (const char* pc = getenv("KVX_PEER_CTAS")) peer_ctas = std::max(0, atoi(pc));
             int64_t full_b = std::min<int64_t>((int64_t)t->num_sms * t->bulk_ctas[vi], local_grid);

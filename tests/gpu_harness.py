@@ -93,6 +93,28 @@ class GpuCase:
                 bad = np.nonzero(got != want)[0]
                 raise AssertionError(f"new stage {k}: {bad.size} bytes differ, first at {bad[:5]}")
 
+    def compare_bytes_by_layer(self, seed: int = SEED):
+        """Every byte of every destination pool against the oracle, one layer
+        at a time, at any size: the expected layer is kvo_fill_layer over the
+        ORACLE's destination table and synced marks (its allocation-only
+        replay of the block rule), i.e. the payload on rows [0, synced) of
+        each request and zeros everywhere else -- partial-block tails, spare
+        blocks and never-allocated blocks included.  Does not use the
+        product's own verify kernel."""
+        L = self.scn.num_layers
+        og = O.geo(L, self.g.num_kv_heads, self.g.head_dim)
+        req = np.arange(self.N, dtype=np.int32)
+        lb = self.dst_blocks * self.g.block_bytes
+        want = np.empty(lb, np.uint8)
+        for j, (b, e) in enumerate(W.stage_ranges(L, self.t.new_boundaries)):
+            for ll in range(e - b):
+                got = self.new_pools[j].read(ll * lb, lb)
+                O.fill_layer(og, seed, b + ll, self.dst_blocks, req, self.dp.synced_hi, self.dp.bt, out=want)
+                if not np.array_equal(got, want):
+                    bad = np.nonzero(got != want)[0]
+                    raise AssertionError(f"new stage {j} layer {b + ll}: {bad.size} bytes differ, "
+                                         f"first at {bad[:5]}")
+
     def compare_source(self):
         for k, p in enumerate(self.old_pools):
             np.testing.assert_array_equal(p.read(), self.dp.old_pools[k])

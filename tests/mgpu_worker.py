@@ -13,6 +13,20 @@ if ROOT not in sys.path:
 SEED = 0x77
 
 
+def device_of(rank: int) -> int:
+    """The GPU rank `rank` runs on: its own on a box with >= world GPUs, else
+    ranks fold onto the visible ones (rank % gpu_count).  CUDA IPC between two
+    processes on one device is legal, so a folded run still goes through
+    IPC export/import, the imported-pool (peer) paths of the movers, the
+    peer/local CTA split and the system fences -- only the bytes stay in one
+    HBM instead of crossing NVLink."""
+    from paper_2510_11938_b200 import kvx
+    n = kvx.device_count()
+    if n < 1:
+        raise RuntimeError("no CUDA device visible to libkvx.so")
+    return rank % n
+
+
 def _init(rank, world, port):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -96,12 +110,13 @@ def _gpu_transition(dist, rank, world, scn, t, heads, dim, mode, pull, layouts=(
         dist.all_gather_object(o, obj)
         return o
 
+    dev = device_of(rank)
     old_pools, new_pools = S.setup_rank_pools(
-        kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, rank, old_blocks,
+        kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, dev, old_blocks,
         dst_blocks, all_gather=gather, fill=(SEED, live, tokens[live], src_bt), pull=pull,
         old_layout=layouts[0], new_layout=layouts[1], layer_pull=layer_pull)
     dist.barrier()
-    tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, rank, N,
+    tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, dev, N,
                         max_blocks, dst_blocks, src_bt, epoch=t.epoch,
                         max_sync_rounds=scn.max_sync_rounds,
                         kv_bytes_per_token=scn.kv_bytes_per_token, pull=pull, layer_pull=layer_pull)
@@ -174,7 +189,8 @@ def handoff_worker(rank, world, port, out):
         from paper_2510_11938_b200 import shard as S
         from paper_2510_11938_b200 import workload as W
 
-        torch.cuda.set_device(rank)
+        dev = device_of(rank)
+        torch.cuda.set_device(dev)
         scn = W.load_golden("engine_consolidate")   # 16 -> 4, 19 in-flight micro-batches at the barrier
         t = scn.transitions[0]
         bar = next(e for e in t.events if isinstance(e, W.Barrier))
@@ -192,7 +208,7 @@ def handoff_worker(rank, world, port, out):
             return o
 
         old_pools, new_pools = S.setup_rank_pools(kvx, g, t.old_boundaries, t.new_boundaries, old_dev,
-                                                  new_dev, rank, rank, cap0, dst, all_gather=gather)
+                                                  new_dev, rank, dev, cap0, dst, all_gather=gather)
         row = 512
         cap = sum(m.tokens * row + 256 for m in bar.microbatches) + 256
         # activation arenas of the new stages: raw pools, exported to the peer
@@ -200,13 +216,13 @@ def handoff_worker(rank, world, port, out):
         arenas, mine = [None] * len(new_dev), {}
         for j, d in enumerate(new_dev):
             if d == rank:
-                arenas[j] = kvx.Pool(rank, g, 1, ablocks)
+                arenas[j] = kvx.Pool(dev, g, 1, ablocks)
                 arenas[j].zero()
                 mine[j] = arenas[j].export_ipc()
         for r, hs in enumerate(gather(mine)):
             for j, h in hs.items():
                 if r != rank:
-                    arenas[int(j)] = kvx.Pool.import_ipc(rank, h, g, 1, ablocks)
+                    arenas[int(j)] = kvx.Pool.import_ipc(dev, h, g, 1, ablocks)
 
         def payload(m):
             gen = torch.Generator(device="cpu").manual_seed(int(m.batch))
@@ -217,7 +233,7 @@ def handoff_worker(rank, world, port, out):
             local = m.after >= 0 and m.after + 1 < len(old_dev) and old_dev[m.after] == rank
             srcs.append(payload(m).cuda() if local else torch.empty(16, dtype=torch.uint8, device="cuda"))
         torch.cuda.synchronize()
-        tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, rank, N,
+        tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, dev, N,
                             max_blocks, dst, src_bt, epoch=t.epoch)
         slots = tr.handoff(row, [(m.batch, m.after, m.tokens, s.data_ptr())
                                  for m, s in zip(bar.microbatches, srcs)],
@@ -292,16 +308,17 @@ def random_worker(rank, world, port, seed, out):
             dist.all_gather_object(o, obj)
             return o
 
+        dev = device_of(rank)
         old_pools, new_pools = S.setup_rank_pools(
-            kvx, g, ob, nb, old_dev, new_dev, rank, rank, cap0, cap1, all_gather=gather,
+            kvx, g, ob, nb, old_dev, new_dev, rank, dev, cap0, cap1, all_gather=gather,
             fill=(seed, live, final[live], src_bt) if len(live) else None, pull=pull)
         for k, p in enumerate(old_pools):   # zero-filled sources where nothing is live
             if p is not None and not p.imported and not len(live):
                 p.zero()
-        bm = kvx.BlockManager(rank, cap1) if use_bm else None
+        bm = kvx.BlockManager(dev, cap1) if use_bm else None
         ref_bm = O.StackBM(cap1) if use_bm else None
         dist.barrier()
-        tr = kvx.Transition(g, ob, old_pools, nb, new_pools, rank, N, max_blocks, cap1, src_bt, epoch=1,
+        tr = kvx.Transition(g, ob, old_pools, nb, new_pools, dev, N, max_blocks, cap1, src_bt, epoch=1,
                             dst_blockmgr=bm, pull=pull)
         dp = O.DataPlane(og, ob, nb, cap0, cap1, N, max_blocks, src_bt, bm=ref_bm)
         if len(live):

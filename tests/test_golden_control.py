@@ -127,3 +127,12 @@ def test_delta_round_cap_and_convergence_pinned():
     conv = W.load_golden("delta_rounds_converge").transitions[0]
     assert [w.tokens for w in conv.waves][:3] == [990, 34, 1]
     assert [e.rounds for e in conv.events if isinstance(e, W.Barrier)] == [2]
+
+
+def test_zero_sync_rounds_pinned():
+    """EngineConfig::max_sync_rounds = 0 (engine.cpp:666): the reference
+    issues wave 0 and then goes straight to the barrier, no delta wave.  The
+    oracle keeps 0 as given (the product used to turn <= 0 into 8)."""
+    t = W.load_golden("delta_rounds_zero").transitions[0]
+    assert len(t.waves) == 2 and t.waves[-1].final and t.waves[0].rounds == 0
+    assert [e.rounds for e in t.events if isinstance(e, W.Barrier)] == [0]

@@ -70,7 +70,8 @@ def test_mt_executor_matches_per_token():
 
 
 @pytest.mark.parametrize("name", ["engine_mid_decode", "engine_consolidate", "criterion12",
-                                  "bursty_repeated", "delta_rounds_cap", "delta_rounds_converge"])
+                                  "bursty_repeated", "delta_rounds_cap", "delta_rounds_converge",
+                                  "delta_rounds_zero"])
 def test_golden_transitions_bytes(name):
     """Every golden transition, replayed through the oracle control plane and
     executed by the oracle data plane: destination bytes equal the pattern of
@@ -121,3 +122,42 @@ def test_activation_owner():
     owners = [O.activation_owner(ob, nb, s) for s in range(7)]
     assert owners == [0, 1, 1, 2, 2, 3, 3]
     assert O.activation_owner(ob, nb, 7) == -1  # last stage: nothing in transit
+
+
+@pytest.mark.parametrize("name", ["criterion12", "bursty_repeated", "delta_rounds_converge"])
+def test_fill_layer_is_the_oracle_destination(name):
+    """kvo_fill_layer (the full-size parity tests' expected image) equals the
+    oracle executor's destination pools layer by layer, zero rows included:
+    given the oracle's destination table and synced marks it regenerates
+    exactly what the per-token executor wrote."""
+    scn = W.load_golden(name)
+    L = scn.num_layers
+    for t in scn.transitions:
+        tokens = t.max_tokens(scn.num_requests)
+        max_blocks = int(max(1, (tokens.max() + 15) // 16))
+        g, dp = small_plane(L, t.old_boundaries, t.new_boundaries, tokens, max_blocks, heads=1, dim=8)
+        live = np.nonzero(tokens)[0].astype(np.int32)
+        dp.fill_source(SEED, live, tokens[live])
+        ctx = O.ControlCtx(scn.num_requests, scn.max_sync_rounds, scn.kv_bytes_per_token)
+
+        class Shim:
+            def begin(self, req, kv):
+                r = ctx.begin(req, kv)
+                assert dp.wave(req, r[1], r[2]) == 0
+                return r
+
+            def on_sync_complete(self, req, kv, inflight):
+                r = ctx.on_sync_complete(req, kv, inflight)
+                if r[0] != O.ACT_BARRIER_WAIT:
+                    assert dp.wave(req, r[2], r[3]) == 0
+                return r
+
+        for _ in replay(Shim(), t):
+            pass
+        req = np.arange(scn.num_requests, dtype=np.int32)
+        lb = dp.new_blocks * 2 * 16 * 1 * 8 * 2
+        for j, (b, e) in enumerate(W.stage_ranges(L, t.new_boundaries)):
+            for ll in range(e - b):
+                want = dp.new_pools[j][ll * lb:(ll + 1) * lb]
+                got = O.fill_layer(g, SEED, b + ll, dp.new_blocks, req, dp.synced_hi, dp.bt, threads=3)
+                np.testing.assert_array_equal(got, want)
