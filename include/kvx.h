@@ -302,7 +302,10 @@ int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_
  * new stage owning layer old_boundaries[after_stage] and resumes there
  * (same layer range semantics as stage_loads, engine.cpp:115-126); a batch
  * that has not finished any stage (after_stage < 0) is re-dispatched at new
- * stage 0 with no bytes.  Destination = a caller-provided activation arena
+ * stage 0 with no bytes; a batch that finished the LAST old stage
+ * (after_stage == K_old - 1) is not in flight any more -- its output is the
+ * pipeline's -- and gets no slot (new_stage = -1, bytes 0).  after_stage >=
+ * K_old is KVX_EINVAL.  Destination = a caller-provided activation arena
  * per new stage (device pointer, local or peer-mapped); each arena is filled
  * by a bump pointer in batch order, offsets aligned to 256 B.  Slots are
  * computed for every batch (deterministic on every rank); bytes move only
@@ -317,7 +320,7 @@ typedef struct kvx_microbatch {
 
 typedef struct kvx_handoff_slot {
     int64_t batch_id;
-    int32_t new_stage;     /* new owner */
+    int32_t new_stage;     /* new owner; -1 = finished on the old pipeline, no slot */
     int32_t resume_layer;  /* first layer the new owner runs for this batch */
     uint64_t offset;       /* byte offset in the new stage's activation arena */
     uint64_t bytes;

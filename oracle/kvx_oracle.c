@@ -483,10 +483,13 @@ int kvo_handoff_plan(int32_t old_stages, const int32_t* ob, int32_t new_stages, 
     if (new_stages > 256) return -1;
     for (int32_t k = 0; k < new_stages; ++k) bump[k] = 0;
     for (int32_t i = 0; i < n; ++i) {
-        if (after[i] < 0 || after[i] + 1 >= old_stages) {
-            /* nothing computed yet (or already past the last stage): re-dispatch */
-            new_stage[i] = 0;
-            resume_layer[i] = 0;
+        if (after[i] >= old_stages) return -1; /* no such old stage */
+        if (after[i] < 0 || after[i] + 1 == old_stages) {
+            /* < 0: nothing computed yet, re-dispatch at the new head;
+             * == K_old-1: the forward pass finished on the old pipeline,
+             * not in flight any more (engine.cpp:449-456 completes it): no slot */
+            new_stage[i] = after[i] < 0 ? 0 : -1;
+            resume_layer[i] = after[i] < 0 ? 0 : -1;
             offset[i] = 0;
             bytes[i] = 0;
             continue;

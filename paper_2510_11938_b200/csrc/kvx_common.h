@@ -95,6 +95,7 @@ inline int stage_begin(const std::vector<int32_t>& b, int s) { return s == 0 ? 0
 
 inline bool plan_ok(const kvx_plan& p, int32_t L, std::string* why, std::vector<int32_t>* out) {
     if (p.num_stages < 1 || p.num_stages > L) return *why = "num_stages out of range", false;
+    if (p.num_stages > 1 && !p.boundaries) return *why = "boundaries is null", false;
     out->assign(p.boundaries, p.boundaries + (p.num_stages - 1));
     int32_t prev = 0;
     for (int32_t b : *out) {
@@ -200,6 +201,18 @@ struct kvx_pool {
 inline kvx::PoolAddr pool_addr(const kvx_pool* p, char* const* d_layers) {
     return kvx::PoolAddr{d_layers, p->blk_stride(), p->kv_stride(), p->tok_stride(), p->head_stride(),
                          (uint32_t)p->head_bytes()};
+}
+
+// True when any layer span of `a` shares an address with one of `b`'s (both
+// mapped in this process: local or imported).  Layer spans are
+// [layer_base, layer_base + layer_bytes) in every layout.
+inline bool pools_overlap(const kvx_pool* a, const kvx_pool* b) {
+    if (!a || !b) return false;
+    const uint64_t na = a->layer_bytes(), nb = b->layer_bytes();
+    for (const char* x : a->layer_base)
+        for (const char* y : b->layer_base)
+            if (x < y + nb && y < x + na) return true;
+    return false;
 }
 
 // Device-resident block manager: a free-id stack on the GPU, its top mirrored

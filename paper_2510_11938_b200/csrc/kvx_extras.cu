@@ -51,9 +51,12 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
         sl.batch_id = mb[i].batch_id;
         if (mb[i].tokens < 0) return fail(KVX_EINVAL, "negative tokens");
         const int32_t a = mb[i].after_stage;
-        if (a < 0 || a + 1 >= k_old) {  // nothing computed yet: re-dispatch at the new head
-            sl.new_stage = 0;
-            sl.resume_layer = 0;
+        if (a >= k_old) return fail(KVX_EINVAL, "after_stage beyond the old pipeline");
+        if (a < 0 || a + 1 == k_old) {
+            // a < 0: nothing computed yet, re-dispatch at the new head;
+            // a == K_old-1: the forward pass is complete, not in flight (no slot)
+            sl.new_stage = a < 0 ? 0 : -1;
+            sl.resume_layer = a < 0 ? 0 : -1;
             sl.offset = 0;
             sl.bytes = 0;
             continue;

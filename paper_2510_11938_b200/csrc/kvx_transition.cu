@@ -69,10 +69,18 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         const int32_t layers = (k + 1 < d->old_plan.num_stages ? ob[(size_t)k] : g.num_layers) -
                                stage_begin(ob, k);
         if (p->num_layers != layers) return fail(KVX_EINVAL, "old pool layer count != stage layer range");
+        if (!p->imported && p->device != d->device) return fail(KVX_EINVAL, "local old pool on another device");
+        if (p->imported && p->device != d->device) return fail(KVX_EINVAL, "imported old pool mapped for another device");
         if (p->g.num_kv_heads != g.num_kv_heads || p->g.head_dim != g.head_dim ||
             p->g.elem_bytes != g.elem_bytes || p->g.block_tokens != g.block_tokens)
             return fail(KVX_EINVAL, "old pool geometry mismatch");
     }
+    // A destination must not alias a source: destination ids are allocated
+    // from 0 and would overwrite source blocks a later wave still reads.
+    for (int j = 0; j < d->new_plan.num_stages; ++j)
+        for (int k = 0; k < d->old_plan.num_stages; ++k)
+            if (pools_overlap(d->new_plan.pools[j], d->old_plan.pools[k]))
+                return fail(KVX_EINVAL, "a new-stage pool overlaps an old-stage pool");
     if (d->dst_blockmgr) {
         const auto* bm = static_cast<const kvx_blockmgr*>(d->dst_blockmgr);
         if (bm->device != d->device) return fail(KVX_EINVAL, "block manager lives on another device");
@@ -400,7 +408,15 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                                         (const kvx::LayerPtr*)t->d_layers, t->n_local_layers,
                                         block_bytes(t->g), token_bytes(t->g), t->g.block_tokens,
                                         t->n_peer_layers, peer_ctas));
-            if (t->head_tails) {
+            if (t->head_tails && t->max_ctas > 0) {
+                // capped wave (HBM shared with serving): the tail mover runs after the
+                // bulk mover on the same stream, so the wave never holds more than
+                // max_ctas CTAs at once
+                KVX_LAUNCHED();
+                kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
+                    t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
+                    (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 1, t->has_peer_dst ? 1 : 0);
+            } else if (t->head_tails) {
                 // head-major partial blocks (the bulk mover skips them): the row mover on a
                 // side stream forked after the plan kernel, so it runs beside the bulk
                 // mover (which holds only ~96 SMs) and joins before the wave's end event

@@ -132,3 +132,55 @@ def test_weights_validation():
     # missing new-stage buffer
     assert L.kvx_weights_migrate(0, None, 4, 16, 2, ob, ptrs, 2, ob, ptrs, None, None,
                                  C.byref(db), C.byref(hb)) == kvx.KVX_EINVAL
+
+
+def _wrap(device, addrs, num_blocks=16):
+    """A bookkeeping-only per-layer pool at fake addresses (no GPU needed)."""
+    g = kvx.geometry(4, 2, 64)
+    h = C.c_void_p()
+    ptrs = (C.c_void_p * len(addrs))(*addrs)
+    assert L.kvx_pool_wrap_layers(device, len(addrs), ptrs, num_blocks * g.block_bytes, C.byref(g), num_blocks,
+                                  kvx.LAYOUT_BLOCKS, C.byref(h)) == kvx.KVX_OK
+    return h
+
+
+def _desc_with(old, new):
+    d, keep = desc()
+    op = (C.c_void_p * 2)(*old)
+    np_ = (C.c_void_p * 2)(*new)
+    d.old_plan = kvx._Plan(2, d.old_plan.boundaries, C.cast(op, C.POINTER(C.c_void_p)))
+    d.new_plan = kvx._Plan(2, d.new_plan.boundaries, C.cast(np_, C.POINTER(C.c_void_p)))
+    return d, keep + (op, np_)
+
+
+def test_new_pool_overlapping_an_old_pool_rejected():
+    """destination ids start at 0, so a new pool aliasing an old one
+    would overwrite source blocks a later wave still reads."""
+    span = 16 * kvx.geometry(4, 2, 64).block_bytes
+    base = 1 << 32
+    old = [_wrap(0, [base, base + span]), _wrap(0, [base + 2 * span, base + 3 * span])]
+    alias = [_wrap(0, [base + 2 * span + 4096]), _wrap(0, [base + 8 * span, base + 9 * span, base + 10 * span])]
+    d, keep = _desc_with(old, alias)
+    assert begin_rc(d) == kvx.KVX_EINVAL
+    assert b"overlaps" in L.kvx_last_error()
+    for h in old + alias:
+        L.kvx_pool_destroy(h)
+
+
+def test_old_pool_on_another_device_rejected():
+    span = 16 * kvx.geometry(4, 2, 64).block_bytes
+    base = 1 << 32
+    old = [_wrap(1, [base, base + span]), _wrap(0, [base + 2 * span, base + 3 * span])]
+    new = [_wrap(0, [base + 8 * span]), _wrap(0, [base + 9 * span, base + 10 * span, base + 11 * span])]
+    d, keep = _desc_with(old, new)
+    assert begin_rc(d) == kvx.KVX_EINVAL
+    assert b"old pool on another device" in L.kvx_last_error()
+    for h in old + new:
+        L.kvx_pool_destroy(h)
+
+
+def test_null_boundaries_rejected():
+    d, keep = desc()
+    d.old_plan = kvx._Plan(2, None, d.old_plan.pools)
+    assert begin_rc(d) == kvx.KVX_EINVAL
+    assert b"boundaries is null" in L.kvx_last_error()

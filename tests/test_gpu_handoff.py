@@ -85,3 +85,25 @@ def test_handoff_mode_commits_at_the_barrier(gpu_count, name):
         assert tr.verify_pattern(SEED, bar.req, bar.kv) == 0
     finally:
         case.close()
+
+
+def test_handoff_finished_and_out_of_range(gpu_count):
+    """The product follows the oracle at the edges: a batch past the last old
+    stage gets no slot, an after_stage beyond the old pipeline is KVX_EINVAL."""
+    import torch
+    scn = W.load_golden("engine_consolidate")
+    t = scn.transitions[0]
+    case = GpuCase(scn, t, 1, 8, oracle=False)
+    try:
+        k_old = len(t.old_boundaries) + 1
+        src = torch.zeros(4 * 256, dtype=torch.uint8, device="cuda")
+        arenas = [torch.zeros(1 << 16, dtype=torch.uint8, device="cuda")
+                  for _ in range(len(t.new_boundaries) + 1)]
+        slots = case.tr.handoff(256, [(7, k_old - 1, 4, src.data_ptr()), (8, -1, 4, src.data_ptr())],
+                                [a.data_ptr() for a in arenas], [1 << 16] * len(arenas))
+        assert slots[0][1:] == (-1, -1, 0, 0) and slots[1][1:] == (0, 0, 0, 0)
+        with pytest.raises(kvx.KvxError):
+            case.tr.handoff(256, [(9, k_old, 4, src.data_ptr())], [a.data_ptr() for a in arenas],
+                            [1 << 16] * len(arenas))
+    finally:
+        case.close()

@@ -54,3 +54,16 @@ def test_plan_routes_to_owner_of_resume_layer(name, ti, t, b):
 def test_arena_overflow_rejected():
     rc, *_ = O.handoff_plan([2], [1, 3], 256, [0], [10], [0, 100, 0])
     assert rc == -1
+
+
+def test_finished_and_out_of_range_stages():
+    """after_stage == K_old-1: the batch finished the old pipeline (engine.cpp:456-458
+    completes it), so it is not in flight and gets no slot; after_stage >= K_old has
+    no old stage and is rejected."""
+    rc, ns, rl, off, by = O.handoff_plan([2], [1, 3], 256, [-1, 0, 1], [4, 4, 4], [1 << 20] * 3)
+    assert rc == 0
+    assert (ns[0], rl[0], by[0]) == (0, 0, 0)      # re-dispatched at the new head
+    assert (ns[1], rl[1], by[1]) == (1, 2, 1024)   # resumes at layer 2, owned by new stage 1
+    assert (ns[2], rl[2], by[2]) == (-1, -1, 0)    # done: no slot
+    rc, *_ = O.handoff_plan([2], [1, 3], 256, [2], [4], [1 << 20] * 3)
+    assert rc == -1
