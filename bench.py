@@ -15,15 +15,21 @@ block-table compaction).  All through the kvx C-ABI (include/kvx.h).
             host memory: kvx_begin (grant + source block table H2D), the wave
             descriptors H2D, the commit result (violations + compacted block
             table + free list) D2H, host wall clock.
-  stall_ms  barrier -> commit done (final wave + commit), engine.cpp:676-686.
+  stall     barrier -> commit (engine.cpp:676-686), three ways: device time
+            of the final wave + commit; host-observed (barrier handler call ->
+            commit result on the host); and under the reference's conditions
+            (weights migrated beside wave 0, commit at max(final wave, weights
+            ready), handoff measured / drain = the reference's simulated drain
+            + measured final wave and commit).
   roofline  dominant kernel = the TMA bulk mover (kvx_bulk_kernel) of wave 0:
             algorithmic read+write bytes / its CUDA-event duration vs
             MEASURED_PEAKS hbm_gbs (N>1: vs the HBM / NVLink bound of the
-            busiest GPU); traffic from the committed ncu capture.
+            busiest GPU); traffic = DRAM bytes of the same launch from an ncu
+            pass run by this bench (child `--traffic-probe`), N=1.
 
-`--impl reference` times the reference's CPU path for the same metric: the
-oracle restatement (oracle/kvx_oracle.c, all host threads) on a bounded
-sample, since the reference itself moves no bytes.
+`--impl reference` times the reference's CPU path for the same metric and
+config: the oracle restatement (oracle/kvx_oracle.c, all host threads) over
+the full wave plan, since the reference itself moves no bytes.
 
 Launch: python bench.py [--gpus N --steps K --warmup W]; N>1 via
 torch.distributed.run (one rank per GPU, NVLink P2P through CUDA IPC pools).
@@ -65,21 +71,108 @@ SEED = 0xB200
 METRIC = "KV-refactor GB/s (% of HBM/NVLink roofline); refactor stall ms at 1/2/4/8 B200"
 
 
-def ncu_traffic(cfg: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum of the wave-0 mover launch
-    from the newest committed ncu capture of this config (scripts/run_ncu.sh
-    -> profiles/*_traffic_<cfg>.csv), or None."""
+def source_hash() -> str:
+    """sha256 (16 hex) of the product sources: csrc/* and include/kvx.h.  An
+    ncu capture is only quoted for the build it was taken of."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2510_11938_b200", "csrc")
+    for f in sorted(os.listdir(csrc)) + ["../../include/kvx.h"]:
+        with open(os.path.join(csrc, f), "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
+
+
+def _ncu_dram(path: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes) and
+    gpu__time_duration.sum (ms) of the single launch in an ncu --csv log."""
     import csv
-    import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*bulk_traffic_{cfg}.csv")))
-    if not files:
+    total, dur = 0.0, None
+    with open(path) as f:
+        rows = [r for r in csv.reader(f) if len(r) > 14]
+    if not rows:
         return None, None
-    total = 0.0
-    with open(files[-1]) as f:
-        for row in csv.reader(f):
-            if len(row) > 14 and row[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                total += float(row[14].replace(",", ""))
-    return (total or None), os.path.relpath(files[-1], ROOT)
+    head = rows[0]
+    try:
+        im, iu, iv = head.index("Metric Name"), head.index("Metric Unit"), head.index("Metric Value")
+    except ValueError:
+        im, iu, iv = 12, 13, 14
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+             "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
+    for r in rows[1:]:
+        v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+        if r[im] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += v
+        elif r[im] == "gpu__time_duration.sum":
+            dur = v
+    return (total or None), dur
+
+
+def ncu_traffic(cfg: str, timeout_s: float = 240.0):
+    """DRAM traffic of the dominant launch (the wave-0 TMA bulk mover), taken
+    IN THIS RUN: ncu (one pass, two dram counters, --clock-control none) over
+    a child `bench.py --traffic-probe` that builds the same pools and issues
+    the same wave 0 once.  Returns (bytes or None, provenance dict)."""
+    import shutil
+    import subprocess
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    src = {"source_hash": source_hash(), "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
+           "-k regex:kvx_bulk_kernel -c 1 over `bench.py --traffic-probe` (this run, this build)"}
+    if not ncu:
+        return None, dict(src, error="ncu not found")
+    log = os.path.join("/tmp", f"kvx_traffic_{os.getpid()}.csv")
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "-k", "regex:kvx_bulk_kernel", "-c", "1", "--csv", "--log-file", log,
+           sys.executable, os.path.abspath(__file__), "--traffic-probe", "--config", cfg]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s)
+        if out.returncode != 0:
+            return None, dict(src, error=f"ncu rc={out.returncode}: {(out.stderr or out.stdout)[-300:]}")
+        traffic, dur = _ncu_dram(log)
+        return traffic, dict(src, ncu_launch_ms=dur)
+    except Exception as e:  # report, never fail the bench on it
+        return None, dict(src, error=str(e)[:300])
+    finally:
+        if os.path.exists(log):
+            os.remove(log)
+
+
+def traffic_probe(args):
+    """Child of ncu_traffic (runs under ncu): the bench's pools for the config
+    and its wave 0, once; the first kvx_bulk_kernel launch is wave 0's mover."""
+    import torch
+    from paper_2510_11938_b200 import kvx
+    torch.cuda.set_device(0)
+    plan = Plan(args.config)
+    t = plan.t
+    g = kvx.geometry(plan.L, plan.H, plan.D)
+    old_dev, new_dev = S.placement(plan.L, t.old_boundaries, t.new_boundaries, 1, "affinity")
+    old_pools, new_pools = S.setup_rank_pools(kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, 0, 0,
+                                              plan.old_blocks, plan.dst_blocks, all_gather=None, fill=None)
+    tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, 0, plan.N, plan.max_blocks,
+                        plan.dst_blocks, plan.src_bt, epoch=t.epoch)
+    w0 = t.waves[0]
+    tr.wave(w0.req, w0.lo, w0.hi)
+    tr.wait()
+    tr.close()
+    for p in old_pools + new_pools:
+        p.close()
+    return 0
+
+
+def host_cpu():
+    """(logical CPUs usable by this process, CPU model) of the host."""
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return n, model
 
 
 def peaks():
@@ -180,39 +273,174 @@ class Plan:
         self.wave0_tokens = int((w0.hi - w0.lo).clip(min=0).sum())
 
 
-def run_step(tr, t, stall_ev=None, wait=True):
-    """One transition through the reference-shaped handlers, in the order the
-    reference engine issued them (engine.cpp:637-713).  stall_ev = (start,
-    end, stream): start is recorded right before the call that issues the
-    final post-barrier wave, end after commit -- the B200 refactor stall."""
+def run_events(tr, ev, at_barrier=None, stop_at_barrier=False):
+    """Issue a transition's events after wave 0 through the reference-shaped
+    handlers, in engine order (engine.cpp:651-688): delta waves, barrier
+    waits, the final wave.  at_barrier() is called right before the handler
+    call that issues the final post-barrier wave.  stop_at_barrier: return
+    the remaining events at the first barrier / final wave instead."""
     from paper_2510_11938_b200 import kvx
-    ev = list(t.events)
-    w0 = ev.pop(0)
-    tr.begin_refactor((w0.req, w0.hi))
+    ev = list(ev)
     while ev:
-        e = ev.pop(0)
+        e = ev[0]
+        if stop_at_barrier and (isinstance(e, W.Barrier) or e.final):
+            return ev
+        ev.pop(0)
         if isinstance(e, W.Barrier):
             if e.inflight_batches > 0:
                 act, _ = tr.on_kv_sync_complete((e.req, e.kv), e.inflight_batches)
                 assert act == kvx.ACT_BARRIER_WAIT, act
                 continue
-            if stall_ev is not None:
-                stall_ev[0].record(stall_ev[2])
+            if at_barrier is not None:
+                at_barrier()
             act, _ = tr.on_kv_sync_complete((e.req, e.kv), 0)
             assert act == kvx.ACT_FINAL, act
             ev.pop(0)  # the final wave this handler just issued
         elif e.final:
-            if stall_ev is not None:
-                stall_ev[0].record(stall_ev[2])
+            if at_barrier is not None:
+                at_barrier()
             act, _ = tr.on_kv_sync_complete((e.req, e.hi), 0)
             assert act == kvx.ACT_FINAL, act
         else:
             act, _ = tr.on_kv_sync_complete((e.req, e.hi), 1)
             assert act == kvx.ACT_DELTA, act
+    return []
+
+
+def run_step(tr, t, stall_ev=None, wait=True, mark=None):
+    """One transition through the reference-shaped handlers, in the order the
+    reference engine issued them (engine.cpp:637-713).  stall_ev = (start,
+    end, stream): start is recorded right before the call that issues the
+    final post-barrier wave, end after commit -- the B200 refactor stall.
+    mark(kind) is called at the same two points ("barrier", "commit")."""
+    w0 = t.events[0]
+    tr.begin_refactor((w0.req, w0.hi))
+
+    def at_barrier():
+        if stall_ev is not None:
+            stall_ev[0].record(stall_ev[2])
+        if mark is not None:
+            mark("barrier")
+
+    run_events(tr, t.events[1:], at_barrier)
     res = tr.on_refactor_commit((t.live_req, t.live_kv), wait=wait)
     if stall_ev is not None:
         stall_ev[1].record(stall_ev[2])  # device time at which the commit result is on the host
+    if mark is not None:
+        mark("commit")
     return res
+
+
+def host_observed_stall(make, t, reps: int = 8):
+    """The stall as the engine's handlers see it on the host: from the call of
+    the barrier handler that issues the final wave (engine.cpp:676-687) --
+    after the host learnt that the earlier waves completed (kvx_wait, the
+    KvSyncComplete arrival) -- to the commit result (violations + compacted
+    block table) back on the host (engine.cpp:690-713).  Wall clock, median."""
+    out = []
+    for rep in range(reps + 1):
+        tr = make()
+        marks = {}
+
+        def mark(kind):
+            if kind == "barrier":
+                tr.wait()
+            marks[kind] = time.perf_counter()
+        run_step(tr, t, mark=mark)
+        tr.close()
+        if rep:
+            out.append((marks["commit"] - marks["barrier"]) * 1e3)
+    return statistics.median(out), min(out), max(out)
+
+
+def reference_condition_stall(make, t, plan, shape, stream, dev, reps: int = 4):
+    """The stall under the reference's own conditions (engine.cpp:614-687):
+    the new stages' weights are migrated WHILE wave 0 runs (same HBM; the
+    reference starts the loads at the grant, :621-631), and commit waits for
+    max(final wave, weights ready) (:686).  Measured on the device for two
+    barrier policies:
+      handoff  the in-flight micro-batches move to their new owners at the
+               barrier (kvx_handoff), the final wave goes out at once, commit
+               waits on the weights: barrier -> commit, all measured;
+      drain    the reference's policy: the old pipeline finishes its in-flight
+               micro-batches first.  The drain is compute this data plane does
+               not run, so its length is the reference's simulated one (barrier
+               -> final wave in the golden timeline); the rest is measured:
+               max(drain, weights left at the barrier) + final wave + commit.
+    Returns a dict (None when the plan has no barrier or weights do not fit)."""
+    import torch
+    from paper_2510_11938_b200 import kvx
+    bars = [e for e in t.events if isinstance(e, W.Barrier)]
+    fin = next((w for w in t.waves if w.final), None)
+    L = plan.L
+    params = {"llama2-13b": 26.0e9, "llama2-7b": 13.5e9, "llama2-70b": 138.0e9}[shape]
+    lb = int(params / L) // 4096 * 4096
+    if lb * L * 2 > 120e9 or fin is None:
+        return None
+    wold = [torch.empty((e - b) * lb, dtype=torch.uint8, device=dev) for b, e in W.stage_ranges(L, t.old_boundaries)]
+    wnew = [torch.empty((e - b) * lb, dtype=torch.uint8, device=dev) for b, e in W.stage_ranges(L, t.new_boundaries)]
+    wstream = torch.cuda.Stream(device=dev)
+    row = {"llama2-13b": 5120, "llama2-7b": 4096, "llama2-70b": 8192}[shape] * 2
+    bar = bars[0] if bars else None
+    mbs = bar.microbatches if bar is not None else []
+    srcs = [torch.full((max(m.tokens, 1) * row,), m.batch % 251, dtype=torch.uint8, device=dev) for m in mbs]
+    cap = sum(m.tokens * row + 256 for m in mbs) + 256
+    arenas = [torch.zeros(cap, dtype=torch.uint8, device=dev) for _ in range(len(t.new_boundaries) + 1)]
+    res = {}
+    for mode in ("handoff", "drain"):
+        rows = []
+        for rep in range(reps + 1):
+            tr = make()
+            if mode == "handoff":
+                tr.set_handoff(True)
+            torch.cuda.synchronize(dev)
+            E = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            E[0].record(stream)                       # the grant: loads and wave 0 start together
+            wstream.wait_event(E[0])
+            kvx.weights_migrate(dev, L, lb, t.old_boundaries, [x.data_ptr() for x in wold], t.new_boundaries,
+                                [x.data_ptr() for x in wnew], stream=wstream.cuda_stream)
+            E[1].record(wstream)                      # weights ready (load_ready_ms)
+            w0 = t.events[0]
+            tr.begin_refactor((w0.req, w0.hi))
+            ev = run_events(tr, t.events[1:], stop_at_barrier=True)   # delta waves before the barrier
+            E[2].record(stream)                       # the barrier: earlier waves done
+            e = ev[0]
+            if mode == "handoff" and isinstance(e, W.Barrier):
+                live = (e.req, e.kv)
+                act, _ = tr.on_kv_sync_complete(live, e.inflight_batches)
+                assert act == kvx.ACT_FINAL, act
+                if mbs:
+                    tr.handoff(row, [(m.batch, m.after, m.tokens, s_.data_ptr()) for m, s_ in zip(mbs, srcs)],
+                               [x.data_ptr() for x in arenas], [cap] * len(arenas))
+                want_v = 0
+            else:  # drain: barrier wait(s), then the final wave over the drained live set
+                run_events(tr, ev)
+                live, want_v = (t.live_req, t.live_kv), t.violations
+            E[3].record(stream)                       # final wave (+ handoff) issued
+            stream.wait_event(E[1])                   # commit at max(final, load_ready) (:686)
+            r = tr.on_refactor_commit(live)
+            E[4].record(stream)
+            torch.cuda.synchronize(dev)
+            assert r.violations == want_v, (mode, r.violations, want_v)
+            tr.close()
+            if rep:
+                rows.append((E[0].elapsed_time(E[2]), E[0].elapsed_time(E[1]), E[2].elapsed_time(E[4])))
+        med = [statistics.median(x[i] for x in rows) for i in range(3)]
+        res[mode] = {"barrier_after_grant_ms": round(med[0], 4), "weights_ready_after_grant_ms": round(med[1], 4),
+                     "barrier_to_commit_ms": round(med[2], 4)}
+    drain_sim = (fin.t_ms - bar.barrier_ms) if (bar is not None and getattr(fin, "t_ms", None) is not None) else None
+    d = res["drain"]
+    w_left = max(0.0, d["weights_ready_after_grant_ms"] - d["barrier_after_grant_ms"])
+    out = {"weights_bytes": lb * L, "weights_concurrent_with_wave0": True,
+           "handoff": dict(res["handoff"], stall_ms=res["handoff"]["barrier_to_commit_ms"]),
+           "drain": dict(d, drain_ms_reference_simulated=drain_sim,
+                         stall_ms=None if drain_sim is None else round(max(drain_sim, w_left) + d["barrier_to_commit_ms"], 4)),
+           "reference_simulated_stall_ms": t.simulated_stall_ms(),
+           "note": "reference condition (engine.cpp:614-687): weights migrated concurrently with wave 0 on the "
+                   "same HBM, commit at max(final wave, weights ready); handoff = measured barrier -> commit "
+                   "on the device; drain = the reference's simulated drain + measured final wave and commit"}
+    del wold, wnew, arenas, srcs
+    return out
 
 
 # ------------------------------------------------------------ NCCL baseline
@@ -278,24 +506,50 @@ def nccl_baseline(kvx, torch, dist, plan, g, old_pools, old_dev, new_dev, rank, 
 
 
 # -------------------------------------------------------------- CPU baseline
-def cpu_sample_run(plan: Plan, steps, warmup: int, threads: int, target_bytes: float = 2.0e9,
-                   seconds: float = 8.0):
-    """The oracle executor (oracle/kvx_oracle.c, pthreads) on a bounded sample
-    of the same transition: the first requests whose KV totals ~target_bytes.
-    steps=None: as many steps as fill ~`seconds` of CPU work (at least 2),
-    sized from the warm-up step.  Returns (GB/s, sample description, bytes
-    per step)."""
+def mem_available() -> int:
+    """MemAvailable of this host in bytes (0 when unknown)."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def cpu_run(plan: Plan, steps, warmup: int, threads: int, target_bytes=None, seconds: float = 8.0):
+    """The oracle executor (oracle/kvx_oracle.c, pthreads) over the SAME
+    transition: every live request of the plan (target_bytes=None) -- the
+    full wave plan, every byte the GPU arm moves -- or, when the host lacks
+    the memory for source + destination pools (or target_bytes is given), the
+    first requests whose KV totals ~target_bytes.  steps=None: as many steps
+    as fill ~`seconds` of CPU work (at least 2), sized from the warm-up step.
+    Returns (GB/s, sample description, bytes per step, full plan?)."""
     from oracle import pyoracle as O
     per_req = plan.tokens * plan.kv_bytes_per_token
     order = plan.live
-    csum = np.cumsum(per_req[order])
-    nsel = int(np.searchsorted(csum, target_bytes) + 1)
-    sel = np.sort(order[:max(1, nsel)])
+    g = O.geo(plan.L, plan.H, plan.D)
+    bb = 2 * 16 * plan.token_bytes
+    full = target_bytes is None
+    if full:
+        need = (plan.old_blocks + plan.dst_blocks) * plan.L * bb
+        avail = mem_available()
+        if avail and need > 0.8 * avail:
+            full, target_bytes = False, 0.3 * avail * plan.step_bytes / need
+    if full:
+        sel = np.sort(order)
+    else:
+        csum = np.cumsum(per_req[order])
+        nsel = int(np.searchsorted(csum, target_bytes) + 1)
+        sel = np.sort(order[:max(1, nsel)])
     tokens = np.zeros_like(plan.tokens)
     tokens[sel] = plan.tokens[sel]
-    src_bt, old_blocks = W.fragmented_block_table(tokens, plan.max_blocks, 16, seed=7)
+    if full:
+        src_bt, old_blocks = plan.src_bt, plan.old_blocks
+    else:
+        src_bt, old_blocks = W.fragmented_block_table(tokens, plan.max_blocks, 16, seed=7)
     dst_blocks = int(((tokens + 15) // 16).sum())
-    g = O.geo(plan.L, plan.H, plan.D)
     t = plan.t
     waves = []
     for w in t.waves:
@@ -325,10 +579,12 @@ def cpu_sample_run(plan: Plan, steps, warmup: int, threads: int, target_bytes: f
         steps = int(min(500, max(2, round(seconds / max(1e-6, min(warm))))))
     times = [one_step() for _ in range(steps)]
     gbs = step_bytes * len(times) / sum(times) / 1e9
-    desc = (f"{len(sel)} of {len(plan.live)} live requests of {plan.golden} "
-            f"({step_bytes / 1e9:.2f} GB of KV per step, real geometry), same wave plan, "
-            f"oracle run-granular memcpy on {threads} threads, {len(times)} steps")
-    return gbs, desc, step_bytes
+    what = (f"the full wave plan of {plan.golden} (all {len(sel)} live requests)" if full else
+            f"{len(sel)} of {len(plan.live)} live requests of {plan.golden} (host memory bound)")
+    desc = (f"{what}: {step_bytes / 1e9:.2f} GB of KV per step, real geometry, same wave plan and block "
+            f"tables, oracle run-granular memcpy on {threads} threads, {len(times)} steps")
+    del dp
+    return gbs, desc, step_bytes, full
 
 
 def reference_control_plane(golden: str):
@@ -348,27 +604,45 @@ def reference_control_plane(golden: str):
         return {"error": str(e)}
 
 
+def bench_config(plan: Plan, args, n_gpus: int):
+    """The `config` object of the JSON line, shared by both arms (the
+    reference arm reports the same workload keys)."""
+    t, L = plan.t, plan.L
+    old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, n_gpus, args.placement)
+    move = "pull" if args.pull else args.move
+    layer_pull = S.move_plan(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev, move)
+    return {"workload": plan.desc, "golden_wave_plan": plan.golden,
+            "bytes_per_step": plan.step_bytes, "tokens_per_step": plan.step_tokens,
+            "placement": {"mode": args.placement, "old_stage_gpu": old_dev, "new_stage_gpu": new_dev},
+            "kv_layouts": args.layouts,
+            "movers": {"policy": move, "pulled_layers": int(sum(layer_pull)),
+                       "cross_gpu_layers": sum(1 for l in range(L) if old_dev[S.stage_of(t.old_boundaries, l)]
+                                               != new_dev[S.stage_of(t.new_boundaries, l)])},
+            "l2": "inputs (17 GB) larger than L2 (126 MB); no flush needed"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     plan = Plan(args.config)
-    threads = os.cpu_count() or 1
+    threads, model = host_cpu()
     steps = args.steps
-    gbs, desc, step_bytes = cpu_sample_run(plan, steps, max(1, args.warmup), threads,
-                                           target_bytes=args.sample_gb * 1e9)
+    gbs, desc, step_bytes, full = cpu_run(plan, steps, max(1, args.warmup), threads,
+                                          target_bytes=args.sample_gb * 1e9 if args.sample_gb else None)
     ms = step_bytes / (gbs * 1e9) * 1e3
+    n_gpus = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "n_gpus": n_gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16 (u16 words)",
-        "data": "synthetic", "config": {"workload": plan.desc, "golden_wave_plan": plan.golden},
-        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": desc,
+        "data": "synthetic", "config": bench_config(plan, args, n_gpus),
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "cpu_model": model,
+                         "kind": "port", "sample": desc, "full_plan": full,
                          "reference_control_plane": reference_control_plane(plan.golden)},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference (pipesim) is a simulator that moves no bytes; its CPU path for this "
-                "metric is the oracle restatement executing the identical byte plan",
+                "metric is the oracle restatement executing the identical byte plan on all host threads",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -489,13 +763,18 @@ def main():
                          "(shard.move_plan); push = the source GPU; pull = the destination GPU")
     ap.add_argument("--pull", action="store_true", help="alias of --move pull")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--sample-gb", type=float, default=2.0,
-                    help="KV bytes per step of the CPU samples (--impl reference, cpu_baseline)")
+    ap.add_argument("--sample-gb", type=float, default=None,
+                    help="KV GB per step of the CPU runs (--impl reference, cpu_baseline); default: the "
+                         "full wave plan (falls back to a sample only when host memory is short)")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu traffic pass")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--layouts", default="blocks,blocks",
                     help="old,new pool layouts: blocks (FlashInfer NHD [blocks][2][B][H][D]), planes "
                          "(FlashAttention [2][blocks][B][H][D]) or heads (FlashInfer HND [blocks][2][H][B][D], "
                          "vLLM's FlashInfer layout on B200); unequal = the refactor converts")
     args = ap.parse_args()
+    if args.traffic_probe:
+        return traffic_probe(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "c5":
@@ -720,6 +999,19 @@ def main():
                            "to their new owners (hidden x fp16 rows), final wave over the barrier's "
                            "live set, commit; device time barrier -> commit result on host"}
 
+    # ---- the stall as the reference defines it (engine.cpp:676-686):
+    #      host-observed (handler call -> commit result on the host) and under
+    #      the reference's conditions (weights loading beside wave 0, commit at
+    #      max(final wave, weights ready), drain vs handoff)
+    h_med, h_lo, h_hi = host_observed_stall(make, t)
+    if world > 1:
+        th = torch.tensor([h_med, h_hi], dtype=torch.float64, device=dev)
+        dist.all_reduce(th, op=dist.ReduceOp.MAX)
+        h_med, h_hi = [float(x) for x in th.tolist()]
+    ref_cond = None
+    if world == 1 and not args.no_weights:
+        ref_cond = reference_condition_stall(make, t, plan, CONFIGS[args.config][1], stream, dev)
+
     # ---- stage weight migration: the new stages' parameters
     #      gathered by layer range on the device (N=1; fp16 weights of the shape)
     weights = None
@@ -791,10 +1083,9 @@ def main():
                  max(i / (nvl_peak * 1e9) for i in inn))
     if n_gpus == 1:
         achieved = w0_bytes / (w0_avg * 1e-3) / 1e9
-        traffic, traffic_src = ncu_traffic(args.config)
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "live_copy_reference": copy_ref,
-                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                "frac": round(achieved / peak, 4), "traffic": None,
                 "kernel": "kvx_bulk_kernel<3,64K> (wave 0, TMA bulk mover)", "bytes_per_launch": w0_bytes,
                 "launch_ms": round(w0_avg, 4), "peak_source": peak_kind}
     else:
@@ -823,6 +1114,13 @@ def main():
             dist.destroy_process_group()
         return 0
 
+    # ---- DRAM traffic of the dominant launch, from an ncu pass of THIS run
+    #      (pools above are freed; the child rebuilds them and issues wave 0)
+    if n_gpus == 1 and not args.no_ncu:
+        roof["traffic"], roof["traffic_source"] = ncu_traffic(args.config)
+        if roof["traffic"]:
+            roof["traffic_over_algorithmic"] = round(roof["traffic"] / w0_bytes, 4)
+
     value = plan.step_bytes * K / (dev_ms * 1e-3) / 1e9
     e2e_value = plan.step_bytes * e2e_steps / e2e_s / 1e9
     clocks = sampler.summary(wall0, wall1)
@@ -830,15 +1128,15 @@ def main():
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": n_gpus, "steps": K,
         "warmup": Wm, "ms_per_step": round(dev_ms / K, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp16 (u16 words)", "data": "synthetic",
-        "config": {"workload": plan.desc, "golden_wave_plan": plan.golden,
-                   "bytes_per_step": plan.step_bytes, "tokens_per_step": plan.step_tokens,
-                   "placement": {"mode": args.placement, "old_stage_gpu": old_dev, "new_stage_gpu": new_dev},
-                   "kv_layouts": args.layouts,
-                   "movers": {"policy": args.move, "pulled_layers": int(sum(layer_pull)),
-                              "cross_gpu_layers": sum(1 for l in range(L) if old_dev[S.stage_of(t.old_boundaries, l)]
-                                                      != new_dev[S.stage_of(t.new_boundaries, l)])},
-                   "l2": "inputs (17 GB) larger than L2 (126 MB); no flush needed"},
+        "config": bench_config(plan, args, n_gpus),
         "stall_ms": round(stall_med, 4), "stall_ms_all": [round(x, 4) for x in (stalls[0], stalls[-1])],
+        "stall": {"device_ms": round(stall_med, 4),
+                  "device_note": "final wave + commit on the device: CUDA events around the barrier handler "
+                                 "call that issues the final wave and the commit (timed loop, no host sync)",
+                  "host_observed_ms": round(h_med, 4), "host_observed_range_ms": [round(h_lo, 4), round(h_hi, 4)],
+                  "host_note": "wall clock from the barrier handler call (after the host saw the earlier waves "
+                               "complete) to the commit result on the host (engine.cpp:676-713)",
+                  "reference_condition": ref_cond},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                 "ms_per_step": round(e2e_s * 1e3 / e2e_steps, 4)},
@@ -854,11 +1152,13 @@ def main():
         line["folded_onto_gpus"] = fold
         line["not_a_measurement"] = "ranks share GPUs (KVX_BENCH_FOLD); functional check of the N-rank path"
     if n_gpus == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        gbs, desc, _ = cpu_sample_run(plan, None, 1, threads, target_bytes=args.sample_gb * 1e9, seconds=8.0)
-        gbs1, desc1, _ = cpu_sample_run(plan, None, 1, 1, target_bytes=0.5e9, seconds=3.0)
-        line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                                "sample": desc, "value_1_thread": round(gbs1, 3), "sample_1_thread": desc1,
+        threads, model = host_cpu()
+        gbs, desc, _, full = cpu_run(plan, None, 1, threads,
+                                     target_bytes=args.sample_gb * 1e9 if args.sample_gb else None, seconds=8.0)
+        gbs1, desc1, _, _ = cpu_run(plan, None, 1, 1, target_bytes=0.5e9, seconds=3.0)
+        line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "cpu_model": model,
+                                "kind": "port", "sample": desc, "full_plan": full,
+                                "value_1_thread": round(gbs1, 3), "sample_1_thread": desc1,
                                 "reference_control_plane": reference_control_plane(plan.golden)}
     print(json.dumps(line), flush=True)
     if world > 1:

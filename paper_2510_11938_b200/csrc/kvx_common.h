@@ -152,6 +152,9 @@ inline const BulkVariant kBulkVariants[] = {
     // packed rings for token-granular waves
     KVX_BV(6, 32768, 3, 4),  KVX_BV(12, 16384, 6, 2), KVX_BV(8, 24576, 4, 3),  KVX_BV(6, 32768, 2, 4),
     KVX_BV(3, 32768, 1, 4),  KVX_BV(6, 16384, 3, 2),  KVX_BV(12, 16384, 4, 2), KVX_BV(4, 49152, 2, 4),
+    // small rings: several CTAs per SM for token-granular waves (more issuing threads)
+    KVX_BV(3, 16384, 2, 1),  KVX_BV(6, 12288, 3, 1),  KVX_BV(8, 12288, 4, 1),  KVX_BV(4, 12288, 2, 1),
+    KVX_BV(4, 24576, 2, 2),  KVX_BV(2, 24576, 1, 2),
 };
 #undef KVX_BV
 constexpr int kSlabVariant = 2;  // 3 x 64 KiB, one chunk per slot

@@ -41,6 +41,7 @@ class Wave:
     hi: np.ndarray
     tokens: int
     kv_synced_bytes_total: float  # reference accumulator after this wave
+    t_ms: float = 0.0             # simulated dispatch time of the wave (KvSyncComplete / commit schedule)
 
 
 @dataclass
@@ -153,7 +154,7 @@ def load_golden(name: str, golden_dir: str = GOLDEN_DIR) -> Scenario:
         elif k == "wave":
             e = np.array(r["entries"], dtype=np.int64).reshape(-1, 3)
             w = Wave(r["wave"], r["final"], r["rounds"], e[:, 0].astype(np.int32), e[:, 1].copy(),
-                     e[:, 2].copy(), r["tokens"], r["kv_synced_bytes_total"])
+                     e[:, 2].copy(), r["tokens"], r["kv_synced_bytes_total"], r.get("t_ms", 0.0))
             cur[r["instance"]].waves.append(w)
             cur[r["instance"]].events.append(w)
             timeline.append((idx[r["instance"]], "wave", w))
