@@ -48,7 +48,8 @@
 extern "C" {
 #endif
 
-#define KVX_ABI_VERSION 3  /* 2: kvx_transition_desc.layer_pull; 3: .max_ctas */
+#define KVX_ABI_VERSION 4  /* 2: kvx_transition_desc.layer_pull; 3: .max_ctas;
+                              4: .src_block_table_dev, kvx_bm_*_async, kvx_stage_kv_bytes */
 
 #define KVX_OK 0
 #define KVX_EINVAL (-1)  /* bad argument (null, out of range, unsorted wave) */
@@ -169,6 +170,16 @@ int kvx_bm_free_count(const kvx_blockmgr* bm, int32_t* n);
 int kvx_bm_pop(kvx_blockmgr* bm, int32_t n, int32_t* ids_out);   /* host out, LIFO order */
 int kvx_bm_push(kvx_blockmgr* bm, int32_t n, const int32_t* ids);
 int kvx_bm_snapshot(const kvx_blockmgr* bm, int32_t* stack_out, int32_t* top_out);
+/* Serving-side, per decode step: the same pop / push on the caller's stream
+ * with DEVICE id arrays -- stream-ordered behind the manager's previous stack
+ * op, no host synchronisation (the free count is mirrored on the host, so
+ * KVX_ENOSPC / capacity errors are still decided synchronously).
+ * dev_ids_out[i] = the i-th pop (LIFO, as kvx_bm_pop).  A pushed id outside
+ * [0, capacity) is dropped on the device and reported (KVX_EINVAL) by the
+ * manager's next call.  (The host-array calls above wait only for the
+ * manager's own stream, never for the device.) */
+int kvx_bm_pop_async(kvx_blockmgr* bm, int32_t n, int32_t* dev_ids_out, void* stream);
+int kvx_bm_push_async(kvx_blockmgr* bm, int32_t n, const int32_t* dev_ids, void* stream);
 int kvx_bm_destroy(kvx_blockmgr* bm);
 
 /* The serving pipeline's decode appends, as test / bench emulation: the
@@ -214,6 +225,12 @@ typedef struct kvx_transition_desc {
     int32_t max_ctas;             /* optional cap on the mover's CTAs per wave (0 = the tuned grid):
                                      waves 0 / delta overlap serving, and fewer CTAs leave serving
                                      more HBM bandwidth */
+    const int32_t* src_block_table_dev; /* optional DEVICE copy of the source table (same shape), as
+                                     serving engines keep it: when non-NULL it is used instead of
+                                     src_block_table (which may then be NULL) -- copied on the
+                                     device, no host scan; ids are bounds-checked by the plan
+                                     kernel on the device (an out-of-pool id fails kvx_wait /
+                                     the commit with KVX_ECUDA, nothing out of range is touched) */
 } kvx_transition_desc;
 
 typedef struct kvx_transition kvx_transition;
@@ -225,6 +242,16 @@ typedef struct kvx_transition kvx_transition;
  * :584-619 stay the engine's).  KVX_ENOSPC maps to a refactor hold
  * (engine.cpp:563,592-593). */
 int kvx_begin(const kvx_transition_desc* d, kvx_transition** out);
+
+/* KV bytes each new stage's GPU holds for a grant of dst_num_blocks blocks
+ * per layer: out[k] = layers(k) * dst_num_blocks * 2 * block_tokens *
+ * token_bytes (pools are dense in every layout).  Host-only, no GPU.  The
+ * engine adds out[k] to stage k's binding (engine.cpp:584-619), so a KV
+ * shortfall is a refactor hold at allocation time (:592-593) instead of
+ * KVX_ENOSPC after the grant.  The reference never accounts KV
+ * (cluster.cpp:75-82 charges stage_param_bytes only). */
+int kvx_stage_kv_bytes(const kvx_geometry* g, int32_t num_stages, const int32_t* boundaries,
+                       int32_t dst_num_blocks, uint64_t* out);
 
 /* Replaces: the simulated sync charge sync_ms = tokens * bpt / kv_bw of
  * wave 0 (engine.cpp:637-647), delta waves (:665-674) and the final wave

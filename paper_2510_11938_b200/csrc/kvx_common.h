@@ -230,6 +230,13 @@ struct kvx_blockmgr {
     // issue order, which is the order the host mirror `top` assumed.
     cudaEvent_t order = nullptr;
     bool order_live = false;
+    // Host-array pop/push/snapshot/reset run on this private stream (after
+    // `order`) and wait for it alone -- never for the device -- so they do not
+    // stall behind serving kernels on other streams.
+    cudaStream_t stream = nullptr;
+    int32_t* h_stage = nullptr;  // pinned staging of host ids
+    int32_t h_stage_cap = 0;
+    int32_t* err = nullptr;      // pinned, device-mapped: a bad id pushed from the device
 };
 
 // Stack-op ordering across streams (see kvx_blockmgr::order).

@@ -188,7 +188,37 @@ int kvx_weights_migrate(int32_t device, void* stream, int32_t num_layers, uint64
     return KVX_OK;
 }
 
+}  // extern "C"
+
 // ------------------------------------------------------------ block manager
+// Every stack operation is stream-ordered behind bm->order (the previous
+// stack op, on whatever stream it ran); the host-array calls run on the
+// manager's private stream and wait for that stream alone.
+namespace {
+int bm_check_err(const kvx_blockmgr* bm) {
+    if (bm->err && *reinterpret_cast<volatile int32_t*>(bm->err))
+        return fail(KVX_EINVAL, "block manager: a device push carried an id outside [0, capacity)");
+    return KVX_OK;
+}
+cudaError_t bm_stage(kvx_blockmgr* bm, int32_t n) {  // pinned staging of >= n ids
+    if (n <= bm->h_stage_cap) return cudaSuccess;
+    kvx::Arena& A = kvx::Arena::of(bm->device);
+    if (bm->h_stage) {
+        const cudaError_t e = cudaStreamSynchronize(bm->stream);
+        if (e != cudaSuccess) return e;
+        A.host_free(bm->h_stage, sizeof(int32_t) * (size_t)bm->h_stage_cap);
+        bm->h_stage = nullptr;
+    }
+    const size_t bytes = kvx::size_class(sizeof(int32_t) * (size_t)n);
+    const cudaError_t e = A.host_alloc((void**)&bm->h_stage, bytes);
+    bm->h_stage_cap = e == cudaSuccess ? (int32_t)(bytes / sizeof(int32_t)) : 0;
+    return e;
+}
+unsigned bm_grid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, (n + 255) / 256)); }
+}  // namespace
+
+extern "C" {
+
 int kvx_bm_create(int32_t device, int32_t capacity, kvx_blockmgr** out) {
     if (!out || capacity < 1) return fail(KVX_EINVAL, "bad block manager arguments");
     *out = nullptr;
@@ -198,16 +228,18 @@ int kvx_bm_create(int32_t device, int32_t capacity, kvx_blockmgr** out) {
     auto* bm = new kvx_blockmgr;
     bm->device = device;
     bm->capacity = capacity;
-    if (cudaMalloc(&bm->d_stack, sizeof(int32_t) * (size_t)capacity) != cudaSuccess) {
+    kvx::Arena& A = kvx::Arena::of(device);
+    if (A.dev_alloc((void**)&bm->d_stack, sizeof(int32_t) * (size_t)capacity) != cudaSuccess) {
         delete bm;
         cudaGetLastError();
         return fail(KVX_ENOSPC, "block manager allocation failed");
     }
-    if (cudaEventCreateWithFlags(&bm->order, cudaEventDisableTiming) != cudaSuccess) {
-        cudaFree(bm->d_stack);
-        delete bm;
-        return fail(KVX_ECUDA, "block manager event");
+    if (cudaEventCreateWithFlags(&bm->order, cudaEventDisableTiming) != cudaSuccess ||
+        A.stream(&bm->stream) != cudaSuccess || A.host_alloc((void**)&bm->err, sizeof(int32_t)) != cudaSuccess) {
+        kvx_bm_destroy(bm);
+        return fail(KVX_ECUDA, "block manager stream / event / error word");
     }
+    *bm->err = 0;
     *out = bm;
     return kvx_bm_reset(bm);
 }
@@ -215,10 +247,12 @@ int kvx_bm_create(int32_t device, int32_t capacity, kvx_blockmgr** out) {
 int kvx_bm_reset(kvx_blockmgr* bm) {
     if (!bm) return fail(KVX_EINVAL, "block manager is null");
     DeviceGuard dg(bm->device);
-    kvx::kvx_bm_init_kernel<<<(unsigned)std::min<int64_t>(1024, (bm->capacity + 255) / 256), 256>>>(
-        bm->d_stack, bm->capacity);
+    KVX_CUDA(bm_order_before(bm, bm->stream));
+    kvx::kvx_bm_init_kernel<<<bm_grid(bm->capacity), 256, 0, bm->stream>>>(bm->d_stack, bm->capacity);
     KVX_LAUNCHED();
-    KVX_CUDA(cudaDeviceSynchronize());
+    KVX_CUDA(bm_order_after(bm, bm->stream));
+    KVX_CUDA(cudaStreamSynchronize(bm->stream));
+    *bm->err = 0;
     bm->top = bm->capacity;
     return KVX_OK;
 }
@@ -231,37 +265,82 @@ int kvx_bm_free_count(const kvx_blockmgr* bm, int32_t* n) {
 
 int kvx_bm_pop(kvx_blockmgr* bm, int32_t n, int32_t* ids_out) {
     if (!bm || n < 0 || (n > 0 && !ids_out)) return fail(KVX_EINVAL, "bad pop arguments");
+    if (const int rc = bm_check_err(bm)) return rc;
     if (n > bm->top) return fail(KVX_ENOSPC, "block manager exhausted");
     if (n == 0) return KVX_OK;
     DeviceGuard dg(bm->device);
-    std::vector<int32_t> tmp((size_t)n);
-    KVX_CUDA(cudaDeviceSynchronize());  // stack pushes queued on transition streams have landed
-    KVX_CUDA(cudaMemcpy(tmp.data(), bm->d_stack + (bm->top - n), sizeof(int32_t) * (size_t)n,
-                        cudaMemcpyDeviceToHost));
-    for (int32_t i = 0; i < n; ++i) ids_out[i] = tmp[(size_t)(n - 1 - i)];  // LIFO order
+    KVX_CUDA(bm_stage(bm, n));
+    // behind the stack's last op (pushes queued on transition streams), on the
+    // manager's own stream: no wait on unrelated streams
+    KVX_CUDA(bm_order_before(bm, bm->stream));
+    KVX_CUDA(cudaMemcpyAsync(bm->h_stage, bm->d_stack + (bm->top - n), sizeof(int32_t) * (size_t)n,
+                             cudaMemcpyDeviceToHost, bm->stream));
+    KVX_CUDA(bm_order_after(bm, bm->stream));
+    KVX_CUDA(cudaStreamSynchronize(bm->stream));
+    for (int32_t i = 0; i < n; ++i) ids_out[i] = bm->h_stage[n - 1 - i];  // LIFO order
     bm->top -= n;
     return KVX_OK;
 }
 
 int kvx_bm_push(kvx_blockmgr* bm, int32_t n, const int32_t* ids) {
     if (!bm || n < 0 || (n > 0 && !ids)) return fail(KVX_EINVAL, "bad push arguments");
+    if (const int rc = bm_check_err(bm)) return rc;
     if (bm->top + n > bm->capacity) return fail(KVX_EINVAL, "push beyond capacity (double free?)");
     for (int32_t i = 0; i < n; ++i)
         if (ids[i] < 0 || ids[i] >= bm->capacity) return fail(KVX_EINVAL, "block id out of range");
     if (n == 0) return KVX_OK;
     DeviceGuard dg(bm->device);
-    KVX_CUDA(cudaDeviceSynchronize());
-    KVX_CUDA(cudaMemcpy(bm->d_stack + bm->top, ids, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice));
+    KVX_CUDA(bm_stage(bm, n));
+    KVX_CUDA(cudaStreamSynchronize(bm->stream));  // the staging buffer's previous upload is consumed
+    std::memcpy(bm->h_stage, ids, sizeof(int32_t) * (size_t)n);
+    KVX_CUDA(bm_order_before(bm, bm->stream));
+    KVX_CUDA(cudaMemcpyAsync(bm->d_stack + bm->top, bm->h_stage, sizeof(int32_t) * (size_t)n,
+                             cudaMemcpyHostToDevice, bm->stream));
+    KVX_CUDA(bm_order_after(bm, bm->stream));
+    bm->top += n;
+    return KVX_OK;
+}
+
+int kvx_bm_pop_async(kvx_blockmgr* bm, int32_t n, int32_t* dev_ids_out, void* stream) {
+    if (!bm || n < 0 || (n > 0 && !dev_ids_out)) return fail(KVX_EINVAL, "bad pop arguments");
+    if (const int rc = bm_check_err(bm)) return rc;
+    if (n > bm->top) return fail(KVX_ENOSPC, "block manager exhausted");
+    if (n == 0) return KVX_OK;
+    DeviceGuard dg(bm->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    KVX_CUDA(bm_order_before(bm, s));
+    kvx::kvx_bm_pop_kernel<<<bm_grid(n), 256, 0, s>>>(bm->d_stack, bm->top, n, dev_ids_out);
+    KVX_LAUNCHED();
+    KVX_CUDA(bm_order_after(bm, s));
+    bm->top -= n;
+    return KVX_OK;
+}
+
+int kvx_bm_push_async(kvx_blockmgr* bm, int32_t n, const int32_t* dev_ids, void* stream) {
+    if (!bm || n < 0 || (n > 0 && !dev_ids)) return fail(KVX_EINVAL, "bad push arguments");
+    if (const int rc = bm_check_err(bm)) return rc;
+    if (bm->top + n > bm->capacity) return fail(KVX_EINVAL, "push beyond capacity (double free?)");
+    if (n == 0) return KVX_OK;
+    DeviceGuard dg(bm->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    KVX_CUDA(bm_order_before(bm, s));
+    kvx::kvx_bm_push_kernel<<<bm_grid(n), 256, 0, s>>>(bm->d_stack, bm->top, n, dev_ids, bm->capacity, bm->err);
+    KVX_LAUNCHED();
+    KVX_CUDA(bm_order_after(bm, s));
     bm->top += n;
     return KVX_OK;
 }
 
 int kvx_bm_snapshot(const kvx_blockmgr* bm, int32_t* stack_out, int32_t* top_out) {
     if (!bm) return fail(KVX_EINVAL, "block manager is null");
+    if (const int rc = bm_check_err(bm)) return rc;
     DeviceGuard dg(bm->device);
-    KVX_CUDA(cudaDeviceSynchronize());
+    auto* m = const_cast<kvx_blockmgr*>(bm);  // ordering state only; the stack is not modified
+    KVX_CUDA(bm_order_before(m, m->stream));
     if (stack_out && bm->top > 0)
-        KVX_CUDA(cudaMemcpy(stack_out, bm->d_stack, sizeof(int32_t) * (size_t)bm->top, cudaMemcpyDeviceToHost));
+        KVX_CUDA(cudaMemcpyAsync(stack_out, bm->d_stack, sizeof(int32_t) * (size_t)bm->top, cudaMemcpyDeviceToHost,
+                                 m->stream));
+    KVX_CUDA(cudaStreamSynchronize(m->stream));
     if (top_out) *top_out = bm->top;
     return KVX_OK;
 }
@@ -269,9 +348,18 @@ int kvx_bm_snapshot(const kvx_blockmgr* bm, int32_t* stack_out, int32_t* top_out
 int kvx_bm_destroy(kvx_blockmgr* bm) {
     if (!bm) return KVX_OK;
     DeviceGuard dg(bm->device);
-    cudaDeviceSynchronize();
-    cudaFree(bm->d_stack);
-    if (bm->order) cudaEventDestroy(bm->order);
+    kvx::Arena& A = kvx::Arena::of(bm->device);
+    if (bm->order) {
+        if (bm->order_live) cudaEventSynchronize(bm->order);  // the stack's last op, on any stream
+        cudaEventDestroy(bm->order);
+    }
+    if (bm->stream) {
+        cudaStreamSynchronize(bm->stream);
+        A.stream_free(bm->stream);
+    }
+    A.dev_free(bm->d_stack, sizeof(int32_t) * (size_t)bm->capacity);
+    A.host_free(bm->h_stage, sizeof(int32_t) * (size_t)bm->h_stage_cap);
+    A.host_free(bm->err, sizeof(int32_t));
     delete bm;
     return KVX_OK;
 }

@@ -207,6 +207,28 @@ static __global__ void kvx_bm_init_kernel(int32_t* __restrict__ stack, int32_t c
         stack[i] = capacity - 1 - i;
 }
 
+// Stream-ordered pop into a device array, LIFO (out[i] = stack[top-1-i], the
+// order kvx_bm_pop and the plan kernel use).
+static __global__ void kvx_bm_pop_kernel(const int32_t* __restrict__ stack, int32_t top, int32_t n,
+                                         int32_t* __restrict__ out) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = stack[top - 1 - i];
+}
+
+// Stream-ordered push of device ids: stack[top+i] = ids[i].  An id outside
+// [0, capacity) is not pushed (its slot gets -1) and raises the manager's
+// error word, reported by the next host call on the manager.
+static __global__ void kvx_bm_push_kernel(int32_t* __restrict__ stack, int32_t top, int32_t n,
+                                          const int32_t* __restrict__ ids, int32_t capacity,
+                                          int32_t* __restrict__ err) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int32_t v = ids[i];
+        const bool ok = v >= 0 && v < capacity;
+        stack[top + i] = ok ? v : -1;
+        if (!ok) *reinterpret_cast<volatile int32_t*>(err) = 1;
+    }
+}
+
 // ------------------------------------------------------------ LSU mover
 constexpr int kMoveThreads = 512;
 constexpr int kMoveUnroll = 8;

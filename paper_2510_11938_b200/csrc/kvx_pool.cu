@@ -14,6 +14,22 @@ cudaError_t preload_pool_kernels() {
 extern "C" {
 
 // ------------------------------------------------------------------ pools
+int kvx_stage_kv_bytes(const kvx_geometry* g, int32_t num_stages, const int32_t* boundaries,
+                       int32_t dst_num_blocks, uint64_t* out) {
+    std::string why;
+    if (!geometry_ok(g, &why)) return fail(KVX_EINVAL, why);
+    if (!out || dst_num_blocks < 0) return fail(KVX_EINVAL, "bad arguments");
+    kvx_pool* dummy = nullptr;
+    const kvx_plan p{num_stages, boundaries, &dummy};
+    std::vector<int32_t> b;
+    if (!plan_ok(p, g->num_layers, &why, &b)) return fail(KVX_EINVAL, why);
+    for (int k = 0; k < num_stages; ++k) {
+        const int32_t layers = (k + 1 < num_stages ? b[(size_t)k] : g->num_layers) - stage_begin(b, k);
+        out[k] = (uint64_t)layers * (uint64_t)dst_num_blocks * block_bytes(*g);
+    }
+    return KVX_OK;
+}
+
 int kvx_pool_create(int32_t device, const kvx_geometry* g, int32_t num_layers, int32_t num_blocks,
                     kvx_pool** out) {
     return kvx_pool_create_layout(device, g, num_layers, num_blocks, KVX_LAYOUT_BLOCKS, out);

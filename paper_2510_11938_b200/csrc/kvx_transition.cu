@@ -44,7 +44,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     if (d->max_requests < 1 || d->max_blocks < 1 || d->dst_num_blocks < 1)
         return fail(KVX_EINVAL, "max_requests/max_blocks/dst_num_blocks must be >= 1");
     if (d->max_ctas < 0) return fail(KVX_EINVAL, "max_ctas must be >= 0");
-    if (!d->src_block_table) return fail(KVX_EINVAL, "src_block_table is null");
+    const bool dev_table = d->src_block_table_dev != nullptr;  // serving engine's device copy
+    if (!d->src_block_table && !dev_table) return fail(KVX_EINVAL, "src_block_table is null");
     for (int k = 0; k < d->new_plan.num_stages; ++k) {
         const kvx_pool* p = d->new_plan.pools[k];
         if (!p) {
@@ -91,10 +92,11 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     int32_t min_old_blocks = INT32_MAX;
     for (int k = 0; k < d->old_plan.num_stages; ++k)
         if (d->old_plan.pools[k]) min_old_blocks = std::min(min_old_blocks, d->old_plan.pools[k]->num_blocks);
-    for (size_t c = 0; c < cells; ++c) {
-        const int32_t v = d->src_block_table[c];
-        if (v >= min_old_blocks) return fail(KVX_EINVAL, "src_block_table id beyond an old pool");
-    }
+    if (!dev_table)  // a device table is checked per segment by the plan kernel instead
+        for (size_t c = 0; c < cells; ++c) {
+            const int32_t v = d->src_block_table[c];
+            if (v >= min_old_blocks) return fail(KVX_EINVAL, "src_block_table id beyond an old pool");
+        }
 
     DeviceGuard dg(d->device);
     if (!dg.ok) return fail(KVX_ECUDA, "cudaSetDevice failed");
@@ -113,7 +115,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     t->max_ctas = d->max_ctas;
     t->epoch = d->epoch;
     t->synced_hi.assign((size_t)d->max_requests, 0);
-    t->src_bt.assign(d->src_block_table, d->src_block_table + cells);
+    if (!dev_table) t->src_bt.assign(d->src_block_table, d->src_block_table + cells);  // host mirror
     t->ctl.init(d->max_requests, d->max_sync_rounds,
                 d->kv_bytes_per_token > 0.0 ? d->kv_bytes_per_token
                                             : (double)g.num_layers * (double)block_bytes(g) /
@@ -185,8 +187,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         if (A.host_alloc((void**)&t->h_wave[s], wave_bytes) != cudaSuccess ||
             A.event(&t->h_wave_free[s], false) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "pinned staging allocation failed"));
-    if (cudaMemcpyAsync(t->d_src_bt, d->src_block_table, bt_bytes, cudaMemcpyHostToDevice, t->stream) !=
-            cudaSuccess ||
+    if (cudaMemcpyAsync(t->d_src_bt, dev_table ? d->src_block_table_dev : d->src_block_table, bt_bytes,
+                        dev_table ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, t->stream) != cudaSuccess ||
         cudaMemsetAsync(t->d_dst_bt, 0xff, bt_bytes, t->stream) != cudaSuccess ||
         cudaMemsetAsync(t->d_synced_hi, 0, sizeof(int64_t) * (size_t)d->max_requests, t->stream) !=
             cudaSuccess)
@@ -288,8 +290,9 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         const int64_t s = t->synced_hi[(size_t)r];
         if (lo[i] < 0 || lo[i] > s) return fail(KVX_EINVAL, "wave interval leaves a gap (lo > synced)");
         if (cdiv64(hi[i], B) > t->max_blocks) return fail(KVX_ENOSPC, "request exceeds max_blocks");
-        const int32_t* srow = t->src_bt.data() + (size_t)r * (size_t)t->max_blocks;
-        if (!skip_host_checks)  // test hook: lets tests/test_gpu_edges.py reach the device check
+        // (a device-resident source table has no host mirror: the plan kernel checks it)
+        const int32_t* srow = t->src_bt.empty() ? nullptr : t->src_bt.data() + (size_t)r * (size_t)t->max_blocks;
+        if (srow && !skip_host_checks)  // test hook: lets tests/test_gpu_edges.py reach the device check
             for (int64_t b = lo[i] / B; b < cdiv64(hi[i], B); ++b)
                 if (srow[b] < 0) return fail(KVX_EINVAL, "wave reads a source block the source table does not back");
         new_blocks += std::max<int64_t>(0, cdiv64(hi[i], B) - cdiv64(s, B));

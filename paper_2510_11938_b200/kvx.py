@@ -22,7 +22,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 from dataclasses import dataclass
-from typing import Optional, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -82,7 +82,7 @@ class _Desc(C.Structure):
                 ("epoch", C.c_uint64), ("max_sync_rounds", C.c_int32),
                 ("kv_bytes_per_token", C.c_double), ("stream", C.c_void_p),
                 ("dst_blockmgr", C.c_void_p), ("pull", C.c_int32), ("layer_pull", C.POINTER(C.c_uint8)),
-                ("max_ctas", C.c_int32)]
+                ("max_ctas", C.c_int32), ("src_block_table_dev", C.POINTER(C.c_int32))]
 
 
 class _CommitResult(C.Structure):
@@ -142,6 +142,9 @@ def _load() -> C.CDLL:
         "kvx_bm_pop": (C.c_int, [VP, I32, P(I32)]),
         "kvx_bm_push": (C.c_int, [VP, I32, P(I32)]),
         "kvx_bm_snapshot": (C.c_int, [VP, P(I32), P(I32)]),
+        "kvx_bm_pop_async": (C.c_int, [VP, I32, VP, VP]),
+        "kvx_bm_push_async": (C.c_int, [VP, I32, VP, VP]),
+        "kvx_stage_kv_bytes": (C.c_int, [P(Geometry), I32, P(I32), I32, P(U64)]),
         "kvx_bm_destroy": (C.c_int, [VP]),
         "kvx_begin": (C.c_int, [P(_Desc), P(VP)]),
         "kvx_wave": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(I64)]),
@@ -373,6 +376,14 @@ class BlockManager(_Handle):
         ids = _i32(ids)
         _check(_lib.kvx_bm_push(self._h, len(ids), _p32(ids)))
 
+    def pop_async(self, n: int, dev_ids_out: int, stream: int = 0) -> None:
+        """Pop n ids into a device int32 array on `stream` (no host sync)."""
+        _check(_lib.kvx_bm_pop_async(self._h, n, dev_ids_out or None, stream or None))
+
+    def push_async(self, n: int, dev_ids: int, stream: int = 0) -> None:
+        """Push n ids from a device int32 array on `stream` (no host sync)."""
+        _check(_lib.kvx_bm_push_async(self._h, n, dev_ids or None, stream or None))
+
     def snapshot(self) -> np.ndarray:
         out = np.zeros(self.capacity, np.int32)
         top = C.c_int32()
@@ -409,7 +420,8 @@ class Transition(_Handle):
                  src_block_table: np.ndarray, epoch: int = 1, max_sync_rounds: int = 8,
                  kv_bytes_per_token: float = 0.0, stream: int = 0,
                  dst_blockmgr: Optional["BlockManager"] = None, pull: bool = False,
-                 layer_pull: Optional[Sequence[int]] = None, max_ctas: int = 0):
+                 layer_pull: Optional[Sequence[int]] = None, max_ctas: int = 0,
+                 src_block_table_dev: int = 0):
         self.geom = geom
         self.max_requests, self.max_blocks = max_requests, max_blocks
         self._ob = _i32(list(old_boundaries))
@@ -418,8 +430,12 @@ class Transition(_Handle):
         self._new = list(new_pools)
         self._op = (C.c_void_p * len(self._old))(*[p.handle.value if p else None for p in self._old])
         self._np = (C.c_void_p * len(self._new))(*[p.handle.value if p else None for p in self._new])
-        src = _i32(src_block_table)
-        if src.shape != (max_requests, max_blocks):
+        # src_block_table_dev: device pointer of the same [max_requests, max_blocks]
+        # int32 table (the serving engine's copy); the host table may then be None
+        src = None if src_block_table is None else _i32(src_block_table)
+        if src is None and not src_block_table_dev:
+            raise ValueError("a source block table (host or device) is required")
+        if src is not None and src.shape != (max_requests, max_blocks):
             raise ValueError("src_block_table must be [max_requests, max_blocks]")
         d = _Desc()
         d.geometry = geom
@@ -427,7 +443,9 @@ class Transition(_Handle):
         d.new_plan = _Plan(len(self._new), _p32(self._nb), C.cast(self._np, C.POINTER(C.c_void_p)))
         d.device = device
         d.max_requests, d.max_blocks, d.dst_num_blocks = max_requests, max_blocks, dst_num_blocks
-        d.src_block_table = _p32(src)
+        d.src_block_table = _p32(src) if src is not None else None
+        if src_block_table_dev:
+            d.src_block_table_dev = C.cast(C.c_void_p(src_block_table_dev), C.POINTER(C.c_int32))
         d.epoch = epoch
         d.max_sync_rounds = max_sync_rounds
         d.kv_bytes_per_token = kv_bytes_per_token
@@ -584,6 +602,14 @@ class Transition(_Handle):
             self.close()
         except Exception:
             pass
+
+
+def stage_kv_bytes(geom: Geometry, boundaries, dst_num_blocks: int) -> List[int]:
+    """kvx_stage_kv_bytes: device KV bytes each new stage holds for a grant."""
+    b = _i32(list(boundaries))
+    out = (C.c_uint64 * (len(b) + 1))()
+    _check(_lib.kvx_stage_kv_bytes(C.byref(geom), len(b) + 1, _p32(b), dst_num_blocks, out))
+    return [int(x) for x in out]
 
 
 def weights_migrate(device: int, num_layers: int, layer_bytes: int, old_boundaries, old_ptrs,

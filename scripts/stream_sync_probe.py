@@ -1,6 +1,9 @@
 """Which operations issued on stream B wait for an unrelated busy stream A?
 Stream A runs a ~100 ms spin kernel; each op is issued on B and we time how
-long B takes to drain.  ~0 = concurrent, ~100 ms = implicit serialisation."""
+long B takes to drain.  ~0 = concurrent, ~100 ms = implicit serialisation.
+The block-manager host-array calls (kvx_bm_pop / push / snapshot / reset)
+run on the manager's own stream, so they are timed by their host call.
+Ends with one JSON line: every kvx op and whether it blocked on stream A."""
 import ctypes as C
 import glob
 import os
@@ -24,6 +27,9 @@ for p in old + new:
 torch.cuda.synchronize()
 
 
+RESULTS = {}
+
+
 def probe(name, fn):
     torch.cuda.synchronize()
     with torch.cuda.stream(sA):
@@ -33,8 +39,12 @@ def probe(name, fn):
     t1 = time.time()
     sB.synchronize()
     t2 = time.time()
+    a_busy = not sA.query()
     print(f"{name:40s} host call {1e3 * (t1 - t0):7.2f} ms   B drained after {1e3 * (t2 - t0):7.2f} ms"
-          f"   A idle at drain: {sA.query()}", flush=True)
+          f"   A idle at drain: {not a_busy}", flush=True)
+    if name.startswith("kvx"):
+        RESULTS[name] = {"host_ms": round(1e3 * (t1 - t0), 3), "drain_ms": round(1e3 * (t2 - t0), 3),
+                         "blocked_on_A": not a_busy}
 
 
 def d2d():
@@ -95,3 +105,27 @@ probe("kvx_begin (block manager)", begin(bm))
 probe("kvx_wave (block manager)", wave)
 probe("kvx_commit_async (block manager, 3 freed)", commit)
 collect(); state["t"].close()
+bm2 = kvx.BlockManager(0, cap)
+ids = torch.zeros(4, dtype=torch.int32, device="cuda")
+host_ids = {}
+probe("kvx_bm_pop (host ids)", lambda: host_ids.setdefault("v", bm2.pop(4)))
+probe("kvx_bm_push (host ids)", lambda: bm2.push(host_ids["v"]))
+probe("kvx_bm_pop_async (device ids)", lambda: bm2.pop_async(4, ids.data_ptr(), sB.cuda_stream))
+probe("kvx_bm_push_async (device ids)", lambda: bm2.push_async(4, ids.data_ptr(), sB.cuda_stream))
+probe("kvx_bm_snapshot", lambda: bm2.snapshot())
+dev_bt = torch.from_numpy(src_bt).to("cuda")
+torch.cuda.synchronize()
+
+
+def begin_dev():
+    state["t"] = kvx.Transition(g, [], old, [], new, 0, N, mb, cap, None, stream=sB.cuda_stream,
+                                src_block_table_dev=dev_bt.data_ptr())
+
+
+probe("kvx_begin (device source table)", begin_dev)
+probe("kvx_wave (device source table)", wave)
+probe("kvx_commit_async (device source table)", commit)
+collect(); state["t"].close()
+import json  # noqa: E402
+print(json.dumps({"probe": "stream_sync", "ops": RESULTS,
+                  "blocked": sorted(k for k, v in RESULTS.items() if v["blocked_on_A"])}), flush=True)

@@ -13,7 +13,7 @@ SEED = 0x5EED
 
 class GpuCase:
     def __init__(self, scn, t, heads, dim, device=0, oracle=True, oracle_pools=True, slack=0.25,
-                 dst_blocks=None):
+                 dst_blocks=None, dev_table=False):
         L = scn.num_layers
         self.scn, self.t = scn, t
         self.g = kvx.geometry(L, heads, dim)
@@ -36,10 +36,17 @@ class GpuCase:
             p = kvx.Pool(device, self.g, e - b, self.dst_blocks)
             p.zero()
             self.new_pools.append(p)
+        self.dev_bt = None
+        if dev_table:  # the serving engine's device-resident copy; no host table passed
+            import torch
+            self.dev_bt = torch.from_numpy(np.ascontiguousarray(self.src_bt, np.int32)).to(f"cuda:{device}")
+            torch.cuda.synchronize(device)
         self.tr = kvx.Transition(self.g, t.old_boundaries, self.old_pools, t.new_boundaries,
                                  self.new_pools, device, self.N, self.max_blocks, self.dst_blocks,
-                                 self.src_bt, epoch=t.epoch, max_sync_rounds=scn.max_sync_rounds,
-                                 kv_bytes_per_token=scn.kv_bytes_per_token)
+                                 None if dev_table else self.src_bt, epoch=t.epoch,
+                                 max_sync_rounds=scn.max_sync_rounds,
+                                 kv_bytes_per_token=scn.kv_bytes_per_token,
+                                 src_block_table_dev=self.dev_bt.data_ptr() if dev_table else 0)
         self.dp = None
         if oracle:
             og = O.geo(L, heads, dim)

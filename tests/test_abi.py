@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(kvx.LIB_PATH)
     missing = [n for n in declared() if not hasattr(lib, n)]
     assert not missing, missing
-    assert kvx.lib().kvx_abi_version() == 3
+    assert kvx.lib().kvx_abi_version() == 4
 
 
 def test_library_is_sm100a():

@@ -184,3 +184,30 @@ def test_null_boundaries_rejected():
     d.old_plan = kvx._Plan(2, None, d.old_plan.pools)
     assert begin_rc(d) == kvx.KVX_EINVAL
     assert b"boundaries is null" in L.kvx_last_error()
+
+
+def test_stage_kv_bytes_host_only():
+    """kvx_stage_kv_bytes (no GPU): per new stage, layers x blocks x block bytes --
+    what the engine adds to the grant's binding (engine.cpp:584-619)."""
+    g = kvx.geometry(40, 40, 128)                 # Llama-2-13B: 320 KiB per layer-block
+    out = kvx.stage_kv_bytes(g, [10, 20, 30], 1300)
+    assert out == [10 * 1300 * 327680] * 4
+    assert kvx.stage_kv_bytes(g, [5], 7) == [5 * 7 * 327680, 35 * 7 * 327680]
+    with pytest.raises(kvx.KvxError):
+        kvx.stage_kv_bytes(g, [30, 20], 4)        # not increasing
+    with pytest.raises(kvx.KvxError):
+        kvx.stage_kv_bytes(kvx.geometry(4, 1, 4), [2], 4)   # token_bytes 8
+
+
+def test_begin_accepts_a_device_table_without_a_host_one():
+    """ABI 4: src_block_table may be NULL when src_block_table_dev is given; without
+    either, kvx_begin rejects the descriptor."""
+    d, keep = desc()
+    d.src_block_table = None
+    assert begin_rc(d) == kvx.KVX_EINVAL
+    assert b"src_block_table is null" in L.kvx_last_error()
+    d, keep = desc()
+    d.src_block_table = None
+    d.src_block_table_dev = C.cast(C.c_void_p(0x1000), C.POINTER(C.c_int32))
+    assert begin_rc(d) == kvx.KVX_EINVAL                # fails later (no pools), not on the table
+    assert b"src_block_table" not in L.kvx_last_error()
