@@ -1,0 +1,100 @@
+"""The reference engine with kvx in its own transition handlers
+(integration/engine_kvx.patch, built by integration/Makefile from a scratch
+copy of /root/reference/proj):
+
+  * CPU: the patch applies to the reference as shipped, and with PIPESIM_KVX
+    unset the patched engine IS the reference -- its own 104 unit tests and
+    12 acceptance criteria pass unchanged;
+  * GPU: the same unmodified test sources with PIPESIM_KVX=parity (every
+    wave / commit / abort moves real paged KV through libkvx.so), the plane's
+    report proving the data plane ran: device Eq. 10 == host Eq. 10 at every
+    commit, every live destination word == the payload; and the patched-engine
+    cases of tests/native/test_kvx_patched.cpp (measured-time scheduling, the
+    KV hold at the grant).
+"""
+import json
+import os
+import shutil
+import subprocess
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+B = os.path.join(ROOT, "integration", "_build")
+REF = "/root/reference/proj"
+
+
+def _bin(name):
+    path = os.path.join(B, name)
+    assert os.path.exists(path), f"{path} missing: build it with __graft_entry__.build() (needs the reference)"
+    return path
+
+
+def _run(name, env_extra=None, timeout=1800):
+    env = dict(os.environ)
+    env.pop("PIPESIM_KVX", None)
+    env.update(env_extra or {})
+    return subprocess.run([_bin(name)], capture_output=True, text=True, timeout=timeout, env=env, cwd=B)
+
+
+def _report(path):
+    with open(path) as f:
+        lines = [json.loads(l) for l in f if l.strip()]
+    assert lines, "the kvx plane wrote no report"
+    return lines[-1]
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="needs /root/reference (build container)")
+def test_patch_applies_to_the_reference():
+    with tempfile.TemporaryDirectory() as d:
+        shutil.copytree(os.path.join(REF, "src"), os.path.join(d, "src"))
+        shutil.copytree(os.path.join(REF, "include"), os.path.join(d, "include"))
+        out = subprocess.run(["patch", "--dry-run", "-p2", "-i", os.path.join(ROOT, "integration", "engine_kvx.patch")],
+                             cwd=d, capture_output=True, text=True)
+        assert out.returncode == 0, out.stdout + out.stderr
+
+
+def test_patched_engine_without_kvx_is_the_reference():
+    out = _run("unit_tests_kvx")
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "104 passed | 0 failed" in out.stdout
+
+
+def test_patched_engine_without_kvx_passes_acceptance():
+    out = _run("acceptance_kvx")
+    assert out.returncode == 0, out.stdout[-3000:]
+    assert "ALL CRITERIA PASS" in out.stdout
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_with_kvx_live(gpu_count, tmp_path):
+    rep = str(tmp_path / "unit.jsonl")
+    out = _run("unit_tests_kvx", {"PIPESIM_KVX": "parity", "PIPESIM_KVX_REPORT": rep})
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "104 passed | 0 failed" in out.stdout
+    r = _report(rep)
+    assert r["mode"] == "parity" and r["engines"] > 0
+    assert r["transitions"] >= 4 and r["commits"] >= 3 and r["aborts"] >= 1   # test_engine.cpp:194-263
+    assert r["waves"] > 0 and r["tokens"] > 0 and r["kvx_launches"] > 0
+    assert r["violation_mismatches"] == 0 and r["violations_device"] == r["violations_host"]
+    assert r["mismatched_words"] == 0 and r["verified_tokens"] > 0
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_with_kvx_live(gpu_count, tmp_path):
+    rep = str(tmp_path / "acc.jsonl")
+    out = _run("acceptance_kvx", {"PIPESIM_KVX": "parity", "PIPESIM_KVX_REPORT": rep}, timeout=3000)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    assert "ALL CRITERIA PASS" in out.stdout
+    r = _report(rep)
+    assert r["commits"] >= 2 and r["waves"] > 0 and r["tokens"] > 0
+    assert r["violation_mismatches"] == 0 and r["violations_device"] == r["violations_host"]
+    assert r["mismatched_words"] == 0
+
+
+@pytest.mark.gpu
+def test_patched_engine_cases(gpu_count):
+    out = _run("test_kvx_patched")
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    assert "4 passed | 0 failed" in out.stdout
