@@ -532,11 +532,13 @@ def cpu_run(plan: Plan, steps, warmup: int, threads: int, target_bytes=None, sec
     g = O.geo(plan.L, plan.H, plan.D)
     bb = 2 * 16 * plan.token_bytes
     full = target_bytes is None
+    why = "sample"
     if full:
         need = (plan.old_blocks + plan.dst_blocks) * plan.L * bb
         avail = mem_available()
         if avail and need > 0.8 * avail:
             full, target_bytes = False, 0.3 * avail * plan.step_bytes / need
+            why = "host memory bound"
     if full:
         sel = np.sort(order)
     else:
@@ -580,7 +582,7 @@ def cpu_run(plan: Plan, steps, warmup: int, threads: int, target_bytes=None, sec
     times = [one_step() for _ in range(steps)]
     gbs = step_bytes * len(times) / sum(times) / 1e9
     what = (f"the full wave plan of {plan.golden} (all {len(sel)} live requests)" if full else
-            f"{len(sel)} of {len(plan.live)} live requests of {plan.golden} (host memory bound)")
+            f"{len(sel)} of {len(plan.live)} live requests of {plan.golden} ({why})")
     desc = (f"{what}: {step_bytes / 1e9:.2f} GB of KV per step, real geometry, same wave plan and block "
             f"tables, oracle run-granular memcpy on {threads} threads, {len(times)} steps")
     del dp

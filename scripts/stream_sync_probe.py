@@ -7,8 +7,10 @@ Ends with one JSON line: every kvx op and whether it blocked on stream A."""
 import ctypes as C
 import glob
 import os
+import sys
 import time
 import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2510_11938_b200 import kvx
 
