@@ -150,10 +150,14 @@ def traffic_probe(args):
     old_pools, new_pools = S.setup_rank_pools(kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, 0, 0,
                                               plan.old_blocks, plan.dst_blocks, all_gather=None, fill=None)
     tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, 0, plan.N, plan.max_blocks,
-                        plan.dst_blocks, plan.src_bt, epoch=t.epoch)
-    w0 = t.waves[0]
-    tr.wave(w0.req, w0.lo, w0.hi)
-    tr.wait()
+                        plan.dst_blocks, plan.src_bt, epoch=t.epoch, max_sync_rounds=plan.scn.max_sync_rounds,
+                        kv_bytes_per_token=plan.kv_bytes_per_token)
+    if args.probe_all_waves:  # every wave + commit (ncu -s k picks the k-th mover launch)
+        run_step(tr, t)
+    else:
+        w0 = t.waves[0]
+        tr.wave(w0.req, w0.lo, w0.hi)
+        tr.wait()
     tr.close()
     for p in old_pools + new_pools:
         p.close()
@@ -770,6 +774,7 @@ def main():
                          "full wave plan (falls back to a sample only when host memory is short)")
     ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu traffic pass")
     ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--probe-all-waves", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--layouts", default="blocks,blocks",
                     help="old,new pool layouts: blocks (FlashInfer NHD [blocks][2][B][H][D]), planes "
                          "(FlashAttention [2][blocks][B][H][D]) or heads (FlashInfer HND [blocks][2][H][B][D], "

@@ -49,7 +49,8 @@ extern "C" {
 #endif
 
 #define KVX_ABI_VERSION 4  /* 2: kvx_transition_desc.layer_pull; 3: .max_ctas;
-                              4: .src_block_table_dev, kvx_bm_*_async, kvx_stage_kv_bytes */
+                              4: .src_block_table_dev, kvx_bm_*_async, kvx_stage_kv_bytes,
+                                 kvx_src_rows */
 
 #define KVX_OK 0
 #define KVX_EINVAL (-1)  /* bad argument (null, out of range, unsorted wave) */
@@ -264,6 +265,14 @@ int kvx_stage_kv_bytes(const kvx_geometry* g, int32_t num_stages, const int32_t*
  * device kernels on the handle's stream. */
 int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req,
              const int64_t* lo, const int64_t* hi);
+/* Serving-side growth of the source block table during a transition: rows
+ * req[i] become rows[i * max_blocks .. +max_blocks) (host arrays), stream-
+ * ordered before the next wave.  A serving engine appends blocks as decode
+ * grows a request, or admits new requests, while the refactor runs
+ * (engine.cpp:267,494-499); the grant's table only covers what existed then.
+ * Ids must lie in the old pools; a block id already set in the row must not
+ * change (an earlier wave may have read it) -- both KVX_EINVAL. */
+int kvx_src_rows(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, const int32_t* rows);
 /* Blocks until every enqueued wave finished; *measured_ms = device time of
  * the waves since the previous wait (CUDA events on the handle's stream).
  * Replaces: the modelled arrival of KvSyncComplete (engine.cpp:646,651). */

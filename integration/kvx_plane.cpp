@@ -117,6 +117,7 @@ struct Xfer {
 
 struct KvxPlane::Impl {
     bool measured = false;
+    bool trace = std::getenv("PIPESIM_KVX_TRACE") != nullptr;  // one stderr line per plane call
     int device = 0;
     std::string geom_spec = "auto";
     int num_layers = 0;
@@ -244,6 +245,9 @@ struct KvxPlane::Impl {
             dst_need += std::max<std::int64_t>(0, cdiv(w.hi[i], kBlockTokens) - cdiv(x.synced[(std::size_t)r], kBlockTokens));
         }
         if (src_need > (std::int64_t)x.src_free.size() || x.dst_alloc + dst_need > x.dst_cap) grow(x, src_need, dst_need);
+        // requests the grant's table did not cover (admitted, or first read, after
+        // it): their rows go to the device table with kvx_src_rows
+        std::vector<std::int32_t> new_req, new_rows;
         for (std::size_t i = 0; i < w.req.size(); ++i) {
             const std::int32_t r = w.req[i];
             if (w.hi[i] <= w.lo[i] || x.src_bt[(std::size_t)r * max_blocks] >= 0) continue;
@@ -252,7 +256,12 @@ struct KvxPlane::Impl {
                 x.src_bt[(std::size_t)r * max_blocks + (std::size_t)b] = x.src_free.back();
                 x.src_free.pop_back();
             }
+            new_req.push_back(r);
+            new_rows.insert(new_rows.end(), x.src_bt.begin() + (std::ptrdiff_t)r * max_blocks,
+                            x.src_bt.begin() + (std::ptrdiff_t)(r + 1) * max_blocks);
         }
+        if (!new_req.empty())
+            KVX_OR_DIE(kvx_src_rows(x.t, x.epoch, (std::int32_t)new_req.size(), new_req.data(), new_rows.data()));
     }
     void grow(Xfer& x, std::int64_t src_need, std::int64_t dst_need) {
         const std::int32_t old_src = x.src_cap;
@@ -361,6 +370,10 @@ std::vector<double> KvxPlane::grant_kv_bytes(const std::vector<int>& new_boundar
 void KvxPlane::begin(std::int64_t instance, std::uint64_t epoch, const std::vector<int>& old_boundaries,
                      const std::vector<int>& new_boundaries, int num_layers) {
     Impl& I = *impl_;
+    if (I.trace)
+        std::fprintf(stderr, "kvx-plane begin inst=%lld epoch=%llu K %zu->%zu blocks=%lld\n", (long long)instance,
+                     (unsigned long long)epoch, old_boundaries.size() + 1, new_boundaries.size() + 1,
+                     (long long)I.pending_blocks);
     if (num_layers != I.num_layers) throw InvalidSpecError("kvx: layer count changed");
     auto it = I.active.find(instance);
     if (it != I.active.end()) {  // a previous transition of this instance never ended (engine reset)
@@ -396,7 +409,12 @@ void KvxPlane::begin(std::int64_t instance, std::uint64_t epoch, const std::vect
 double KvxPlane::wave(std::int64_t instance, std::uint64_t epoch, const std::map<std::int32_t, std::int64_t>& sync_target,
                       const std::map<std::int32_t, std::int64_t>& synced_tokens, double modelled_ms, double now_ms) {
     Impl& I = *impl_;
-    Xfer& x = I.active.at(instance);
+    if (I.trace)
+        std::fprintf(stderr, "kvx-plane wave inst=%lld epoch=%llu entries=%zu now=%.3f\n", (long long)instance,
+                     (unsigned long long)epoch, sync_target.size(), now_ms);
+    auto xit = I.active.find(instance);
+    if (xit == I.active.end()) throw InvalidSpecError("kvx: wave without a transition");
+    Xfer& x = xit->second;
     Xfer::Wave w;
     std::int64_t tokens = 0;
     for (const auto& [r, target] : sync_target) {  // std::map: ascending request ids (engine.hpp:153-154)
@@ -437,6 +455,9 @@ double KvxPlane::wave(std::int64_t instance, std::uint64_t epoch, const std::map
 void KvxPlane::commit(std::int64_t instance, std::uint64_t epoch, const std::vector<std::int32_t>& live_req,
                       const std::vector<std::int64_t>& live_kv, std::int64_t host_violations) {
     Impl& I = *impl_;
+    if (I.trace)
+        std::fprintf(stderr, "kvx-plane commit inst=%lld epoch=%llu live=%zu\n", (long long)instance,
+                     (unsigned long long)epoch, live_req.size());
     auto it = I.active.find(instance);
     if (it == I.active.end()) throw InvalidSpecError("kvx: commit without a transition");
     Xfer& x = it->second;
@@ -477,6 +498,7 @@ void KvxPlane::commit(std::int64_t instance, std::uint64_t epoch, const std::vec
 
 void KvxPlane::abort(std::int64_t instance) {
     Impl& I = *impl_;
+    if (I.trace) std::fprintf(stderr, "kvx-plane abort inst=%lld\n", (long long)instance);
     auto it = I.active.find(instance);
     if (it == I.active.end()) return;
     KVX_OR_DIE(kvx_abort(it->second.t));

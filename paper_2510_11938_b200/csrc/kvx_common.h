@@ -320,6 +320,11 @@ struct kvx_transition {
     int64_t piece_cap = 0;
     cudaEvent_t pieces_free = nullptr;
 
+    // kvx_src_rows staging (pinned, read by kvx_rows_kernel) and its reuse event
+    int32_t* h_rows = nullptr;
+    size_t h_rows_bytes = 0;
+    cudaEvent_t rows_free = nullptr;
+
     // host mirror of the destination rule (capacity checks are synchronous)
     std::vector<int64_t> synced_hi;
     std::vector<int32_t> src_bt;  // host copy: every wave's source blocks must be backed

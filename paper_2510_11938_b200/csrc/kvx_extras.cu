@@ -28,8 +28,13 @@ cudaError_t preload_extras_kernels() {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kWeightSlabStages * (int)kWeightSlabChunk)) != cudaSuccess)
         return e;
+    // every block-manager kernel: a lazily loaded one would wait for the
+    // serving kernels running at its first launch
     cudaFuncAttributes a;
-    return cudaFuncGetAttributes(&a, (const void*)kvx::kvx_bm_init_kernel);
+    for (const void* fn : {(const void*)kvx::kvx_bm_init_kernel, (const void*)kvx::kvx_bm_pop_kernel,
+                           (const void*)kvx::kvx_bm_push_kernel})
+        if ((e = cudaFuncGetAttributes(&a, fn)) != cudaSuccess) return e;
+    return cudaSuccess;
 }
 }  // namespace kvx_host
 

@@ -229,6 +229,15 @@ static __global__ void kvx_bm_push_kernel(int32_t* __restrict__ stack, int32_t t
     }
 }
 
+// Source-table rows replaced mid-transition (kvx_src_rows): table[req[i]] =
+// rows[i], read straight from the pinned staging (zero-copy).
+static __global__ void kvx_rows_kernel(const int32_t* __restrict__ req, const int32_t* __restrict__ rows, int32_t n,
+                                       int32_t max_blocks, int32_t* __restrict__ table) {
+    for (int32_t i = blockIdx.x; i < n; i += gridDim.x)
+        for (int32_t b = threadIdx.x; b < max_blocks; b += blockDim.x)
+            table[(int64_t)req[i] * max_blocks + b] = rows[(int64_t)i * max_blocks + b];
+}
+
 // ------------------------------------------------------------ LSU mover
 constexpr int kMoveThreads = 512;
 constexpr int kMoveUnroll = 8;

@@ -17,6 +17,7 @@ cudaError_t preload_transition_kernels() {
     cudaFuncAttributes a;
     cudaError_t e = cudaSuccess;
     for (const void* fn : {(const void*)kvx::kvx_plan_kernel, (const void*)kvx::kvx_move_kernel,
+                           (const void*)kvx::kvx_rows_kernel,
                            (const void*)kvx::kvx_move_any_kernel,
                            (const void*)kvx::kvx_move256_kernel, (const void*)kvx::kvx_commit_kernel,
                            (const void*)kvx::kvx_verify_kernel})
@@ -454,6 +455,49 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     return KVX_OK;
 }
 
+int kvx_src_rows(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, const int32_t* rows) {
+    if (!t) return fail(KVX_EINVAL, "transition is null");
+    if (epoch != t->epoch) return fail(KVX_ESTALE, "stale epoch");
+    if (t->state != kvx_transition::kActive) return fail(KVX_ESTATE, "transition is not active");
+    if (n < 0 || n > t->max_requests || (n > 0 && (!req || !rows))) return fail(KVX_EINVAL, "bad row arrays");
+    if (n == 0) return KVX_OK;
+    const size_t mb = (size_t)t->max_blocks;
+    for (int32_t i = 0; i < n; ++i) {
+        if (req[i] < 0 || req[i] >= t->max_requests) return fail(KVX_EINVAL, "req out of range");
+        for (size_t b = 0; b < mb; ++b) {
+            const int32_t v = rows[(size_t)i * mb + b];
+            if (v >= t->src_cap) return fail(KVX_EINVAL, "src_block_table id beyond an old pool");
+            if (!t->src_bt.empty()) {  // host mirror (host-table grants): blocks already set stay put
+                const int32_t old = t->src_bt[(size_t)req[i] * mb + b];
+                if (old >= 0 && v != old)
+                    return fail(KVX_EINVAL, "a source block an earlier wave may have read was remapped");
+            }
+        }
+    }
+    DeviceGuard dg(t->device);
+    kvx::Arena& A = kvx::Arena::of(t->device);
+    const size_t bytes = sizeof(int32_t) * ((size_t)n + (size_t)n * mb);
+    if (!t->rows_free) KVX_CUDA(A.event(&t->rows_free, false));
+    KVX_CUDA(cudaEventSynchronize(t->rows_free));  // the previous update's staging was consumed
+    if (bytes > t->h_rows_bytes) {
+        A.host_free(t->h_rows, t->h_rows_bytes);
+        t->h_rows = nullptr;
+        const size_t cap = kvx::size_class(bytes);
+        KVX_CUDA(A.host_alloc((void**)&t->h_rows, cap));
+        t->h_rows_bytes = cap;
+    }
+    std::memcpy(t->h_rows, req, sizeof(int32_t) * (size_t)n);
+    std::memcpy(t->h_rows + n, rows, sizeof(int32_t) * (size_t)n * mb);
+    kvx::kvx_rows_kernel<<<(unsigned)std::min<int32_t>(n, 1024), 128, 0, t->stream>>>(
+        t->h_rows, t->h_rows + n, n, t->max_blocks, t->d_src_bt);
+    KVX_LAUNCHED();
+    KVX_CUDA(cudaEventRecord(t->rows_free, t->stream));
+    if (!t->src_bt.empty())
+        for (int32_t i = 0; i < n; ++i)
+            std::memcpy(t->src_bt.data() + (size_t)req[i] * mb, rows + (size_t)i * mb, sizeof(int32_t) * mb);
+    return KVX_OK;
+}
+
 int kvx_wait(kvx_transition* t, uint64_t epoch, double* measured_ms) {
     if (!t) return fail(KVX_EINVAL, "transition is null");
     if (epoch != t->epoch) return fail(KVX_ESTALE, "stale epoch");
@@ -655,6 +699,8 @@ int kvx_destroy(kvx_transition* t) {
     A.dev_free(t->d_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
     A.host_free(t->h_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
     A.event_free(t->pieces_free, false);
+    A.host_free(t->h_rows, t->h_rows_bytes);
+    A.event_free(t->rows_free, false);
     for (auto& ev : t->move_ev) {
         A.event_free(ev.first, true);
         A.event_free(ev.second, true);

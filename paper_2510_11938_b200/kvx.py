@@ -149,6 +149,7 @@ def _load() -> C.CDLL:
         "kvx_begin": (C.c_int, [P(_Desc), P(VP)]),
         "kvx_wave": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(I64)]),
         "kvx_wait": (C.c_int, [VP, U64, P(C.c_double)]),
+        "kvx_src_rows": (C.c_int, [VP, U64, I32, P(I32), P(I32)]),
         "kvx_commit": (C.c_int, [VP, U64, I32, P(I32), P(I64), P(_CommitResult)]),
         "kvx_abort": (C.c_int, [VP]),
         "kvx_destroy": (C.c_int, [VP]),
@@ -474,6 +475,12 @@ class Transition(_Handle):
         req, lo, hi = _i32(req), _i64(lo), _i64(hi)
         _check(_lib.kvx_wave(self._h, self.epoch if epoch is None else epoch, len(req), _p32(req),
                              _p64(lo), _p64(hi)))
+
+    def src_rows(self, req, rows, epoch: Optional[int] = None) -> None:
+        """kvx_src_rows: replace source-table rows of `req` ([n, max_blocks])."""
+        req = _i32(req)
+        rows = np.ascontiguousarray(rows, dtype=np.int32).reshape(len(req), self.max_blocks)
+        _check(_lib.kvx_src_rows(self._h, self.epoch if epoch is None else epoch, len(req), _p32(req), _p32(rows)))
 
     def wait(self, epoch: Optional[int] = None) -> float:
         ms = C.c_double()
