@@ -13,6 +13,8 @@
 #include <fstream>
 #include <mutex>
 #include <string>
+#include <exception>
+#include <execinfo.h>
 #include <unistd.h>
 
 #include <json.hpp>
@@ -125,7 +127,7 @@ struct KvxPlane::Impl {
     int max_sync_rounds = 8;
     std::int32_t max_requests = 0, max_blocks = 1;
     std::vector<std::int64_t> req_max_tokens;  // prompt + output per request
-    double max_pool_bytes = 24e9;              // cap per transition (source + destination)
+    double max_pool_bytes = 96e9;              // cap per transition (source + destination), of 180 GB
     kvx_geometry pending{};                    // fixed by grant_kv_bytes for the next begin
     std::int64_t pending_blocks = 0;
     std::map<std::int64_t, Xfer> active;
@@ -153,9 +155,9 @@ struct KvxPlane::Impl {
             throw InvalidSpecError("PIPESIM_KVX_GEOMETRY must be auto or H,D");
         }
         kvx_geometry g = geometry(h, d);
-        // source (with fragmentation slack) + destination must fit the cap
-        if (real && 2.5 * pool_bytes(g, blocks) > max_pool_bytes) g = geometry(2, 64);
-        if (2.5 * pool_bytes(g, blocks) > max_pool_bytes) g = geometry(1, 8);
+        // source (1.25x, fragmentation slack) + destination must fit the cap
+        if (real && 2.3 * pool_bytes(g, blocks) > max_pool_bytes) g = geometry(2, 64);
+        if (2.3 * pool_bytes(g, blocks) > max_pool_bytes) g = geometry(1, 8);
         return g;
     }
 
@@ -323,7 +325,17 @@ std::shared_ptr<KvxPlane> KvxPlane::from_env(const EngineConfig& cfg, const std:
         impl->max_blocks = (std::int32_t)std::max<std::int64_t>(impl->max_blocks, cdiv(impl->req_max_tokens[i], kBlockTokens));
     }
     static std::once_flag once;
-    std::call_once(once, [] { std::atexit(write_report); });
+    std::call_once(once, [] {
+        std::atexit(write_report);
+        if (std::getenv("PIPESIM_KVX_TRACE"))  // where an escaping exception came from
+            std::set_terminate([] {
+                void* frames[64];
+                const int n = backtrace(frames, 64);
+                std::fprintf(stderr, "kvx-plane: terminate; backtrace:\n");
+                backtrace_symbols_fd(frames, n, 2);
+                std::abort();
+            });
+    });
     {
         std::lock_guard<std::mutex> lk(stats().mu);
         stats().mode = impl->measured ? "measured" : "parity";
@@ -356,6 +368,8 @@ void KvxPlane::reset_stats() {
 std::vector<double> KvxPlane::grant_kv_bytes(const std::vector<int>& new_boundaries,
                                              const std::vector<std::int64_t>& live_max_tokens) {
     Impl& I = *impl_;
+    if (I.trace)
+        std::fprintf(stderr, "kvx-plane grant K=%zu live=%zu\n", new_boundaries.size() + 1, live_max_tokens.size());
     std::int64_t blocks = 0;
     for (std::int64_t t : live_max_tokens) blocks += cdiv(t, kBlockTokens);
     blocks = std::max<std::int64_t>(blocks, 16);

@@ -27,6 +27,9 @@
 //                          equals kv_bytes_per_token, else 2 heads x 64) or
 //                          "H,D"
 //   PIPESIM_KVX_DEVICE     CUDA device (default 0)
+//   PIPESIM_KVX_MAX_GB     cap on one transition's pools, source + destination
+//                          (default 96); above it the plane moves a smaller
+//                          test geometry (2 x 64, then 1 x 8) -- and charges that
 //   PIPESIM_KVX_REPORT     file that receives one JSON line per process at exit:
 //                          transitions, waves, bytes, device vs host Eq. 10
 //                          counts, mismatched payload words, the wave log

@@ -473,69 +473,100 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-struct ChunkIter {  // walks (unit, run, offset) -> chunks of <= `chunk` bytes
-    const Seg* segs;
-    const LayerPtr* layers;
-    int32_t nseg;
-    int64_t units, u, ustep;
-    uint64_t block_bytes, token_bytes;
-    int32_t block_tokens;
+// Copy descriptor of one (segment, layer) unit, resolved ahead of time by the
+// CTA's helper lanes (kvx_bulk_kernel): the issuing lane then never waits on
+// the dependent global loads of segs[] / layers[] -- one per unit, i.e. per
+// 20 KiB of a token-granular wave -- between two bulk copies.
+struct UnitDesc {
+    const char* src;  // first run (K rows of the first head), offset applied
+    char* dst;
+    uint64_t src_kv, dst_kv, src_hs, dst_hs;
+    uint32_t run_bytes;
+    int32_t nrun;  // 0: nothing to move (empty segment / head-major tail)
+    uint32_t nh;
+    uint32_t pad;
+};
+constexpr int kDescBatch = 31;  // helper lanes 1..31 resolve one unit each per batch
+
+__device__ __forceinline__ UnitDesc resolve_unit(const Seg* __restrict__ segs, const LayerPtr* __restrict__ layers,
+                                                 int32_t nseg, int64_t u, uint64_t block_bytes,
+                                                 int32_t block_tokens) {
+    UnitDesc d{};
+    if (u < 0) return d;
+    const int32_t layer = (int32_t)(u / nseg);
+    const Seg sg = segs[u - (int64_t)layer * nseg];
+    const LayerPtr lp = layers[layer];
+    const bool full = sg.t0 == 0 && sg.t1 == block_tokens;
+    if (sg.t1 <= sg.t0) return d;      // emptied by the plan kernel's bounds check
+    if (lp.nh > 1 && !full) return d;  // head-major tail: kvx_move_any_kernel(tails_only)
+    const char* bs = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
+    char* bd = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
+    const uint64_t half = block_bytes >> 1;
+    d.src_kv = lp.src_kv;
+    d.dst_kv = lp.dst_kv;
+    d.src_hs = lp.src_hs;
+    d.dst_hs = lp.dst_hs;
+    if (full && lp.src_kv == half && lp.dst_kv == half) {
+        d.nrun = 1;  // the whole block is one run on both sides (BLOCKS, HEADS)
+        d.nh = 1;
+        d.run_bytes = (uint32_t)block_bytes;
+        d.src = bs;
+        d.dst = bd;
+    } else {  // K rows then V rows; per head for head-major pools
+        const uint64_t off0 = (uint64_t)sg.t0 * lp.run_tok;
+        d.nh = lp.nh;
+        d.nrun = 2 * (int32_t)lp.nh;
+        d.run_bytes = (uint32_t)((uint64_t)(sg.t1 - sg.t0) * lp.run_tok);
+        d.src = bs + off0;
+        d.dst = bd + off0;
+    }
+    return d;
+}
+
+// The issuing lane's side: walks the descriptors batch by batch (double
+// buffered in shared memory; one __syncwarp hand-off per batch with the
+// helpers, which resolve batch b+1 while batch b streams) and cuts each run
+// into chunks of <= `chunk` bytes.
+struct UnitIter {
+    UnitDesc (*desc)[kDescBatch];
+    int64_t my_units, nbatch;
+    int64_t batch = -1;  // batch currently in `desc[batch & 1]`
+    int pos = kDescBatch;
+    int64_t seen = 0;    // units consumed so far
     uint32_t chunk;
-    // current run
+    UnitDesc cur;
+    int run = 0;
     const char* src;
     char* dst;
-    uint64_t left;
-    int run, nrun;  // current run / runs of the unit: 1 (whole block), 2 (K, V) or 2*nh
-    uint32_t nh;    // runs per K/V (head-major pools: one per head)
-    uint64_t run_bytes, off0;
-    const char* base_src;
-    char* base_dst;
-    uint64_t src_kv, dst_kv, src_hs, dst_hs;  // of the current unit's layer
+    uint64_t left = 0;
 
     __device__ bool load_unit() {
-        for (; u < units; u += ustep) {
-            const int32_t layer = (int32_t)(u / nseg);
-            const Seg sg = segs[u - (int64_t)layer * nseg];
-            const LayerPtr lp = layers[layer];
-            const bool full = sg.t0 == 0 && sg.t1 == block_tokens;
-            if (sg.t1 <= sg.t0) continue;      // emptied by the plan kernel's bounds check
-            if (lp.nh > 1 && !full) continue;  // head-major tail: kvx_move_any_kernel(tails_only)
-            base_src = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
-            base_dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
-            src_kv = lp.src_kv;
-            dst_kv = lp.dst_kv;
-            src_hs = lp.src_hs;
-            dst_hs = lp.dst_hs;
-            const uint64_t half = block_bytes >> 1;
-            run = 0;
-            if (sg.t0 == 0 && sg.t1 == block_tokens && src_kv == half && dst_kv == half) {
-                nrun = 1;  // the whole block is one run on both sides (BLOCKS, HEADS)
-                nh = 1;
-                off0 = 0;
-                run_bytes = block_bytes;
-            } else {  // K rows then V rows; per head for head-major pools
-                nh = lp.nh;
-                nrun = 2 * (int)nh;
-                off0 = (uint64_t)sg.t0 * lp.run_tok;
-                run_bytes = (uint64_t)(sg.t1 - sg.t0) * lp.run_tok;
+        for (;;) {
+            if (seen >= my_units) return false;
+            if (pos == kDescBatch) {  // next batch: meet the helpers
+                ++batch;
+                __syncwarp();
+                pos = 0;
             }
-            src = base_src + off0;
-            dst = base_dst + off0;
-            left = run_bytes;
+            cur = desc[batch & 1][pos++];
+            ++seen;
+            if (cur.nrun == 0) continue;
+            run = 0;
+            src = cur.src;
+            dst = cur.dst;
+            left = cur.run_bytes;
             return true;
         }
-        return false;
     }
     __device__ bool next(const char** s, char** d, uint32_t* n) {
-        while (left == 0) {  // (load_unit never yields an empty run, so this ends)
-            if (++run < nrun) {  // next (K|V, head) run of the unit
-                const uint32_t kv = (uint32_t)run / nh, h = (uint32_t)run % nh;
-                src = base_src + kv * src_kv + h * src_hs + off0;
-                dst = base_dst + kv * dst_kv + h * dst_hs + off0;
-                left = run_bytes;
+        while (left == 0) {
+            if (++run < cur.nrun) {  // next (K|V, head) run of the unit
+                const uint32_t kv = (uint32_t)run / cur.nh, h = (uint32_t)run % cur.nh;
+                src = cur.src + kv * cur.src_kv + h * cur.src_hs;
+                dst = cur.dst + kv * cur.dst_kv + h * cur.dst_hs;
+                left = cur.run_bytes;
                 continue;
             }
-            u += ustep;
             if (!load_unit()) return false;
         }
         const uint32_t c = left > chunk ? chunk : (uint32_t)left;
@@ -633,34 +664,45 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
                 int32_t n_peer, int32_t peer_ctas) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[kStages];
-    if (threadIdx.x != 0) return;
+    __shared__ UnitDesc desc[2][kDescBatch];
+    (void)token_bytes;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the plan kernel's segments
-    ChunkIter it;
-    it.segs = segs;
-    it.layers = layers;
-    it.nseg = nseg;
+    // this CTA's units: u0, u0 + ustep, ... < units
+    int64_t u0, ustep, units;
     const int64_t split = (int64_t)nseg * n_peer;
     if (peer_ctas > 0 && n_peer > 0 && n_peer < nlayers && (int)gridDim.x > peer_ctas) {
         if ((int)blockIdx.x < peer_ctas) {
-            it.u = blockIdx.x;
-            it.ustep = peer_ctas;
-            it.units = split;
+            u0 = blockIdx.x;
+            ustep = peer_ctas;
+            units = split;
         } else {
-            it.u = split + (blockIdx.x - peer_ctas);
-            it.ustep = gridDim.x - peer_ctas;
-            it.units = (int64_t)nseg * nlayers;
+            u0 = split + (blockIdx.x - peer_ctas);
+            ustep = gridDim.x - peer_ctas;
+            units = (int64_t)nseg * nlayers;
         }
     } else {
-        it.u = blockIdx.x;
-        it.ustep = gridDim.x;
-        it.units = (int64_t)nseg * nlayers;
+        u0 = blockIdx.x;
+        ustep = gridDim.x;
+        units = (int64_t)nseg * nlayers;
     }
-    it.block_bytes = block_bytes;
-    it.token_bytes = token_bytes;
-    it.block_tokens = block_tokens;
+    const int64_t my_units = u0 < units ? (units - u0 + ustep - 1) / ustep : 0;
+    const int64_t nbatch = (my_units + kDescBatch - 1) / kDescBatch;
+    if (nbatch == 0) return;
+    const int lane = (int)threadIdx.x;
+    if (lane != 0) {  // helpers: resolve batch b, publish it, go on with b + 1
+        for (int64_t b = 0; b < nbatch; ++b) {
+            const int64_t k = b * kDescBatch + (lane - 1);
+            desc[b & 1][lane - 1] =
+                resolve_unit(segs, layers, nseg, k < my_units ? u0 + k * ustep : -1, block_bytes, block_tokens);
+            __syncwarp();  // batch b is visible to the issuing lane
+        }
+        return;
+    }
+    UnitIter it;
+    it.desc = desc;
+    it.my_units = my_units;
+    it.nbatch = nbatch;
     it.chunk = kChunk;
-    it.left = 0;
-    it.run = 1;
     if (!it.load_unit()) return;
     bulk_stream<kStages, kChunk, kLag, kPack>(it, smem, bars);
 }
