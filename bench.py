@@ -1101,6 +1101,10 @@ def main():
         roof = {"bound": bound, "achieved": round(frac * (peak if bound == "hbm" else nvl_peak), 1),
                 "peak": peak if bound == "hbm" else nvl_peak, "unit": "GB/s", "frac": round(frac, 4),
                 "traffic": None, "kernel": "kvx_bulk_kernel (wave 0, slowest rank)",
+                "algorithmic_bytes_per_gpu": {"hbm_rw": [int(x) for x in hbm], "nvlink_out": [int(x) for x in out],
+                                              "nvlink_in": [int(x) for x in inn]},
+                "traffic_note": "N>1: DRAM / NVLink bytes of the movers come from ncu on rank 0 "
+                                "(scripts/nvlink_r02.sh, profiles/), not from this run",
                 "t_roof_ms": round(t_roof * 1e3, 4), "launch_ms": round(w0_avg, 4),
                 "peak_source": f"hbm {peak_kind}; nvlink 770 GB/s measured peer copy"}
 
