@@ -326,6 +326,10 @@ std::shared_ptr<KvxPlane> KvxPlane::from_env(const EngineConfig& cfg, const std:
     }
     static std::once_flag once;
     std::call_once(once, [] {
+        // the statistics object must outlive the exit handler: construct it
+        // first (function statics die in reverse order of construction,
+        // interleaved with atexit handlers)
+        stats();
         std::atexit(write_report);
         if (std::getenv("PIPESIM_KVX_TRACE"))  // where an escaping exception came from
             std::set_terminate([] {
