@@ -158,18 +158,11 @@ inline const BulkVariant kBulkVariants[] = {
 };
 #undef KVX_BV
 constexpr int kSlabVariant = 2;  // 3 x 64 KiB, one chunk per slot
-constexpr int kTokVariant = 0;   // 6 x 32 KiB (round 1 default; sweeps in profiles/)
+// 4 x 16 KiB, two CTAs per SM on a 296-CTA grid: the C3 final wave in 73.7-77.8 us on
+// four boxes, against 88-96 us for round 1's 6 x 32 KiB on 148 (profiles/r02*_wave_sweep_tok*)
+constexpr int kTokVariant = 7;
 constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
 
-// LSU token movers (kvx_tok_kernel<kU>): warp per unit, kU vectors per lane in flight.
-using TokFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, int32_t, int32_t);
-struct TokVariant {
-    int u;
-    TokFn fn;
-};
-inline const TokVariant kTokVariants[] = {{4, kvx::kvx_tok_kernel<4>}, {8, kvx::kvx_tok_kernel<8>},
-                                          {16, kvx::kvx_tok_kernel<16>}};
-constexpr int kNumTokVariants = sizeof(kTokVariants) / sizeof(kTokVariants[0]);
 
 }  // namespace kvx_host
 
@@ -269,8 +262,6 @@ struct kvx_transition {
     int bulk_ctas[32] = {};  // resident CTAs per SM of each bulk variant
     int bulk_variant_slab = kvx_host::kSlabVariant;  // ring of slab-sized waves (KVX_BULK_CFG[_SLAB])
     int bulk_variant_tok = kvx_host::kTokVariant;    // ring of token-granular waves (KVX_BULK_CFG[_TOK])
-    int tok_lsu = -1;        // token-granular waves on kvx_tok_kernel (kTokVariants index), -1 = bulk ring
-    int tok_ctas[4] = {};    // resident CTAs per SM of each LSU token variant
     bool use_bulk = false;   // TMA bulk mover for local destinations
     bool peer_bulk = false;  // ... and for peer (NVLink) destinations
     bool lsu256 = false;     // LSU mover with 256-bit accesses (KVX_MOVE_IMPL=lsu256)

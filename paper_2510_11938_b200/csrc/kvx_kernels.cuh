@@ -707,55 +707,6 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     bulk_stream<kStages, kChunk, kLag, kPack>(it, smem, bars);
 }
 
-// ------------------------------------------- LSU token mover (warp per unit)
-// Token-granular waves (delta / final): each (segment, layer) unit is a K and
-// a V run of (t1 - t0) * token_bytes (10 KiB for one 13B token).  One warp
-// owns a unit: its lanes resolve the descriptor (resolve_unit), then stream
-// the unit's runs as one virtual vector range, kU 16-byte loads per lane in
-// flight before the stores -- 32 * kU * 16 B per warp step, many warps per
-// SM -- so the scattered short runs get the memory-level parallelism the
-// single-issuer bulk ring cannot give them.  Head-major tails are left to
-// kvx_move_any_kernel (tails_only), as in the bulk mover.
-constexpr int kTokThreads = 256;
-
-template <int kU>
-__global__ void __launch_bounds__(kTokThreads)
-kvx_tok_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers, int32_t nlayers,
-               uint64_t block_bytes, int32_t block_tokens, int32_t fence_system) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint32_t lane = threadIdx.x & 31u;
-    const int64_t nwarps = (int64_t)gridDim.x * (kTokThreads / 32);
-    const int64_t units = (int64_t)nseg * nlayers;
-    for (int64_t u = (int64_t)blockIdx.x * (kTokThreads / 32) + (threadIdx.x >> 5); u < units; u += nwarps) {
-        const UnitDesc d = resolve_unit(segs, layers, nseg, u, block_bytes, block_tokens);
-        if (d.nrun == 0) continue;
-        const uint32_t per = d.run_bytes >> 4;  // vectors per run
-        const uint32_t total = per * (uint32_t)d.nrun;
-        // element i of the unit's virtual vector range -> run r = i / per,
-        // vector w = i % per of the run; recomputed at the store (ALU is idle,
-        // registers buy occupancy = bytes in flight)
-        auto addr = [&](uint32_t i, uint64_t kvs, uint64_t hs, const char* base) {
-            const uint32_t r = i / per, w = i - r * per;
-            const uint32_t kv = r / d.nh, h = r - kv * d.nh;
-            return reinterpret_cast<const uint4*>(base + kv * kvs + h * hs) + w;
-        };
-        for (uint32_t base = 0; base < total; base += 32u * kU) {
-            uint4 v[kU];
-#pragma unroll
-            for (int k = 0; k < kU; ++k) {
-                const uint32_t i = base + (uint32_t)k * 32u + lane;
-                if (i < total) v[k] = ld_stream(addr(i, d.src_kv, d.src_hs, d.src));
-            }
-#pragma unroll
-            for (int k = 0; k < kU; ++k) {
-                const uint32_t i = base + (uint32_t)k * 32u + lane;
-                if (i < total) st_stream(const_cast<uint4*>(addr(i, d.dst_kv, d.dst_hs, d.dst)), v[k]);
-            }
-        }
-    }
-    if (fence_system) __threadfence_system();
-}
-
 // ------------------------------------------------- generic copy list
 // Activation handoff (and any batched device copy): a list of (src, dst,
 // bytes) pieces, 16-byte aligned, streamed by the same bulk engine loop.

@@ -26,8 +26,6 @@ cudaError_t preload_transition_kernels() {
         if ((e = cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       bv.stages * (int)bv.chunk)) != cudaSuccess)
             return e;
-    for (const TokVariant& tv : kTokVariants)
-        if ((e = cudaFuncGetAttributes(&a, (const void*)tv.fn)) != cudaSuccess) return e;
     return e;
 }
 }  // namespace kvx_host
@@ -161,15 +159,6 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         t->lsu256 = impl && std::string(impl) == "lsu256";
         const char* pb = getenv("KVX_PEER_BULK");
         t->peer_bulk = t->use_bulk && !(pb && std::string(pb) == "0");
-        // token-granular waves: KVX_TOK_MOVER = bulk | lsu4 | lsu8 | lsu16
-        for (int v = 0; v < kNumTokVariants; ++v) {
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kTokVariants[v].fn, kvx::kTokThreads, 0) != cudaSuccess)
-                return bail(fail(KVX_ECUDA, "token mover occupancy"));
-            t->tok_ctas[v] = std::max(1, occ);
-        }
-        if (const char* tm = getenv("KVX_TOK_MOVER"))
-            for (int v = 0; v < kNumTokVariants; ++v)
-                if (std::string(tm) == "lsu" + std::to_string(kTokVariants[v].u)) t->tok_lsu = v;
     }
 
     if (d->stream) {
@@ -377,37 +366,10 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         // the 70B-GQA slab waves -- 64 KiB blocks, partial tails pulling the
         // average to 65,015 B -- on the token ring.)
         const bool slab = 2 * full_tokens >= tokens;
-        const bool tok_lsu_wave = !slab && t->tok_lsu >= 0 && !t->transpose;
         if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
             kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                 (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0);
-        } else if (tok_lsu_wave) {
-            // token-granular wave on the LSU warp-per-unit mover (kvx_tok_kernel)
-            const TokVariant& tv = kTokVariants[t->tok_lsu];
-            constexpr int64_t kWarps = kvx::kTokThreads / 32;
-            int64_t full_t = (int64_t)t->num_sms * t->tok_ctas[t->tok_lsu];
-            if (const char* tg = getenv("KVX_TOK_GRID")) full_t = std::max<int64_t>(1, atoll(tg));
-            if (t->max_ctas > 0) full_t = std::min<int64_t>(full_t, t->max_ctas);
-            const unsigned grid_t = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv64(units, kWarps), full_t));
-            cudaLaunchAttribute attr{};
-            attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr.val.programmaticStreamSerializationAllowed = 1;
-            cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3(grid_t);
-            cfg.blockDim = dim3(kvx::kTokThreads);
-            cfg.stream = t->stream;
-            cfg.attrs = &attr;
-            cfg.numAttrs = 1;
-            KVX_CUDA(cudaLaunchKernelEx(&cfg, tv.fn, (const kvx::Seg*)t->d_segs, (int32_t)nseg,
-                                        (const kvx::LayerPtr*)t->d_layers, t->n_local_layers, block_bytes(t->g),
-                                        t->g.block_tokens, t->has_peer_dst ? 1 : 0));
-            if (t->head_tails) {  // head-major partial blocks: the row mover, after it on the stream
-                KVX_LAUNCHED();
-                kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
-                    t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
-                    (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 1, t->has_peer_dst ? 1 : 0);
-            }
         } else if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
             const int vi = slab ? t->bulk_variant_slab : t->bulk_variant_tok;
             const BulkVariant& bv = kBulkVariants[vi];
@@ -418,10 +380,11 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             // own CTAs and the local layers the rest: NVLink pushes saturate with
             // ~16-32 CTAs, pulls (TMA loads from the peer) want ~64
             // (profiles/r01_nvlink_split.jsonl, r01_movers_n2.jsonl).
-            // Token-granular waves (delta / final: runs of a few KiB) want every SM
-            // (C3 final wave: 148 -> 73.8 us, 128 -> 75.8, 96 -> 86.0;
-            // profiles/grid_cross_box/grid_tok.jsonl; KVX_BULK_GRID_TOK overrides).
-            constexpr int64_t kLocalGrid = 96, kLocalGridTok = 148, kPushCtas = 32, kPullCtas = 64;
+            // Token-granular waves (delta / final: runs of a few KiB) want every SM,
+            // two small-ring CTAs on each: the 4 x 16 KiB ring on 296 CTAs is at or
+            // within 2 us of the best of 40 (ring, grid) pairs on four boxes
+            // (profiles/r02*_wave_sweep_tok*; KVX_BULK_GRID_TOK overrides).
+            constexpr int64_t kLocalGrid = 96, kLocalGridTok = 296, kPushCtas = 32, kPullCtas = 64;
             const char* gt = getenv("KVX_BULK_GRID_TOK");
             const int64_t grid_tok = gt ? std::max<int64_t>(1, atoll(gt)) : kLocalGridTok;
             const int64_t local_grid = slab ? kLocalGrid : grid_tok;
