@@ -41,11 +41,15 @@ def main():
     peak = bench.peaks()[0]
     for v in args.variants.split(","):
         for grid in [int(x) for x in args.grids.split(",")]:
-            os.environ["KVX_BULK_CFG_" + args.kind.upper()] = v
-            if args.kind == "tok":
-                os.environ["KVX_BULK_GRID_TOK"] = str(grid)
+            if v.startswith("lsu"):  # LSU warp-per-run token mover (kvx_run_kernel, experiment)
+                os.environ["KVX_TOK_MOVER"] = v
+                os.environ["KVX_TOK_GRID"] = str(grid)
             else:
-                os.environ["KVX_BULK_GRID"] = str(grid)
+                os.environ["KVX_BULK_CFG_" + args.kind.upper()] = v
+                if args.kind == "tok":
+                    os.environ["KVX_BULK_GRID_TOK"] = str(grid)
+                else:
+                    os.environ["KVX_BULK_GRID"] = str(grid)
             times = []
             for s in range(args.steps + 2):
                 tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, 0, plan.N,
@@ -67,7 +71,8 @@ def main():
                               "move_ms_by_wave": [round(x, 4) for x in ms],
                               "frac_by_wave": [round(b / (m * 1e-3) / 1e9 / peak, 4) for b, m in zip(by, ms)]}),
                   flush=True)
-            for k in ("KVX_BULK_CFG_TOK", "KVX_BULK_CFG_SLAB", "KVX_BULK_GRID_TOK", "KVX_BULK_GRID"):
+            for k in ("KVX_BULK_CFG_TOK", "KVX_BULK_CFG_SLAB", "KVX_BULK_GRID_TOK", "KVX_BULK_GRID", "KVX_TOK_MOVER",
+                      "KVX_TOK_GRID"):
                 os.environ.pop(k, None)
     for p in old_pools + new_pools:
         p.close()
