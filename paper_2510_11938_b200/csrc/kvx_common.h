@@ -58,6 +58,25 @@ struct DeviceGuard {
     }
 };
 
+// A pool of this process on another GPU is usable over NVLink when the two
+// devices have peer access (enabled here; idempotent).  One process may drive
+// several GPUs, one transition handle per device -- the single-process
+// analogue of one rank per GPU.
+inline bool peer_ok(int dev, int other) {
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, dev, other) != cudaSuccess || !can) {
+        cudaGetLastError();
+        return false;
+    }
+    DeviceGuard dg(dev);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(other, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return true;
+    }
+    return e == cudaSuccess;
+}
+
 inline bool geometry_ok(const kvx_geometry* g, std::string* why) {
     if (!g) return *why = "geometry is null", false;
     if (g->num_layers < 1 || g->num_kv_heads < 1 || g->head_dim < 1 || g->elem_bytes < 1 ||

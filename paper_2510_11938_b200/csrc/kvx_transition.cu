@@ -61,7 +61,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
                                stage_begin(nb, k);
         if (p->num_layers != layers) return fail(KVX_EINVAL, "new pool layer count != stage layer range");
         if (p->num_blocks < d->dst_num_blocks) return fail(KVX_EINVAL, "new pool smaller than dst_num_blocks");
-        if (!p->imported && p->device != d->device) return fail(KVX_EINVAL, "local new pool on another device");
+        if (!p->imported && p->device != d->device && !peer_ok(d->device, p->device))
+            return fail(KVX_EINVAL, "local new pool on another device without peer access");
         if (p->imported && p->device != d->device) return fail(KVX_EINVAL, "imported pool mapped for another device");
         if (p->g.num_kv_heads != g.num_kv_heads || p->g.head_dim != g.head_dim ||
             p->g.elem_bytes != g.elem_bytes || p->g.block_tokens != g.block_tokens)
@@ -73,7 +74,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         const int32_t layers = (k + 1 < d->old_plan.num_stages ? ob[(size_t)k] : g.num_layers) -
                                stage_begin(ob, k);
         if (p->num_layers != layers) return fail(KVX_EINVAL, "old pool layer count != stage layer range");
-        if (!p->imported && p->device != d->device) return fail(KVX_EINVAL, "local old pool on another device");
+        if (!p->imported && p->device != d->device && !peer_ok(d->device, p->device))
+            return fail(KVX_EINVAL, "local old pool on another device without peer access");
         if (p->imported && p->device != d->device) return fail(KVX_EINVAL, "imported old pool mapped for another device");
         if (p->g.num_kv_heads != g.num_kv_heads || p->g.head_dim != g.head_dim ||
             p->g.elem_bytes != g.elem_bytes || p->g.block_tokens != g.block_tokens)
@@ -226,8 +228,10 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         const int so = stage_of_layer(ob, l), sn = stage_of_layer(nb, l);
         kvx_pool* src = t->old_pools[(size_t)so];
         kvx_pool* dst = t->new_pools[(size_t)sn];
-        const bool src_local = src && !src->imported && src->device == d->device;
-        const bool dst_local = dst && !dst->imported && dst->device == d->device;
+        // remote = behind NVLink: a peer rank's pool (CUDA IPC) or this process's pool on another GPU
+        auto remote = [&](const kvx_pool* p) { return p->imported || p->device != d->device; };
+        const bool src_local = src && !remote(src);
+        const bool dst_local = dst && !remote(dst);
         const bool pulled = d->layer_pull ? d->layer_pull[l] != 0 : d->pull != 0;
         if (src_local && dst_local) {
             // both pools here: a local move whichever side would otherwise move it
@@ -251,8 +255,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
                           src->head_stride(), dst->head_stride(),
                           (uint32_t)(heads_runs ? src->head_bytes() : token_bytes(g)),
                           heads_runs ? (uint32_t)g.num_kv_heads : 1u});
-        layer_is_peer.push_back(dst->imported || src->imported ? 1 : 0);
-        if (dst->imported) t->has_peer_dst = true;
+        layer_is_peer.push_back(remote(dst) || remote(src) ? 1 : 0);
+        if (remote(dst)) t->has_peer_dst = true;
     }
     // peer-destination layers first (see kvx_bulk_kernel's CTA split)
     {
@@ -816,7 +820,7 @@ int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_
     KVX_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), t->stream));
     std::vector<char*> lay;  // every local new pool's layer bases, back to back
     for (const kvx_pool* p : t->new_pools)
-        if (p && !p->imported) lay.insert(lay.end(), p->layer_base.begin(), p->layer_base.end());
+        if (p && !p->imported && p->device == t->device) lay.insert(lay.end(), p->layer_base.begin(), p->layer_base.end());
     char** d_lay = nullptr;
     const size_t lay_bytes = sizeof(char*) * std::max<size_t>(1, lay.size());
     KVX_CUDA(A.dev_alloc((void**)&d_lay, lay_bytes));
@@ -826,7 +830,7 @@ int kvx_verify_pattern(kvx_transition* t, uint64_t seed, int32_t n, const int32_
     size_t at = 0;
     for (size_t k = 0; k < t->new_pools.size(); ++k) {
         const kvx_pool* p = t->new_pools[k];
-        if (!p || p->imported) continue;  // the owning rank verifies it
+        if (!p || p->imported || p->device != t->device) continue;  // the owning rank / device verifies it
         kvx::kvx_verify_kernel<<<grid, 256, 0, t->stream>>>(
             pool_addr(p, d_lay + at), stage_begin(t->new_b, (int)k), p->num_layers, d_req, d_kv,
             t->d_dst_bt, t->max_blocks, t->g.block_tokens, token_bytes(t->g), seed, d_bad);
