@@ -447,6 +447,60 @@ def reference_condition_stall(make, t, plan, shape, stream, dev, reps: int = 4):
     return out
 
 
+def nvlink_probe(kvx, torch, dist, plan, g, rank, world, dev, gather, reps: int = 5):
+    """Wave 0 of the same transition under the reference's DISJOINT grant
+    (engine.cpp:584-591: the new stages on GPUs that do not hold the model's
+    old stages; placement 'disjoint'), so every KV byte crosses NVLink, with
+    the default per-layer movers.  Max over ranks of the mover time against
+    the NVLink roofline (770 GB/s per direction, measured peer copy).  The
+    bench's own placement (affinity) keeps layers local where it can; this
+    puts the link itself in every N>1 line.  Returns a dict."""
+    t, L = plan.t, plan.L
+    old_dev, new_dev = S.placement(L, t.old_boundaries, t.new_boundaries, world, "disjoint")
+    layer_pull = S.move_plan(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev, "auto")
+    old_pools, new_pools = S.setup_rank_pools(
+        kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, rank, dev, plan.old_blocks, plan.dst_blocks,
+        all_gather=gather, fill=(SEED, plan.live, plan.tokens[plan.live], plan.src_bt), layer_pull=layer_pull)
+    dist.barrier()
+    stream = torch.cuda.Stream(device=dev)
+    w0 = t.waves[0]
+    ms = []
+    for rep in range(reps + 1):
+        tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, dev, plan.N,
+                            plan.max_blocks, plan.dst_blocks, plan.src_bt, epoch=t.epoch,
+                            stream=stream.cuda_stream, layer_pull=layer_pull)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        tr.wave(w0.req, w0.lo, w0.hi)
+        tr.wait()
+        m = tr.move_timings()
+        if rep:
+            ms.append(m[0][0] if m else 0.0)
+        tr.close()
+    dist.barrier()
+    med = torch.tensor([statistics.median(ms)], dtype=torch.float64, device=dev)
+    dist.all_reduce(med, op=dist.ReduceOp.MAX)
+    w0_ms = float(med.item())
+    hbm, out, inn = S.link_bytes(L, t.old_boundaries, t.new_boundaries, old_dev, new_dev,
+                                 plan.wave0_tokens * 2 * plan.token_bytes, world)
+    t_roof = max(max(o for o in out) / 770e9, max(i for i in inn) / 770e9, max(h for h in hbm) / (peaks()[0] * 1e9))
+    for p in old_pools + new_pools:
+        if p is not None and p.imported:
+            p.close()
+    dist.barrier()
+    for p in old_pools + new_pools:
+        if p is not None and not p.imported:
+            p.close()
+    dist.barrier()
+    return {"placement": {"mode": "disjoint", "old_stage_gpu": old_dev, "new_stage_gpu": new_dev},
+            "movers": "auto", "pulled_layers": int(sum(layer_pull)), "wave0_mover_ms": round(w0_ms, 4),
+            "nvlink_out_bytes_per_gpu": [int(x) for x in out], "nvlink_in_bytes_per_gpu": [int(x) for x in inn],
+            "t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / w0_ms, 4),
+            "GBps_per_direction_busiest": round(max(out + inn) / (w0_ms * 1e-3) / 1e9, 1),
+            "note": "every KV byte crosses NVLink (the reference's disjoint grant); max over ranks; roofline "
+                    "770 GB/s per direction (measured peer copy), HBM for the local share"}
+
+
 # ------------------------------------------------------------ NCCL baseline
 def nccl_baseline(kvx, torch, dist, plan, g, old_pools, old_dev, new_dev, rank, world, dev, stream,
                   reps=5):
@@ -773,6 +827,7 @@ def main():
                     help="KV GB per step of the CPU runs (--impl reference, cpu_baseline); default: the "
                          "full wave plan (falls back to a sample only when host memory is short)")
     ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu traffic pass")
+    ap.add_argument("--no-nvlink-probe", action="store_true", help="N>1: skip the disjoint-grant NVLink wave")
     ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--probe-all-waves", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--layouts", default="blocks,blocks",
@@ -1049,6 +1104,11 @@ def main():
                                "reference models this as host/storage loads (load_ready_ms)"}
             del wold, wnew
 
+    # ---- NVLink under the reference's disjoint grant (N > 1)
+    nvl = None
+    if world > 1 and not fold and not args.no_nvlink_probe:
+        nvl = nvlink_probe(kvx, torch, dist, plan, g, rank, world, dev, gather)
+
     # ---- NCCL baseline of the cross-GPU path (N > 1, when bytes cross GPUs)
     nccl = None
     if world > 1 and not args.no_nccl:
@@ -1152,7 +1212,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                 "ms_per_step": round(e2e_s * 1e3 / e2e_steps, 4)},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clocks, "handoff": handoff,
-        "weights": weights, "nccl_baseline": nccl,
+        "weights": weights, "nccl_baseline": nccl, "nvlink_disjoint": nvl,
         "move_kernel_ms_per_step": round(all_move_ms / K, 4), "move_ms_by_wave": wave_ms,
         "rank_ms_per_step": rank_ms, "rank_wave0_move_ms": rank_w0,
         "mover": os.environ.get("KVX_MOVE_IMPL", "bulk") + ":" + os.environ.get("KVX_BULK_CFG", "auto"),
