@@ -182,15 +182,6 @@ constexpr int kSlabVariant = 2;  // 3 x 64 KiB, one chunk per slot
 constexpr int kTokVariant = 7;
 constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
 
-// LSU run movers for token-granular waves (KVX_TOK_MOVER=lsu<u>, experiment).
-using RunFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, int32_t, int32_t);
-struct RunVariant {
-    int u;
-    RunFn fn;
-};
-inline const RunVariant kRunVariants[] = {{4, kvx::kvx_run_kernel<4>}, {8, kvx::kvx_run_kernel<8>},
-                                          {20, kvx::kvx_run_kernel<20>}};
-constexpr int kNumRunVariants = sizeof(kRunVariants) / sizeof(kRunVariants[0]);
 
 
 }  // namespace kvx_host
@@ -291,8 +282,6 @@ struct kvx_transition {
     int bulk_ctas[32] = {};  // resident CTAs per SM of each bulk variant
     int bulk_variant_slab = kvx_host::kSlabVariant;  // ring of slab-sized waves (KVX_BULK_CFG[_SLAB])
     int bulk_variant_tok = kvx_host::kTokVariant;    // ring of token-granular waves (KVX_BULK_CFG[_TOK])
-    int run_lsu = -1;        // token-granular waves on kvx_run_kernel (kRunVariants index), -1 = bulk ring
-    int run_ctas[4] = {};    // resident CTAs per SM of each LSU run variant
     bool use_bulk = false;   // TMA bulk mover for local destinations
     bool peer_bulk = false;  // ... and for peer (NVLink) destinations
     bool lsu256 = false;     // LSU mover with 256-bit accesses (KVX_MOVE_IMPL=lsu256)

@@ -707,47 +707,6 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     bulk_stream<kStages, kChunk, kLag, kPack>(it, smem, bars);
 }
 
-// ------------------------------------------------ LSU run mover (warp per run)
-// Experimental mover for token-granular waves (KVX_TOK_MOVER=lsu<kU>): one
-// warp per (unit, K|V) run, the run's 16-byte vectors strided over the lanes,
-// kU loads in flight per lane before the stores.  Token-major units (and
-// whole blocks of either layout: their K and V planes are contiguous) only;
-// head-major partial blocks stay with kvx_move_any_kernel (tails_only).
-constexpr int kRunThreads = 512;
-
-template <int kU>
-__global__ void __launch_bounds__(kRunThreads)
-kvx_run_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers, int32_t nlayers,
-               uint64_t block_bytes, int32_t block_tokens, int32_t fence_system) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint32_t lane = threadIdx.x & 31u;
-    const int64_t nwarps = (int64_t)gridDim.x * (kRunThreads / 32);
-    const int64_t items = 2 * (int64_t)nseg * nlayers;  // (unit, K|V)
-    for (int64_t it = (int64_t)blockIdx.x * (kRunThreads / 32) + (threadIdx.x >> 5); it < items; it += nwarps) {
-        const int64_t u = it >> 1;
-        const uint32_t kv = (uint32_t)(it & 1);
-        const int32_t layer = (int32_t)(u / nseg);
-        const Seg sg = segs[u - (int64_t)layer * nseg];
-        const LayerPtr lp = layers[layer];
-        const bool full = sg.t0 == 0 && sg.t1 == block_tokens;
-        if (sg.t1 <= sg.t0 || (lp.nh > 1 && !full)) continue;
-        const uint64_t off = full ? 0 : (uint64_t)sg.t0 * lp.run_tok;
-        const uint32_t nvec = (uint32_t)((full ? (block_bytes >> 1) : (uint64_t)(sg.t1 - sg.t0) * lp.run_tok) >> 4);
-        const uint4* src = reinterpret_cast<const uint4*>(lp.src + (uint64_t)sg.src_blk * lp.src_bs + kv * lp.src_kv + off);
-        uint4* dst = reinterpret_cast<uint4*>(lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs + kv * lp.dst_kv + off);
-        for (uint32_t b = lane; b < nvec; b += 32u * kU) {
-            uint4 v[kU];
-#pragma unroll
-            for (int k = 0; k < kU; ++k)
-                if (b + 32u * k < nvec) v[k] = ld_stream(src + b + 32u * k);
-#pragma unroll
-            for (int k = 0; k < kU; ++k)
-                if (b + 32u * k < nvec) st_stream(dst + b + 32u * k, v[k]);
-        }
-    }
-    if (fence_system) __threadfence_system();
-}
-
 // ------------------------------------------------- generic copy list
 // Activation handoff (and any batched device copy): a list of (src, dst,
 // bytes) pieces, 16-byte aligned, streamed by the same bulk engine loop.

@@ -26,8 +26,6 @@ cudaError_t preload_transition_kernels() {
         if ((e = cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       bv.stages * (int)bv.chunk)) != cudaSuccess)
             return e;
-    for (const RunVariant& rv : kRunVariants)
-        if ((e = cudaFuncGetAttributes(&a, (const void*)rv.fn)) != cudaSuccess) return e;
     return e;
 }
 }  // namespace kvx_host
@@ -163,14 +161,6 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         t->lsu256 = impl && std::string(impl) == "lsu256";
         const char* pb = getenv("KVX_PEER_BULK");
         t->peer_bulk = t->use_bulk && !(pb && std::string(pb) == "0");
-        for (int v = 0; v < kNumRunVariants; ++v) {
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kRunVariants[v].fn, kvx::kRunThreads, 0) != cudaSuccess)
-                return bail(fail(KVX_ECUDA, "run mover occupancy"));
-            t->run_ctas[v] = std::max(1, occ);
-        }
-        if (const char* tm = getenv("KVX_TOK_MOVER"))  // experiment: lsu4 | lsu8 | lsu20
-            for (int v = 0; v < kNumRunVariants; ++v)
-                if (std::string(tm) == "lsu" + std::to_string(kRunVariants[v].u)) t->run_lsu = v;
     }
 
     if (d->stream) {
@@ -380,28 +370,10 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         // the 70B-GQA slab waves -- 64 KiB blocks, partial tails pulling the
         // average to 65,015 B -- on the token ring.)
         const bool slab = 2 * full_tokens >= tokens;
-        const bool run_wave = !slab && t->run_lsu >= 0 && !t->transpose;
         if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
             kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                 (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0);
-        } else if (run_wave) {
-            // token-granular wave on the LSU warp-per-run mover (experiment, KVX_TOK_MOVER)
-            const RunVariant& rv = kRunVariants[t->run_lsu];
-            int64_t full_r = (int64_t)t->num_sms * t->run_ctas[t->run_lsu];
-            if (const char* tg = getenv("KVX_TOK_GRID")) full_r = std::max<int64_t>(1, atoll(tg));
-            if (t->max_ctas > 0) full_r = std::min<int64_t>(full_r, t->max_ctas);
-            const unsigned grid_r = (unsigned)std::max<int64_t>(
-                1, std::min<int64_t>(cdiv64(2 * units, kvx::kRunThreads / 32), full_r));
-            rv.fn<<<grid_r, kvx::kRunThreads, 0, t->stream>>>(t->d_segs, (int32_t)nseg, t->d_layers,
-                                                             t->n_local_layers, block_bytes(t->g),
-                                                             t->g.block_tokens, t->has_peer_dst ? 1 : 0);
-            if (t->head_tails) {  // head-major partial blocks: the row mover, after it on the stream
-                KVX_LAUNCHED();
-                kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
-                    t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
-                    (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 1, t->has_peer_dst ? 1 : 0);
-            }
         } else if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
             const int vi = slab ? t->bulk_variant_slab : t->bulk_variant_tok;
             const BulkVariant& bv = kBulkVariants[vi];

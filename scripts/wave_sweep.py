@@ -41,15 +41,11 @@ def main():
     peak = bench.peaks()[0]
     for v in args.variants.split(","):
         for grid in [int(x) for x in args.grids.split(",")]:
-            if v.startswith("lsu"):  # LSU warp-per-run token mover (kvx_run_kernel, experiment)
-                os.environ["KVX_TOK_MOVER"] = v
-                os.environ["KVX_TOK_GRID"] = str(grid)
+            os.environ["KVX_BULK_CFG_" + args.kind.upper()] = v
+            if args.kind == "tok":
+                os.environ["KVX_BULK_GRID_TOK"] = str(grid)
             else:
-                os.environ["KVX_BULK_CFG_" + args.kind.upper()] = v
-                if args.kind == "tok":
-                    os.environ["KVX_BULK_GRID_TOK"] = str(grid)
-                else:
-                    os.environ["KVX_BULK_GRID"] = str(grid)
+                os.environ["KVX_BULK_GRID"] = str(grid)
             times = []
             for s in range(args.steps + 2):
                 tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, 0, plan.N,
@@ -71,9 +67,27 @@ def main():
                               "move_ms_by_wave": [round(x, 4) for x in ms],
                               "frac_by_wave": [round(b / (m * 1e-3) / 1e9 / peak, 4) for b, m in zip(by, ms)]}),
                   flush=True)
-            for k in ("KVX_BULK_CFG_TOK", "KVX_BULK_CFG_SLAB", "KVX_BULK_GRID_TOK", "KVX_BULK_GRID", "KVX_TOK_MOVER",
-                      "KVX_TOK_GRID"):
+            for k in ("KVX_BULK_CFG_TOK", "KVX_BULK_CFG_SLAB", "KVX_BULK_GRID_TOK", "KVX_BULK_GRID"):
                 os.environ.pop(k, None)
+    if args.kind == "tok":
+        # control: one contiguous copy of the final wave's bytes (read side), so the
+        # token wave's scatter cost is separated from what a launch of this size costs
+        fin = [w for w in t.waves if w.final] or t.waves[-1:]
+        nbytes = int((fin[0].hi - fin[0].lo).clip(min=0).sum()) * 2 * plan.token_bytes * plan.L
+        a = torch.empty(nbytes // 2, dtype=torch.bfloat16, device="cuda")
+        b = torch.empty_like(a)
+        best = []
+        for _ in range(20):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            b.copy_(a)
+            e1.record()
+            torch.cuda.synchronize()
+            best.append(e0.elapsed_time(e1))
+        ms = statistics.median(best)
+        print(json.dumps({"config": args.config, "control": "contiguous torch copy of the final wave's bytes",
+                          "bytes_read": nbytes, "ms": round(ms, 4),
+                          "frac": round(2 * nbytes / (ms * 1e-3) / 1e9 / peak, 4)}), flush=True)
     for p in old_pools + new_pools:
         p.close()
 

@@ -172,22 +172,3 @@ def test_c5_adaptive_chain_full_shape(gpu_count):
     assert ran >= 8
 
 
-
-@pytest.mark.parametrize("mover", ["lsu4", "lsu8", "lsu20"])
-@pytest.mark.parametrize("name,heads,dim", [("criterion12", 2, 64), ("delta_rounds_cap", 2, 64),
-                                            ("engine_mid_decode", 8, 128), ("bursty_repeated", 1, 8)])
-def test_token_waves_on_the_lsu_run_mover_bit_exact(gpu_count, monkeypatch, mover, name, heads, dim):
-    """KVX_TOK_MOVER=lsu*: token-granular waves (delta / final) on the warp-per-run
-    LSU mover (kvx_run_kernel) -- every destination byte, table and commit as the oracle."""
-    monkeypatch.setenv("KVX_TOK_MOVER", mover)
-    scn = W.load_golden(name)
-    for t in scn.transitions:
-        case = GpuCase(scn, t, heads, dim)
-        try:
-            case.run_ctl()
-            case.compare_tables()
-            case.compare_bytes()
-            if t.outcome == "commit":
-                _commit_and_compare(case)
-        finally:
-            case.close()
