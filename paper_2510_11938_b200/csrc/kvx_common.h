@@ -182,6 +182,10 @@ constexpr int kSlabVariant = 2;  // 3 x 64 KiB, one chunk per slot
 constexpr int kTokVariant = 7;
 constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
 
+// TMA transposer ring (kvx_tmap_kernel): slots of up to kTmapSlot bytes
+constexpr int kTmapStages = 6, kTmapLag = 2;
+constexpr uint32_t kTmapSlot = 32768;
+
 
 
 }  // namespace kvx_host
@@ -304,6 +308,12 @@ struct kvx_transition {
     int32_t n_pull_layers = 0;  // of which pulled (read from a peer's old pool)
     bool transpose = false;     // some layer pairs a token-major with a head-major pool
     bool head_tails = false;    // head-major to head-major layers (H > 1): partial blocks go to the row mover
+    // TMA tensor-map transposer (kvx_tmap_kernel) for the whole blocks of a
+    // transposing transition: one map per local layer over its token-major side
+    CUtensorMap* d_maps = nullptr;
+    size_t maps_bytes = 0;
+    int tmap_t2h = -1;          // -1: not used; 1: token-major -> head-major; 0: the reverse
+    int tmap_hc = 0;            // heads per box
     cudaStream_t side = nullptr;  // side stream (arena-cached): head-major tails, the commit kernel
     cudaEvent_t ev_side_commit = nullptr;
     int last_plan_slot = -1;      // h_wave_free[slot] recorded after the most recent plan kernel

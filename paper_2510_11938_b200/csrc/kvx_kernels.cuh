@@ -39,6 +39,7 @@
 // linkage (static), templates are instantiated where used.
 
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (the type only; no driver calls here)
 #include <cuda_runtime.h>
 
 namespace kvx {
@@ -370,7 +371,8 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
 // (BLOCKS, KV_PLANES) and head-major (HEADS) pools (tails_only = 0), and for
 // the partial blocks of head-major-to-head-major moves, whose 2*H short runs
 // would starve the bulk mover's single issuing thread (tails_only = 1: full
-// blocks are left to kvx_bulk_kernel).  Vectors of one row go to consecutive
+// blocks are left to kvx_bulk_kernel; tails_only = 2: the partial blocks of a
+// transposing wave whose whole blocks go to kvx_tmap_kernel).  Vectors of one row go to consecutive
 // threads; rows are ordered tokens-inner when the source is head-major (its
 // contiguous direction), heads-inner otherwise.  4 independent 16-byte loads
 // in flight per thread.
@@ -387,7 +389,9 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
         const int32_t layer = (int32_t)(u / nseg);
         const Seg sg = segs[u - (int64_t)layer * nseg];
         const LayerPtr lp = layers[layer];
-        if (tails_only && (lp.nh <= 1 || (sg.t0 == 0 && sg.t1 == block_tokens))) continue;
+        const bool full = sg.t0 == 0 && sg.t1 == block_tokens;
+        if (tails_only == 1 && (lp.nh <= 1 || full)) continue;
+        if (tails_only == 2 && full) continue;  // whole blocks: kvx_tmap_kernel
         const char* sb = lp.src + (uint64_t)sg.src_blk * lp.src_bs;
         char* db = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs;
         const uint32_t ntok = (uint32_t)(sg.t1 - sg.t0);
@@ -705,6 +709,142 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     it.chunk = kChunk;
     if (!it.load_unit()) return;
     bulk_stream<kStages, kChunk, kLag, kPack>(it, smem, bars);
+}
+
+// ------------------------------------------- TMA tensor-map transposer
+// Whole blocks between a token-major pool (per K|V plane [B][H][D]) and a
+// head-major one ([H][B][D]).  The token-major side of every layer is
+// described by a 5-D tensor map over (D, B, H, K|V, block) -- dims ordered
+// head-outer with the pool's real strides -- so one box (D, B, hc) lands in
+// shared memory as a head-major tile [hc][B][D]: the bulk engine does the
+// transpose, no thread touches the payload.  The head-major side is a plain
+// contiguous range of hc head planes.
+//   t2h (token-major -> head-major): tensor load, 1-D bulk store
+//   h2t (head-major -> token-major): 1-D bulk load, tensor store
+// A box that runs past the last head is zero-filled on load (and only the
+// valid heads are stored) or clipped on store.  Partial blocks stay with the
+// row mover (kvx_move_any_kernel, tails_only = 2).  Same ring discipline as
+// bulk_stream: kStages slots, refill once the store kLag slots back has read
+// its slot.
+__device__ __forceinline__ void tmap_g2s(void* smem, const CUtensorMap* map, int32_t c2, int32_t c3, int32_t c4,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5, %6}], [%7];" ::"r"(smem_u32(smem)),
+        "l"(map), "r"(0), "r"(0), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tmap_s2g(const CUtensorMap* map, int32_t c2, int32_t c3, int32_t c4, const void* smem) {
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                     map),
+                 "r"(0), "r"(0), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(smem))
+                 : "memory");
+}
+
+template <int kStages, int kLag>
+__global__ void __launch_bounds__(32)
+kvx_tmap_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers, int32_t nlayers,
+                const CUtensorMap* __restrict__ maps, int32_t heads, int32_t hc, uint32_t head_plane,
+                int32_t block_tokens, int32_t t2h) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[kStages];
+    if (threadIdx.x != 0) return;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint32_t slot = (uint32_t)hc * head_plane;  // bytes of one full box
+    const int32_t nchunk = (heads + hc - 1) / hc;
+    const int64_t pieces_per_unit = 2 * (int64_t)nchunk;
+    const int64_t units = (int64_t)nseg * nlayers;
+    // walk (unit, K|V, head chunk) of this CTA's units; full blocks only
+    int64_t u = blockIdx.x;
+    int64_t p = 0;  // piece within the unit
+    struct Piece {
+        const CUtensorMap* map;
+        const char* hm_src;  // head-major side (h2t: load from; t2h: store to)
+        char* hm_dst;
+        int32_t c2, c3, c4;
+        uint32_t bytes;  // valid head-plane bytes
+    };
+    Piece cur{};
+    bool unit_ok = false;
+    LayerPtr lp{};
+    Seg sg{};
+    int32_t layer = 0;
+    auto next = [&](Piece* out) -> bool {
+        for (;;) {
+            if (u >= units) return false;
+            if (!unit_ok || p == pieces_per_unit) {
+                if (unit_ok) u += gridDim.x;
+                p = 0;
+                unit_ok = false;
+                if (u >= units) return false;
+                layer = (int32_t)(u / nseg);
+                sg = segs[u - (int64_t)layer * nseg];
+                lp = layers[layer];
+                if (!(sg.t0 == 0 && sg.t1 == block_tokens)) {  // partial: the row mover's
+                    u += gridDim.x;
+                    continue;
+                }
+                unit_ok = true;
+            }
+            const int32_t kv = (int32_t)(p / nchunk), ch = (int32_t)(p % nchunk);
+            ++p;
+            const int32_t h0 = ch * hc;
+            const int32_t nh = heads - h0 < hc ? heads - h0 : hc;
+            out->map = maps + layer;
+            out->c2 = h0;
+            out->c3 = kv;
+            out->c4 = t2h ? sg.src_blk : sg.dst_blk;
+            out->bytes = (uint32_t)nh * head_plane;
+            if (t2h) {
+                out->hm_dst = lp.dst + (uint64_t)sg.dst_blk * lp.dst_bs + kv * lp.dst_kv + (uint64_t)h0 * lp.dst_hs;
+                out->hm_src = nullptr;
+            } else {
+                out->hm_src = lp.src + (uint64_t)sg.src_blk * lp.src_bs + kv * lp.src_kv + (uint64_t)h0 * lp.src_hs;
+                out->hm_dst = nullptr;
+            }
+            return true;
+        }
+    };
+    for (int i = 0; i < kStages; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    Piece pend[kStages];
+    bool have = next(&cur);
+    auto fill = [&](int st) -> bool {
+        if (!have) return false;
+        pend[st] = cur;
+        unsigned char* s = smem + (size_t)st * slot;
+        if (t2h) {
+            mbar_expect_tx(&bars[st], slot);  // the whole box arrives (heads past the end zero-filled)
+            tmap_g2s(s, cur.map, cur.c2, cur.c3, cur.c4, &bars[st]);
+        } else {
+            mbar_expect_tx(&bars[st], cur.bytes);
+            bulk_g2s(s, cur.hm_src, cur.bytes, &bars[st]);
+        }
+        have = next(&cur);
+        return true;
+    };
+    int64_t issued = 0, stored = 0;
+    for (int st = 0; st < kStages; ++st) {
+        if (!fill(st)) break;
+        ++issued;
+    }
+    while (stored < issued) {
+        const int st = (int)(stored % kStages);
+        mbar_wait(&bars[st], (uint32_t)((stored / kStages) & 1));
+        const Piece& pc = pend[st];
+        unsigned char* s = smem + (size_t)st * slot;
+        if (t2h)
+            bulk_s2g(pc.hm_dst, s, pc.bytes);
+        else
+            tmap_s2g(pc.map, pc.c2, pc.c3, pc.c4, s);  // heads past the end are clipped
+        bulk_commit();
+        ++stored;
+        if (have && stored >= kLag) {
+            bulk_wait_read<kLag - 1>();
+            if (fill((int)((stored - kLag) % kStages))) ++issued;
+        }
+    }
+    bulk_wait_all();
 }
 
 // ------------------------------------------------- generic copy list

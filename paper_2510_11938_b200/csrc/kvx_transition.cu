@@ -10,7 +10,34 @@
 // block table without exchanging it.
 #include "kvx_common.h"
 
+#include <cudaTypedefs.h>
+
 using namespace kvx_host;
+
+namespace {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// The token-major side of one layer as a 5-D tensor (D, B, H, K|V, block),
+// dims ordered head-outer so a (D, B, hc) box is a head-major smem tile.
+struct TmSide {
+    char* base;
+    int32_t num_blocks;
+    uint64_t ts, hs, kv, bs;
+};
+}  // namespace
 
 namespace kvx_host {
 cudaError_t preload_transition_kernels() {
@@ -26,6 +53,10 @@ cudaError_t preload_transition_kernels() {
         if ((e = cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       bv.stages * (int)bv.chunk)) != cudaSuccess)
             return e;
+    if ((e = cudaFuncSetAttribute(kvx::kvx_tmap_kernel<kTmapStages, kTmapLag>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kTmapStages * (int)kTmapSlot)) !=
+        cudaSuccess)
+        return e;
     return e;
 }
 }  // namespace kvx_host
@@ -214,6 +245,8 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     // Per-layer slab bases for the layers this GPU sources.
     std::vector<kvx::LayerPtr> layers;
     std::vector<uint8_t> layer_is_peer;
+    std::vector<TmSide> tm_side;  // per layer: the token-major pool of a transposing pair
+    std::vector<int> tm_dir;      // 1: src token-major -> dst head-major, 0: the reverse, -1: same family
     for (int32_t l = 0; l < g.num_layers; ++l) {
         const int so = stage_of_layer(ob, l), sn = stage_of_layer(nb, l);
         kvx_pool* src = t->old_pools[(size_t)so];
@@ -246,15 +279,67 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
                           (uint32_t)(heads_runs ? src->head_bytes() : token_bytes(g)),
                           heads_runs ? (uint32_t)g.num_kv_heads : 1u});
         layer_is_peer.push_back(remote(dst) || remote(src) ? 1 : 0);
+        {
+            const kvx_pool* tmp = src->head_major() ? dst : src;  // token-major side
+            const size_t ll = (size_t)(l - (tmp == src ? stage_begin(ob, so) : stage_begin(nb, sn)));
+            tm_side.push_back({tmp->layer_base[ll], tmp->num_blocks, tmp->tok_stride(), tmp->head_stride(),
+                               tmp->kv_stride(), tmp->blk_stride()});
+            tm_dir.push_back(src->head_major() == dst->head_major() ? -1 : (dst->head_major() ? 1 : 0));
+        }
         if (remote(dst)) t->has_peer_dst = true;
     }
     // peer-destination layers first (see kvx_bulk_kernel's CTA split)
     {
         std::vector<kvx::LayerPtr> peer, local;
-        for (size_t i = 0; i < layers.size(); ++i) (layer_is_peer[i] ? peer : local).push_back(layers[i]);
+        std::vector<TmSide> tpeer, tlocal;
+        std::vector<int> dpeer, dlocal;
+        for (size_t i = 0; i < layers.size(); ++i) {
+            (layer_is_peer[i] ? peer : local).push_back(layers[i]);
+            (layer_is_peer[i] ? tpeer : tlocal).push_back(tm_side[i]);
+            (layer_is_peer[i] ? dpeer : dlocal).push_back(tm_dir[i]);
+        }
         t->n_peer_layers = (int32_t)peer.size();
         layers = peer;
         layers.insert(layers.end(), local.begin(), local.end());
+        tm_side = tpeer;
+        tm_side.insert(tm_side.end(), tlocal.begin(), tlocal.end());
+        tm_dir = dpeer;
+        tm_dir.insert(tm_dir.end(), dlocal.begin(), dlocal.end());
+    }
+    // Whole blocks of a transposing transition on the TMA transposer: every
+    // local layer pairs the two families in the same direction, the geometry
+    // fits one box (D <= 256 elements, a head plane <= one ring slot) and the
+    // driver encodes the maps; else everything stays on the row mover.
+    if (t->transpose && !layers.empty() && !(getenv("KVX_TMAP") && std::string(getenv("KVX_TMAP")) == "0")) {
+        const uint64_t head_plane = (uint64_t)g.block_tokens * g.head_dim * g.elem_bytes;
+        bool ok = tm_dir[0] >= 0 && g.head_dim <= 256 && g.block_tokens <= 256 && head_plane <= kTmapSlot &&
+                  (g.elem_bytes == 1 || g.elem_bytes == 2 || g.elem_bytes == 4) &&
+                  ((uint64_t)g.head_dim * g.elem_bytes) % 16 == 0 && tmap_encode() != nullptr;
+        for (int dir : tm_dir) ok = ok && dir == tm_dir[0];
+        std::vector<CUtensorMap> maps(layers.size());
+        const int hc = (int)std::min<uint64_t>((uint64_t)g.num_kv_heads, kTmapSlot / std::max<uint64_t>(1, head_plane));
+        for (size_t i = 0; ok && i < layers.size(); ++i) {
+            const TmSide& s = tm_side[i];
+            const cuuint64_t dims[5] = {(cuuint64_t)g.head_dim, (cuuint64_t)g.block_tokens, (cuuint64_t)g.num_kv_heads, 2,
+                                        (cuuint64_t)s.num_blocks};
+            const cuuint64_t strides[4] = {s.ts, s.hs, s.kv, s.bs};
+            const cuuint32_t box[5] = {(cuuint32_t)g.head_dim, (cuuint32_t)g.block_tokens, (cuuint32_t)hc, 1, 1};
+            const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+            const CUtensorMapDataType dt = g.elem_bytes == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                           : g.elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                                               : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+            ok = tmap_encode()(&maps[i], dt, 5, s.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+        if (ok) {
+            t->maps_bytes = sizeof(CUtensorMap) * maps.size();
+            if (kvx::Arena::of(d->device).dev_alloc((void**)&t->d_maps, t->maps_bytes) != cudaSuccess ||
+                cudaMemcpyAsync(t->d_maps, maps.data(), t->maps_bytes, cudaMemcpyHostToDevice, t->stream) != cudaSuccess)
+                return bail(fail(KVX_ECUDA, "tensor map upload"));
+            t->tmap_t2h = tm_dir[0];
+            t->tmap_hc = hc;
+        }
     }
     t->n_local_layers = (int32_t)layers.size();
     if (!layers.empty()) {
@@ -370,7 +455,30 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         // the 70B-GQA slab waves -- 64 KiB blocks, partial tails pulling the
         // average to 65,015 B -- on the token ring.)
         const bool slab = 2 * full_tokens >= tokens;
-        if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
+        if (t->transpose && t->tmap_t2h >= 0 && full_tokens > 0) {
+            // whole blocks: the TMA transposer; partial blocks: the row mover beside it
+            // on the side stream (joined before the wave's end event)
+            const uint32_t head_plane = (uint32_t)(t->g.block_tokens * t->g.head_dim * t->g.elem_bytes);
+            int64_t tgrid = std::min<int64_t>(units, 96);
+            if (const char* tg = getenv("KVX_TMAP_GRID")) tgrid = std::max<int64_t>(1, atoll(tg));
+            if (t->max_ctas > 0) tgrid = std::min<int64_t>(tgrid, t->max_ctas);
+            kvx::kvx_tmap_kernel<kTmapStages, kTmapLag><<<(unsigned)std::max<int64_t>(1, tgrid), 32,
+                                                          kTmapStages * (size_t)t->tmap_hc * head_plane, t->stream>>>(
+                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->d_maps, t->g.num_kv_heads, t->tmap_hc,
+                head_plane, t->g.block_tokens, t->tmap_t2h);
+            if (full_tokens < tokens) {
+                KVX_LAUNCHED();
+                cudaStream_t ts = t->max_ctas > 0 ? t->stream : t->side;
+                if (ts == t->side) KVX_CUDA(cudaStreamWaitEvent(t->side, t->h_wave_free[slot], 0));
+                kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, ts>>>(
+                    t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
+                    (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 2, t->has_peer_dst ? 1 : 0);
+                if (ts == t->side) {
+                    KVX_CUDA(cudaEventRecord(t->ev_join, t->side));
+                    KVX_CUDA(cudaStreamWaitEvent(t->stream, t->ev_join, 0));
+                }
+            }
+        } else if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
             kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
                 t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                 (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0);
@@ -687,6 +795,7 @@ int kvx_destroy(kvx_transition* t) {
     A.dev_free(t->d_dst_bt, t->bt_bytes);
     A.dev_free(t->d_synced_hi, sizeof(int64_t) * (size_t)t->max_requests);
     A.dev_free(t->d_layers, t->layers_bytes);
+    A.dev_free(t->d_maps, t->maps_bytes);
     A.dev_free(t->d_wave, t->wave_bytes);
     A.dev_free(t->d_segs, sizeof(kvx::Seg) * (size_t)t->seg_cap);
     A.dev_free(t->d_live, (size_t)t->max_requests);

@@ -124,7 +124,20 @@ def test_lsu_movers_convert_layouts(gpu_count, impl, monkeypatch):
 def test_head_major_layouts(gpu_count, pair, impl, monkeypatch):
     """Head-major pools on every stage of one side or both: head-major to
     head-major through run copies (2*H runs per partial block), the rest
-    through the transposing mover."""
+    through the transposing movers (whole blocks on the TMA tensor-map
+    transposer, partial blocks on the row mover)."""
     monkeypatch.setenv("KVX_MOVE_IMPL", impl)
     for seed in (11, 12, 13):
+        test_random_layouts_bit_exact(gpu_count, seed, uniform=pair)
+
+
+@pytest.mark.parametrize("pair", [(0, 2), (2, 0), (1, 2), (2, 1)],
+                         ids=["blocks-to-heads", "heads-to-blocks", "planes-to-heads", "heads-to-planes"])
+@pytest.mark.parametrize("tmap", ["on", "off"])
+def test_transposes_tmap_and_row_mover(gpu_count, pair, tmap, monkeypatch):
+    """Every transposing pairing with the TMA tensor-map transposer for whole
+    blocks (default) and without it (KVX_TMAP=0: the row mover moves all)."""
+    if tmap == "off":
+        monkeypatch.setenv("KVX_TMAP", "0")
+    for seed in range(20, 28):
         test_random_layouts_bit_exact(gpu_count, seed, uniform=pair)
