@@ -98,3 +98,21 @@ def test_patched_engine_cases(gpu_count):
     out = _run("test_kvx_patched")
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
     assert "4 passed | 0 failed" in out.stdout
+
+
+@pytest.mark.gpu
+def test_measured_time_mode_c3_real_geometry(gpu_count):
+    """C3 (13B 8->4) through the patched engine at the real KV geometry: in
+    measured mode wave 0's KvSyncComplete fires at begin + the B200's measured
+    wave time, well before the reference's modelled 18.67 ms (kv_sync_bw 900 GB/s)."""
+    env = {"PIPESIM_KVX": "measured"}
+    out = subprocess.run([_bin("engine_patched_run"), "llama13b_8to4"], capture_output=True, text=True,
+                         timeout=900, env=dict(os.environ, **env), cwd=B)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["refactor_commits"] == 1 and r["kv_violations"] == 0 and r["mismatched_words"] == 0
+    assert "40x128" in r["geometries"]
+    w0 = r["waves"][0]
+    assert w0["scheduled_ms"] == w0["measured_ms"] < w0["modelled_ms"]
+    first_sync = r["kv_sync_complete_ms"][0][1][0]
+    assert first_sync == w0["issued_ms"] + w0["measured_ms"]
