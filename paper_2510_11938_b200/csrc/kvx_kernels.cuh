@@ -149,6 +149,10 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
                 int32_t* __restrict__ dst_bt, int64_t* __restrict__ synced_hi, int32_t max_blocks,
                 int32_t block_tokens, int32_t alloc_base, const int32_t* __restrict__ pop_stack,
                 Seg* __restrict__ segs, int32_t src_cap, int32_t dst_cap, int32_t* __restrict__ err) {
+    // let the mover (launched behind with programmatic stream serialization)
+    // become resident now; it waits (griddepcontrol.wait) for this grid's
+    // completion before it reads the segments
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int64_t B = block_tokens;
     int2 carry = make_int2(0, 0);
     for (int32_t base = 0; base < n; base += kPlanThreads) {

@@ -433,7 +433,11 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         t->g.block_tokens, t->bm ? t->bm->top : t->alloc, t->bm ? t->bm->d_stack : nullptr, t->d_segs,
         t->src_cap, t->dst_num_blocks, t->d_err);
     KVX_LAUNCHED();
-    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
+    // KVX_TIGHT (experiment): 1 = no per-launch timing events around the mover,
+    // 2 = also record the staging-free event after the mover, so the plan kernel
+    // and the mover are adjacent in the stream (programmatic dependent launch)
+    static const int tight = getenv("KVX_TIGHT") ? atoi(getenv("KVX_TIGHT")) : 0;
+    if (tight < 2) KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     t->last_plan_slot = slot;  // this event now marks the table / synced marks as final
     t->handoff_since_plan = false;
     if (t->bm && new_blocks > 0) KVX_CUDA(bm_order_after(t->bm, t->stream));
@@ -443,12 +447,14 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         if (t->max_ctas > 0) full = std::min<int64_t>(full, t->max_ctas);  // sharing HBM with serving
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full));
         std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-        KVX_CUDA(kvx::Arena::of(t->device).event(&ev.first, true));
-        KVX_CUDA(kvx::Arena::of(t->device).event(&ev.second, true));
-        t->move_ev.push_back(ev);
+        if (!tight) {
+            KVX_CUDA(kvx::Arena::of(t->device).event(&ev.first, true));
+            KVX_CUDA(kvx::Arena::of(t->device).event(&ev.second, true));
+            t->move_ev.push_back(ev);
+        }
         t->move_bytes.push_back(2ull * (uint64_t)tokens * 2ull * token_bytes(t->g) *
                                 (uint64_t)t->n_local_layers);
-        KVX_CUDA(cudaEventRecord(ev.first, t->stream));
+        if (!tight) KVX_CUDA(cudaEventRecord(ev.first, t->stream));
         // A wave is slab-sized when most of its bytes sit in whole blocks
         // (each one contiguous run of 2 * block_tokens * token_bytes), else
         // token-granular.  (Round 1 used the average run >= 64 KiB, which put
@@ -555,8 +561,9 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                 token_bytes(t->g), t->g.block_tokens, t->has_peer_dst ? 1 : 0);
         }
         KVX_LAUNCHED();
-        KVX_CUDA(cudaEventRecord(ev.second, t->stream));
+        if (!tight) KVX_CUDA(cudaEventRecord(ev.second, t->stream));
     }
+    if (tight >= 2) KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     KVX_CUDA(cudaEventRecord(t->ev_end, t->stream));
     // Commit the mirror only once every launch was accepted.
     for (int32_t i = 0; i < n; ++i)
