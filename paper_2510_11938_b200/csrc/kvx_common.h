@@ -157,7 +157,7 @@ int ensure_loaded(int device);
 // or V row per run) kTokVariant; KVX_BULK_CFG pins one variant for both,
 // KVX_BULK_CFG_SLAB / KVX_BULK_CFG_TOK one kind.
 using BulkFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, uint64_t, int32_t,
-                        int32_t, int32_t);
+                        int32_t, int32_t, unsigned long long*, unsigned long long*);
 struct BulkVariant {
     int stages;
     uint32_t chunk;
@@ -343,9 +343,17 @@ struct kvx_transition {
     // timing
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     bool timing_open = false;
-    // one (start, end) event pair per move-kernel launch of this handle
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> move_ev;
+    // per move-kernel launch of this handle: its duration from the bulk mover's
+    // own %globaltimer slots (timer >= 0), else a (start, end) event pair
+    struct MoveRec {
+        cudaEvent_t a = nullptr, b = nullptr;
+        int32_t timer = -1;
+    };
+    std::vector<MoveRec> move_rec;
     std::vector<uint64_t> move_bytes;
+    static constexpr int32_t kTimerSlots = 64;
+    unsigned long long* d_timer = nullptr;  // [start x kTimerSlots | end x kTimerSlots]
+    int32_t n_timers = 0;
 
     // activation handoff pieces (grown on demand, freed at destroy)
     kvx::Piece* d_pieces = nullptr;

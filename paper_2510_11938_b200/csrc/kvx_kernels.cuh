@@ -665,16 +665,26 @@ __device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint6
 // a wave mixes them with local layers, CTAs [0, peer_ctas) stream only the
 // peer units and the rest only the local ones, so the NVLink-bound and the
 // HBM-bound traffic overlap instead of running layer after layer.
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// t_start / t_end (optional): the launch's own duration, first CTA start to
+// last CTA end on %globaltimer (atomicMin / atomicMax) -- kvx_move_timings
+// reads it, so no timing events sit in the stream on the stall path.
 template <int kStages, uint32_t kChunk, int kLag = 2, int kPack = 1>
 __global__ void __launch_bounds__(kBulkThreads)
 kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
                 int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
-                int32_t n_peer, int32_t peer_ctas) {
+                int32_t n_peer, int32_t peer_ctas, unsigned long long* t_start, unsigned long long* t_end) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[kStages];
     __shared__ UnitDesc desc[2][kDescBatch];
     (void)token_bytes;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the plan kernel's segments
+    if (t_start && threadIdx.x == 0) atomicMin(t_start, global_ns());
     // this CTA's units: u0, u0 + ustep, ... < units
     int64_t u0, ustep, units;
     const int64_t split = (int64_t)nseg * n_peer;
@@ -711,8 +721,8 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     it.my_units = my_units;
     it.nbatch = nbatch;
     it.chunk = kChunk;
-    if (!it.load_unit()) return;
-    bulk_stream<kStages, kChunk, kLag, kPack>(it, smem, bars);
+    if (it.load_unit()) bulk_stream<kStages, kChunk, kLag, kPack>(it, smem, bars);
+    if (t_end) atomicMax(t_end, global_ns());  // after bulk_wait_all: this CTA's stores landed
 }
 
 // ------------------------------------------- TMA tensor-map transposer

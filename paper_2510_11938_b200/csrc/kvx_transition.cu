@@ -235,6 +235,11 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         t->seg_cap = (int64_t)(kvx::size_class(sizeof(kvx::Seg) * cells) / sizeof(kvx::Seg));
         t->commit_i32_cap = (int64_t)(d->max_requests + 1) + 2 * (int64_t)cells;
         t->h_commit_bytes = 32 + sizeof(int32_t) * (size_t)t->commit_i32_cap;
+        constexpr size_t kTimerBytes = sizeof(unsigned long long) * kvx_transition::kTimerSlots;
+        if (A.dev_alloc((void**)&t->d_timer, 2 * kTimerBytes) != cudaSuccess ||
+            cudaMemsetAsync(t->d_timer, 0xff, kTimerBytes, t->stream) != cudaSuccess ||  // starts: +inf
+            cudaMemsetAsync(t->d_timer + kvx_transition::kTimerSlots, 0, kTimerBytes, t->stream) != cudaSuccess)
+            return bail(fail(KVX_ENOSPC, "timer slots"));
         if (A.dev_alloc((void**)&t->d_segs, sizeof(kvx::Seg) * (size_t)t->seg_cap) != cudaSuccess ||
             A.dev_alloc((void**)&t->d_commit_i32, sizeof(int32_t) * (size_t)t->commit_i32_cap) != cudaSuccess ||
             A.host_alloc((void**)&t->h_commit, t->h_commit_bytes) != cudaSuccess ||
@@ -433,11 +438,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         t->g.block_tokens, t->bm ? t->bm->top : t->alloc, t->bm ? t->bm->d_stack : nullptr, t->d_segs,
         t->src_cap, t->dst_num_blocks, t->d_err);
     KVX_LAUNCHED();
-    // KVX_TIGHT (experiment): 1 = no per-launch timing events around the mover,
-    // 2 = also record the staging-free event after the mover, so the plan kernel
-    // and the mover are adjacent in the stream (programmatic dependent launch)
-    static const int tight = getenv("KVX_TIGHT") ? atoi(getenv("KVX_TIGHT")) : 0;
-    if (tight < 2) KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
+    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     t->last_plan_slot = slot;  // this event now marks the table / synced marks as final
     t->handoff_since_plan = false;
     if (t->bm && new_blocks > 0) KVX_CUDA(bm_order_after(t->bm, t->stream));
@@ -446,15 +447,21 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         int64_t full = (int64_t)t->num_sms * t->move_ctas_per_sm;
         if (t->max_ctas > 0) full = std::min<int64_t>(full, t->max_ctas);  // sharing HBM with serving
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, full));
-        std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-        if (!tight) {
-            KVX_CUDA(kvx::Arena::of(t->device).event(&ev.first, true));
-            KVX_CUDA(kvx::Arena::of(t->device).event(&ev.second, true));
-            t->move_ev.push_back(ev);
+        // Timing: the bulk mover times itself (%globaltimer slots; timing events
+        // around it cost ~7 us of stall, profiles/r02m_ab_tight.jsonl); the other
+        // movers get an event pair.
+        const bool bulk_path = !t->transpose && t->use_bulk && (!t->has_peer_dst || t->peer_bulk);
+        kvx_transition::MoveRec rec;
+        if (bulk_path && t->d_timer && t->n_timers < kvx_transition::kTimerSlots) {
+            rec.timer = t->n_timers++;
+        } else {
+            KVX_CUDA(kvx::Arena::of(t->device).event(&rec.a, true));
+            KVX_CUDA(kvx::Arena::of(t->device).event(&rec.b, true));
+            KVX_CUDA(cudaEventRecord(rec.a, t->stream));
         }
+        t->move_rec.push_back(rec);
         t->move_bytes.push_back(2ull * (uint64_t)tokens * 2ull * token_bytes(t->g) *
                                 (uint64_t)t->n_local_layers);
-        if (!tight) KVX_CUDA(cudaEventRecord(ev.first, t->stream));
         // A wave is slab-sized when most of its bytes sit in whole blocks
         // (each one contiguous run of 2 * block_tokens * token_bytes), else
         // token-granular.  (Round 1 used the average run >= 64 KiB, which put
@@ -530,7 +537,9 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             KVX_CUDA(cudaLaunchKernelEx(&cfg, bv.fn, (const kvx::Seg*)t->d_segs, (int32_t)nseg,
                                         (const kvx::LayerPtr*)t->d_layers, t->n_local_layers,
                                         block_bytes(t->g), token_bytes(t->g), t->g.block_tokens,
-                                        t->n_peer_layers, peer_ctas));
+                                        t->n_peer_layers, peer_ctas,
+                                        rec.timer >= 0 ? t->d_timer + rec.timer : nullptr,
+                                        rec.timer >= 0 ? t->d_timer + kvx_transition::kTimerSlots + rec.timer : nullptr));
             if (t->head_tails && t->max_ctas > 0) {
                 // capped wave (HBM shared with serving): the tail mover runs after the
                 // bulk mover on the same stream, so the wave never holds more than
@@ -561,9 +570,8 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                 token_bytes(t->g), t->g.block_tokens, t->has_peer_dst ? 1 : 0);
         }
         KVX_LAUNCHED();
-        if (!tight) KVX_CUDA(cudaEventRecord(ev.second, t->stream));
+        if (rec.b) KVX_CUDA(cudaEventRecord(rec.b, t->stream));
     }
-    if (tight >= 2) KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     KVX_CUDA(cudaEventRecord(t->ev_end, t->stream));
     // Commit the mirror only once every launch was accepted.
     for (int32_t i = 0; i < n; ++i)
@@ -822,10 +830,11 @@ int kvx_destroy(kvx_transition* t) {
     A.event_free(t->pieces_free, false);
     A.host_free(t->h_rows, t->h_rows_bytes);
     A.event_free(t->rows_free, false);
-    for (auto& ev : t->move_ev) {
-        A.event_free(ev.first, true);
-        A.event_free(ev.second, true);
+    for (auto& rec : t->move_rec) {
+        A.event_free(rec.a, true);
+        A.event_free(rec.b, true);
     }
+    A.dev_free(t->d_timer, sizeof(unsigned long long) * 2 * kvx_transition::kTimerSlots);
     if (t->side) {
         cudaStreamSynchronize(t->side);
         A.stream_free(t->side);
@@ -863,11 +872,24 @@ int kvx_move_timings(const kvx_transition* t, int32_t cap, double* move_ms, uint
                      int32_t* n_out) {
     if (!t || !n_out || cap < 0) return fail(KVX_EINVAL, "bad arguments");
     DeviceGuard dg(t->device);
-    const int32_t n = (int32_t)t->move_ev.size();
+    const int32_t n = (int32_t)t->move_rec.size();
+    unsigned long long ts[2 * kvx_transition::kTimerSlots];
+    if (t->n_timers > 0) {  // the bulk mover's own start / end stamps
+        KVX_CUDA(cudaMemcpyAsync(ts, t->d_timer, sizeof(ts), cudaMemcpyDeviceToHost, t->stream));
+        KVX_CUDA(cudaStreamSynchronize(t->stream));
+    }
     for (int32_t i = 0; i < n && i < cap; ++i) {
-        float ms = 0.f;
-        KVX_CUDA(cudaEventSynchronize(t->move_ev[(size_t)i].second));
-        KVX_CUDA(cudaEventElapsedTime(&ms, t->move_ev[(size_t)i].first, t->move_ev[(size_t)i].second));
+        const kvx_transition::MoveRec& r = t->move_rec[(size_t)i];
+        double ms = 0.0;
+        if (r.timer >= 0) {
+            const unsigned long long s = ts[r.timer], e = ts[kvx_transition::kTimerSlots + r.timer];
+            ms = e > s && s != ~0ull ? (double)(e - s) * 1e-6 : 0.0;
+        } else {
+            float f = 0.f;
+            KVX_CUDA(cudaEventSynchronize(r.b));
+            KVX_CUDA(cudaEventElapsedTime(&f, r.a, r.b));
+            ms = f;
+        }
         if (move_ms) move_ms[i] = ms;
         if (rw_bytes) rw_bytes[i] = t->move_bytes[(size_t)i];
     }
