@@ -96,6 +96,21 @@ def test_two_gpu_transition_bit_exact(gpu_count, mode, name, heads, dim, pull):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("pull", [False, True, "auto"], ids=["push", "pull", "auto"])
+@pytest.mark.parametrize("mode", ["affinity", "disjoint", "spread", "oneway"])
+@pytest.mark.parametrize("name", ["criterion12", "llama13b_8to4"])
+def test_four_rank_transition_bit_exact(gpu_count, mode, name, pull):
+    """World size 4 (the N=4 scaling run's shape): each rank owns a quarter of
+    the stages; every destination pool is compared with the oracle by the rank
+    that owns it, so all new stages are checked exactly once.  Ranks fold onto
+    the visible GPUs (four physical GPUs on a 4-GPU box)."""
+    res = _run(mgpu_worker.gpu_worker, 4, name, 2, 64, mode, pull, 0, (0, 0))
+    from paper_2510_11938_b200 import workload as W
+    t = [x for x in W.load_golden(name).transitions if x.outcome == "commit"][-1]
+    assert sum(r["checked"] for r in res.values()) == len(t.new_boundaries) + 1
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["affinity", "spread"])
 def test_two_gpu_controller_chain_bit_exact(gpu_count, mode):
     """BASELINE C5 across 2 GPUs: every 4th transition of the refactor chain
