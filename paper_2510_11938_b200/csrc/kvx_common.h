@@ -317,12 +317,6 @@ struct kvx_transition {
     cudaStream_t side = nullptr;  // side stream (arena-cached): head-major tails, the commit kernel
     cudaEvent_t ev_side_commit = nullptr;
     int last_plan_slot = -1;      // h_wave_free[slot] recorded after the most recent plan kernel
-    // plan-sequence word (device): each plan kernel publishes its wave number;
-    // the side-stream commit waits on it, so no event sits between the plan
-    // kernel and the mover it launches programmatically (KVX_PLAN_FLAG=0: events)
-    unsigned int* d_plan_seq = nullptr;
-    unsigned int plan_seq = 0;
-    bool plan_flag = false;
     bool handoff_since_plan = false;
     int32_t max_ctas = 0;         // cap on mover CTAs per wave (0 = tuned grid)
     cudaEvent_t ev_join = nullptr;

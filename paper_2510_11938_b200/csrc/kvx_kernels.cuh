@@ -148,8 +148,7 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
                 const int64_t* __restrict__ hi, int32_t n, const int32_t* __restrict__ src_bt,
                 int32_t* __restrict__ dst_bt, int64_t* __restrict__ synced_hi, int32_t max_blocks,
                 int32_t block_tokens, int32_t alloc_base, const int32_t* __restrict__ pop_stack,
-                Seg* __restrict__ segs, int32_t src_cap, int32_t dst_cap, int32_t* __restrict__ err,
-                unsigned int* __restrict__ done_seq = nullptr, unsigned int seq = 0) {
+                Seg* __restrict__ segs, int32_t src_cap, int32_t dst_cap, int32_t* __restrict__ err) {
     // let the mover (launched behind with programmatic stream serialization)
     // become resident now; it waits (griddepcontrol.wait) for this grid's
     // completion before it reads the segments
@@ -204,16 +203,6 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
         }
         carry.x += tot.x;
         carry.y += tot.y;
-    }
-    // Publish "the table and synced marks of wave `seq` are final" for a commit
-    // kernel on another stream (kvx_commit_async) that waits on this word
-    // instead of an event between this kernel and the mover.
-    if (done_seq) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicMax(done_seq, seq);
-        }
     }
 }
 
@@ -937,43 +926,13 @@ kvx_commit_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ k
                   int32_t* __restrict__ blocks, int32_t* __restrict__ free_list,
                   int64_t* __restrict__ out /* [0]=violations [1]=n_blocks [2]=n_free */,
                   int32_t* __restrict__ free_list_dev /* optional device copy (block-manager push) */,
-                  const int32_t* __restrict__ err = nullptr /* plan-kernel error word -> out[3] */,
-                  const unsigned int* __restrict__ plan_seq = nullptr, unsigned int want = 0) {
+                  const int32_t* __restrict__ err = nullptr /* plan-kernel error word -> out[3] */) {
     __shared__ unsigned long long s_viol;
-    __shared__ int s_timeout;
-    if (threadIdx.x == 0) {
-        s_viol = 0;
-        s_timeout = 0;
-    }
+    if (threadIdx.x == 0) s_viol = 0;
     for (int32_t r = threadIdx.x; r < max_requests; r += kCommitThreads) live_flag[r] = 0;
     __syncthreads();
     for (int32_t i = threadIdx.x; i < n; i += kCommitThreads) live_flag[req[i]] = 1;
-    if (plan_seq && threadIdx.x == 0) {
-        // wait for the last wave's plan kernel (kvx_plan_kernel publishes its
-        // sequence number); bounded, so a missing plan can never hang the GPU
-        unsigned long long t0;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-        for (;;) {
-            unsigned int v;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(plan_seq) : "memory");
-            if (v >= want) break;
-            unsigned long long t1;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 2000000000ull) {  // 2 s
-                s_timeout = 1;
-                break;
-            }
-            __nanosleep(200);
-        }
-    }
     __syncthreads();
-    if (s_timeout) {
-        if (threadIdx.x == 0) {
-            out[0] = out[1] = out[2] = -1;
-            out[3] = 2;  // reported as a device error by kvx_commit_collect
-        }
-        return;
-    }
     const int64_t B = block_tokens;
 
     // Live rows: violation ballot + CSR of the allocated blocks.

@@ -235,10 +235,6 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         t->seg_cap = (int64_t)(kvx::size_class(sizeof(kvx::Seg) * cells) / sizeof(kvx::Seg));
         t->commit_i32_cap = (int64_t)(d->max_requests + 1) + 2 * (int64_t)cells;
         t->h_commit_bytes = 32 + sizeof(int32_t) * (size_t)t->commit_i32_cap;
-        t->plan_flag = !(getenv("KVX_PLAN_FLAG") && std::string(getenv("KVX_PLAN_FLAG")) == "0");
-        if (A.dev_alloc((void**)&t->d_plan_seq, sizeof(unsigned int)) != cudaSuccess ||
-            cudaMemsetAsync(t->d_plan_seq, 0, sizeof(unsigned int), t->stream) != cudaSuccess)
-            return bail(fail(KVX_ENOSPC, "plan sequence word"));
         constexpr size_t kTimerBytes = sizeof(unsigned long long) * kvx_transition::kTimerSlots;
         if (A.dev_alloc((void**)&t->d_timer, 2 * kTimerBytes) != cudaSuccess ||
             cudaMemsetAsync(t->d_timer, 0xff, kTimerBytes, t->stream) != cudaSuccess ||  // starts: +inf
@@ -440,15 +436,10 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     kvx::kvx_plan_kernel<<<1, kvx::kPlanThreads, 0, t->stream>>>(
         h_req, h_lo, h_hi, n, t->d_src_bt, t->d_dst_bt, t->d_synced_hi, t->max_blocks,
         t->g.block_tokens, t->bm ? t->bm->top : t->alloc, t->bm ? t->bm->d_stack : nullptr, t->d_segs,
-        t->src_cap, t->dst_num_blocks, t->d_err, t->d_plan_seq, ++t->plan_seq);
+        t->src_cap, t->dst_num_blocks, t->d_err);
     KVX_LAUNCHED();
-    // The event that frees the staging slot (and, without the plan flag, tells the
-    // side stream the table is final) goes right after the plan kernel only when a
-    // side-stream mover needs it; else after the mover, so the plan kernel and the
-    // mover stay adjacent (programmatic dependent launch).
-    const bool plan_event_now = !t->plan_flag || t->head_tails || (t->transpose && t->tmap_t2h >= 0);
-    if (plan_event_now) KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
-    t->last_plan_slot = plan_event_now ? slot : -1;  // the event marks the table / synced marks as final
+    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
+    t->last_plan_slot = slot;  // this event now marks the table / synced marks as final
     t->handoff_since_plan = false;
     if (t->bm && new_blocks > 0) KVX_CUDA(bm_order_after(t->bm, t->stream));
     if (t->n_local_layers > 0) {
@@ -581,7 +572,6 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         KVX_LAUNCHED();
         if (rec.b) KVX_CUDA(cudaEventRecord(rec.b, t->stream));
     }
-    if (!plan_event_now) KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     KVX_CUDA(cudaEventRecord(t->ev_end, t->stream));
     // Commit the mirror only once every launch was accepted.
     for (int32_t i = 0; i < n; ++i)
@@ -703,13 +693,8 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
     // (not after a handoff: there the fork/join cost more than they hid, same-box A/B
     // profiles/r01_ab_stall.txt)
     cudaStream_t cs = t->stream;
-    const unsigned int* wait_seq = nullptr;
-    if (t->side && !t->handoff_since_plan && t->plan_seq > 0) {
-        if (t->last_plan_slot >= 0) {  // the plan's event is in the stream: wait on it
-            KVX_CUDA(cudaStreamWaitEvent(t->side, t->h_wave_free[t->last_plan_slot], 0));
-        } else {  // plan flag: the commit kernel waits for the last plan's sequence number
-            wait_seq = t->d_plan_seq;
-        }
+    if (t->last_plan_slot >= 0 && t->side && !t->handoff_since_plan) {
+        KVX_CUDA(cudaStreamWaitEvent(t->side, t->h_wave_free[t->last_plan_slot], 0));
         cs = t->side;
     }
     int32_t* h32 = reinterpret_cast<int32_t*>(t->h_commit + 32);
@@ -717,7 +702,7 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
         reinterpret_cast<const int32_t*>(h), reinterpret_cast<const int64_t*>(h + off_kv), n_live, t->d_dst_bt,
         t->d_synced_hi, t->d_live, t->max_requests, t->max_blocks, t->g.block_tokens, h32, h32 + (n_live + 1),
         h32 + (n_live + 1) + nb_live, reinterpret_cast<int64_t*>(t->h_commit), t->bm ? d_free : nullptr,
-        t->d_err, wait_seq, t->plan_seq);
+        t->d_err);
     KVX_LAUNCHED();
     KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], cs));
     if (cs != t->stream) {
@@ -750,7 +735,6 @@ int kvx_commit_collect(kvx_transition* t, kvx_commit_result* out) {
     KVX_CUDA(cudaEventSynchronize(t->ev_commit));
     int64_t res[4];
     std::memcpy(res, t->h_commit, sizeof(res));
-    if (res[3] == 2) return fail(KVX_ECUDA, "commit kernel timed out waiting for the last wave's plan kernel");
     if (res[3]) return fail(KVX_ECUDA, "device bounds check failed: a wave referenced a block outside its pool");
     if (res[1] != t->pend_nb_live || res[2] != t->pend_nb_free)
         return fail(KVX_ECUDA, "device compaction disagrees with the host mirror");
@@ -851,7 +835,6 @@ int kvx_destroy(kvx_transition* t) {
         A.event_free(rec.b, true);
     }
     A.dev_free(t->d_timer, sizeof(unsigned long long) * 2 * kvx_transition::kTimerSlots);
-    A.dev_free(t->d_plan_seq, sizeof(unsigned int));
     if (t->side) {
         cudaStreamSynchronize(t->side);
         A.stream_free(t->side);
