@@ -4,8 +4,8 @@
 set -u
 out=gpurun_out
 tag=${1:-r01b}
-C3="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 --no-verify --no-weights"
-C1="python bench.py --config c1 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 --no-verify --no-weights"
+C3="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 --no-verify --no-weights --no-ncu"
+C1="python bench.py --config c1 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 --no-verify --no-weights --no-ncu"
 : > $out/ncu_status.txt
 # 1. launch list of the C3 bench (every kernel, device time; cold-cache, serialised)
 $C3 > $out/plain_c3.log 2>&1 && \
