@@ -16,21 +16,41 @@ import pytest
 from tests import mgpu_worker
 
 
+def _free_port() -> int:
+    """A TCP port nothing listens on now (the gloo store binds it next); a
+    random pick could collide and leave the other ranks waiting for a store
+    that never comes up."""
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def _run(target, world, *args, timeout=600):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = random.randint(20000, 40000)
+    port = _free_port()
     procs = [ctx.Process(target=target, args=(r, world, port, *args, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
-    for _ in range(world):
-        rank, status, payload = q.get(timeout=timeout)
-        res[rank] = (status, payload)
-    for p in procs:
-        p.join(timeout=60)
-    for rank, (status, payload) in res.items():
-        assert status == "ok", f"rank {rank}:\n{payload}"
+    try:
+        for _ in range(world):
+            try:
+                rank, status, payload = q.get(timeout=timeout)
+            except Exception:  # queue.Empty: report who never answered, and how they ended
+                codes = {i: p.exitcode for i, p in enumerate(procs)}
+                raise AssertionError(f"ranks {sorted(set(range(world)) - set(res))} gave no result within "
+                                     f"{timeout} s; exit codes {codes}; results so far {res}")
+            res[rank] = (status, payload)
+            # a failed rank will not reach the others' barriers: fail now, not at the timeout
+            assert status == "ok", f"rank {rank}:\n{payload}"
+    finally:
+        for p in procs:
+            p.join(timeout=60 if len(res) == world else 1)
+            if p.is_alive():
+                p.terminate()
+                p.join(timeout=10)
     return {r: p for r, (_, p) in res.items()}
 
 
