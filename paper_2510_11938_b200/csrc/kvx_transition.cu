@@ -477,9 +477,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                 out[o++] = sg;
             }
         }
-        // one DMA of the host-built list into the device copy the movers read
-        KVX_CUDA(cudaMemcpyAsync(t->d_segs, out, sizeof(kvx::Seg) * (size_t)nseg, cudaMemcpyHostToDevice,
-                                 t->stream));
+        segs = out;
         if (!t->side_synced) {  // the side stream starts behind the grant's table uploads on the main stream
             KVX_CUDA(cudaEventRecord(t->ev_join, t->stream));
             KVX_CUDA(cudaStreamWaitEvent(t->side, t->ev_join, 0));
@@ -632,7 +630,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         if (rec.b) KVX_CUDA(cudaEventRecord(rec.b, t->stream));
     }
     if (t->host_plan) {
-        KVX_CUDA(cudaEventRecord(t->h_segs_free[slot], t->stream));        // the DMA has read the pinned list
+        KVX_CUDA(cudaEventRecord(t->h_segs_free[slot], t->stream));        // the movers read the pinned segments
         KVX_CUDA(cudaStreamWaitEvent(t->stream, t->h_wave_free[slot], 0));  // the device tables are final
     }
     KVX_CUDA(cudaEventRecord(t->ev_end, t->stream));
