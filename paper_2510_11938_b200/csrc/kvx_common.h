@@ -366,17 +366,6 @@ struct kvx_transition {
     size_t h_rows_bytes = 0;
     cudaEvent_t rows_free = nullptr;
 
-    // host-planned waves (bump rule, host source mirror): the host builds the
-    // segment list into pinned memory and the mover reads it from there, so no
-    // plan kernel sits before the mover; the plan kernel (tables only) runs on
-    // the side stream.  KVX_HOST_PLAN=0 keeps the device plan before the mover.
-    bool host_plan = false;
-    bool side_synced = false;          // the side stream has waited for the grant's uploads
-    std::vector<int32_t> dst_bt_h;     // host mirror of the destination table
-    kvx::Seg* h_segs[2] = {nullptr, nullptr};
-    int64_t h_segs_cap[2] = {0, 0};
-    cudaEvent_t h_segs_free[2] = {nullptr, nullptr};
-
     // host mirror of the destination rule (capacity checks are synchronous)
     std::vector<int64_t> synced_hi;
     std::vector<int32_t> src_bt;  // host copy: every wave's source blocks must be backed

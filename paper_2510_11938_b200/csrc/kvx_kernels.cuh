@@ -185,8 +185,8 @@ kvx_plan_kernel(const int32_t* __restrict__ req, const int64_t* __restrict__ lo,
             }
             if (h > s) synced_hi[r] = h;
             const int64_t b0 = l / B;
-            Seg* out = segs ? segs + carry.y + off.y : nullptr;  // null: the host planned the segments
-            for (int32_t k = 0; out && k < cnt.y; ++k) {
+            Seg* out = segs + carry.y + off.y;
+            for (int32_t k = 0; k < cnt.y; ++k) {
                 const int64_t b = b0 + k;
                 const int64_t t0 = l > b * B ? l - b * B : 0;
                 const int64_t t1 = h < (b + 1) * B ? h - b * B : B;

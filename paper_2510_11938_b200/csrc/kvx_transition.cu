@@ -150,9 +150,6 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     t->epoch = d->epoch;
     t->synced_hi.assign((size_t)d->max_requests, 0);
     if (!dev_table) t->src_bt.assign(d->src_block_table, d->src_block_table + cells);  // host mirror
-    t->host_plan = !dev_table && !d->dst_blockmgr &&
-                   !(getenv("KVX_HOST_PLAN") && std::string(getenv("KVX_HOST_PLAN")) == "0");
-    if (t->host_plan) t->dst_bt_h.assign(cells, -1);
     t->ctl.init(d->max_requests, d->max_sync_rounds,
                 d->kv_bytes_per_token > 0.0 ? d->kv_bytes_per_token
                                             : (double)g.num_layers * (double)block_bytes(g) /
@@ -222,8 +219,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     t->src_cap = min_old_blocks;  // INT32_MAX when no old pool is visible here (no local sources)
     for (int s = 0; s < 2; ++s)
         if (A.host_alloc((void**)&t->h_wave[s], wave_bytes) != cudaSuccess ||
-            A.event(&t->h_wave_free[s], false) != cudaSuccess ||
-            (t->host_plan && A.event(&t->h_segs_free[s], false) != cudaSuccess))
+            A.event(&t->h_wave_free[s], false) != cudaSuccess)
             return bail(fail(KVX_ECUDA, "pinned staging allocation failed"));
     if (cudaMemcpyAsync(t->d_src_bt, dev_table ? d->src_block_table_dev : d->src_block_table, bt_bytes,
                         dev_table ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, t->stream) != cudaSuccess ||
@@ -437,65 +433,12 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
     const int32_t* h_req = reinterpret_cast<const int32_t*>(h);
     const int64_t* h_lo = reinterpret_cast<const int64_t*>(h + off_lo);
     const int64_t* h_hi = reinterpret_cast<const int64_t*>(h + off_hi);
-    const kvx::Seg* segs = t->d_segs;  // what the movers read
-    if (t->host_plan) {
-        // The host runs the destination rule on its mirrors (synced marks, bump
-        // pointer, both tables) and writes the segment list into pinned memory;
-        // the movers read it from there.  The plan kernel still updates the
-        // device tables, on the side stream beside the mover.
-        if (nseg > t->h_segs_cap[slot]) {
-            kvx::Arena& A = kvx::Arena::of(t->device);
-            KVX_CUDA(cudaEventSynchronize(t->h_segs_free[slot]));
-            A.host_free(t->h_segs[slot], sizeof(kvx::Seg) * (size_t)t->h_segs_cap[slot]);
-            t->h_segs[slot] = nullptr;
-            const int64_t cap = (int64_t)(kvx::size_class(sizeof(kvx::Seg) * (size_t)nseg) / sizeof(kvx::Seg));
-            KVX_CUDA(A.host_alloc((void**)&t->h_segs[slot], sizeof(kvx::Seg) * (size_t)cap));
-            t->h_segs_cap[slot] = cap;
-        }
-        KVX_CUDA(cudaEventSynchronize(t->h_segs_free[slot]));
-        kvx::Seg* out = t->h_segs[slot];
-        int64_t o = 0;
-        int32_t next_id = t->alloc;
-        const size_t mb = (size_t)t->max_blocks;
-        for (int32_t i = 0; i < n; ++i) {
-            if (hi[i] <= lo[i]) continue;
-            const size_t r = (size_t)req[i];
-            const int64_t have = cdiv64(t->synced_hi[r], B), need = cdiv64(hi[i], B);
-            int32_t* drow = t->dst_bt_h.data() + r * mb;
-            const int32_t* srow = t->src_bt.data() + r * mb;
-            for (int64_t k = have; k < need; ++k) drow[k] = next_id++;
-            for (int64_t b = lo[i] / B; b < need; ++b) {
-                const int64_t t0 = lo[i] > b * B ? lo[i] - b * B : 0;
-                const int64_t t1 = hi[i] < (b + 1) * B ? hi[i] - b * B : B;
-                kvx::Seg sg{srow[b], drow[b], (int32_t)t0, (int32_t)t1};
-                // the plan kernel's bounds check, on the host: an id outside its pool
-                // becomes an empty run and raises the (host-mapped) error word
-                if (sg.src_blk < 0 || sg.src_blk >= t->src_cap || sg.dst_blk < 0 || sg.dst_blk >= t->dst_num_blocks) {
-                    *reinterpret_cast<volatile int32_t*>(t->d_err) = 1;
-                    sg.t0 = sg.t1 = 0;
-                }
-                out[o++] = sg;
-            }
-        }
-        segs = out;
-        if (!t->side_synced) {  // the side stream starts behind the grant's table uploads on the main stream
-            KVX_CUDA(cudaEventRecord(t->ev_join, t->stream));
-            KVX_CUDA(cudaStreamWaitEvent(t->side, t->ev_join, 0));
-            t->side_synced = true;
-        }
-        kvx::kvx_plan_kernel<<<1, kvx::kPlanThreads, 0, t->side>>>(
-            h_req, h_lo, h_hi, n, t->d_src_bt, t->d_dst_bt, t->d_synced_hi, t->max_blocks, t->g.block_tokens,
-            t->alloc, nullptr, nullptr, t->src_cap, t->dst_num_blocks, t->d_err);
-        KVX_LAUNCHED();
-        KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->side));
-    } else {
-        kvx::kvx_plan_kernel<<<1, kvx::kPlanThreads, 0, t->stream>>>(
-            h_req, h_lo, h_hi, n, t->d_src_bt, t->d_dst_bt, t->d_synced_hi, t->max_blocks,
-            t->g.block_tokens, t->bm ? t->bm->top : t->alloc, t->bm ? t->bm->d_stack : nullptr, t->d_segs,
-            t->src_cap, t->dst_num_blocks, t->d_err);
-        KVX_LAUNCHED();
-        KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
-    }
+    kvx::kvx_plan_kernel<<<1, kvx::kPlanThreads, 0, t->stream>>>(
+        h_req, h_lo, h_hi, n, t->d_src_bt, t->d_dst_bt, t->d_synced_hi, t->max_blocks,
+        t->g.block_tokens, t->bm ? t->bm->top : t->alloc, t->bm ? t->bm->d_stack : nullptr, t->d_segs,
+        t->src_cap, t->dst_num_blocks, t->d_err);
+    KVX_LAUNCHED();
+    KVX_CUDA(cudaEventRecord(t->h_wave_free[slot], t->stream));
     t->last_plan_slot = slot;  // this event now marks the table / synced marks as final
     t->handoff_since_plan = false;
     if (t->bm && new_blocks > 0) KVX_CUDA(bm_order_after(t->bm, t->stream));
@@ -534,14 +477,14 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             if (t->max_ctas > 0) tgrid = std::min<int64_t>(tgrid, t->max_ctas);
             kvx::kvx_tmap_kernel<kTmapStages, kTmapLag><<<(unsigned)std::max<int64_t>(1, tgrid), 32,
                                                           kTmapStages * (size_t)t->tmap_hc * head_plane, t->stream>>>(
-                segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->d_maps, t->g.num_kv_heads, t->tmap_hc,
+                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->d_maps, t->g.num_kv_heads, t->tmap_hc,
                 head_plane, t->g.block_tokens, t->tmap_t2h);
             if (full_tokens < tokens) {
                 KVX_LAUNCHED();
                 cudaStream_t ts = t->max_ctas > 0 ? t->stream : t->side;
                 if (ts == t->side) KVX_CUDA(cudaStreamWaitEvent(t->side, t->h_wave_free[slot], 0));
                 kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, ts>>>(
-                    segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
+                    t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                     (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 2, t->has_peer_dst ? 1 : 0);
                 if (ts == t->side) {
                     KVX_CUDA(cudaEventRecord(t->ev_join, t->side));
@@ -550,7 +493,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             }
         } else if (t->transpose) {  // token-major <-> head-major pools: per-(token, head) rows
             kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
-                segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
+                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                 (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0);
         } else if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
             const int vi = slab ? t->bulk_variant_slab : t->bulk_variant_tok;
@@ -591,7 +534,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             cfg.stream = t->stream;
             cfg.attrs = &attr;
             cfg.numAttrs = 1;
-            KVX_CUDA(cudaLaunchKernelEx(&cfg, bv.fn, (const kvx::Seg*)segs, (int32_t)nseg,
+            KVX_CUDA(cudaLaunchKernelEx(&cfg, bv.fn, (const kvx::Seg*)t->d_segs, (int32_t)nseg,
                                         (const kvx::LayerPtr*)t->d_layers, t->n_local_layers,
                                         block_bytes(t->g), token_bytes(t->g), t->g.block_tokens,
                                         t->n_peer_layers, peer_ctas,
@@ -603,7 +546,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                 // max_ctas CTAs at once
                 KVX_LAUNCHED();
                 kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
-                    segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
+                    t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                     (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 1, t->has_peer_dst ? 1 : 0);
             } else if (t->head_tails) {
                 // head-major partial blocks (the bulk mover skips them): the row mover on a
@@ -612,26 +555,22 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                 KVX_LAUNCHED();
                 KVX_CUDA(cudaStreamWaitEvent(t->side, t->h_wave_free[slot], 0));
                 kvx::kvx_move_any_kernel<<<grid, kvx::kMoveThreads, 0, t->side>>>(
-                    segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
+                    t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, t->g.num_kv_heads,
                     (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 1, t->has_peer_dst ? 1 : 0);
                 KVX_CUDA(cudaEventRecord(t->ev_join, t->side));
                 KVX_CUDA(cudaStreamWaitEvent(t->stream, t->ev_join, 0));
             }
         } else if (t->lsu256 && token_bytes(t->g) % 32 == 0) {
             kvx::kvx_move256_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
-                segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
+                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
                 token_bytes(t->g), t->g.block_tokens, t->has_peer_dst ? 1 : 0);
         } else {
             kvx::kvx_move_kernel<<<grid, kvx::kMoveThreads, 0, t->stream>>>(
-                segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
+                t->d_segs, (int32_t)nseg, t->d_layers, t->n_local_layers, block_bytes(t->g),
                 token_bytes(t->g), t->g.block_tokens, t->has_peer_dst ? 1 : 0);
         }
         KVX_LAUNCHED();
         if (rec.b) KVX_CUDA(cudaEventRecord(rec.b, t->stream));
-    }
-    if (t->host_plan) {
-        KVX_CUDA(cudaEventRecord(t->h_segs_free[slot], t->stream));        // the movers read the pinned segments
-        KVX_CUDA(cudaStreamWaitEvent(t->stream, t->h_wave_free[slot], 0));  // the device tables are final
     }
     KVX_CUDA(cudaEventRecord(t->ev_end, t->stream));
     // Commit the mirror only once every launch was accepted.
@@ -670,10 +609,6 @@ int kvx_src_rows(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* re
     KVX_CUDA(cudaEventSynchronize(t->rows_free));  // the previous update's staging was consumed
     if (bytes > t->h_rows_bytes) {
         A.host_free(t->h_rows, t->h_rows_bytes);
-    for (int s2 = 0; s2 < 2; ++s2) {
-        A.host_free(t->h_segs[s2], sizeof(kvx::Seg) * (size_t)t->h_segs_cap[s2]);
-        A.event_free(t->h_segs_free[s2], false);
-    }
         t->h_rows = nullptr;
         const size_t cap = kvx::size_class(bytes);
         KVX_CUDA(A.host_alloc((void**)&t->h_rows, cap));
@@ -858,7 +793,6 @@ int kvx_abort(kvx_transition* t) {
     ++t->epoch;  // engine.cpp:769
     t->alloc = 0;
     std::fill(t->synced_hi.begin(), t->synced_hi.end(), 0);
-    std::fill(t->dst_bt_h.begin(), t->dst_bt_h.end(), -1);
     const size_t bt_bytes = sizeof(int32_t) * (size_t)t->max_requests * (size_t)t->max_blocks;
     KVX_CUDA(cudaMemsetAsync(t->d_dst_bt, 0xff, bt_bytes, t->stream));
     KVX_CUDA(cudaMemsetAsync(t->d_synced_hi, 0, sizeof(int64_t) * (size_t)t->max_requests, t->stream));
@@ -895,10 +829,6 @@ int kvx_destroy(kvx_transition* t) {
     A.host_free(t->h_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
     A.event_free(t->pieces_free, false);
     A.host_free(t->h_rows, t->h_rows_bytes);
-    for (int s2 = 0; s2 < 2; ++s2) {
-        A.host_free(t->h_segs[s2], sizeof(kvx::Seg) * (size_t)t->h_segs_cap[s2]);
-        A.event_free(t->h_segs_free[s2], false);
-    }
     A.event_free(t->rows_free, false);
     for (auto& rec : t->move_rec) {
         A.event_free(rec.a, true);
