@@ -124,8 +124,7 @@ def test_lsu_movers_convert_layouts(gpu_count, impl, monkeypatch):
 def test_head_major_layouts(gpu_count, pair, impl, monkeypatch):
     """Head-major pools on every stage of one side or both: head-major to
     head-major through run copies (2*H runs per partial block), the rest
-    through the transposing movers (whole blocks on the TMA tensor-map
-    transposer, partial blocks on the row mover)."""
+    through the transposing row mover."""
     monkeypatch.setenv("KVX_MOVE_IMPL", impl)
     for seed in (11, 12, 13):
         test_random_layouts_bit_exact(gpu_count, seed, uniform=pair)
@@ -136,8 +135,7 @@ def test_head_major_layouts(gpu_count, pair, impl, monkeypatch):
 @pytest.mark.parametrize("tmap", ["on", "off"])
 def test_transposes_tmap_and_row_mover(gpu_count, pair, tmap, monkeypatch):
     """Every transposing pairing with the TMA tensor-map transposer for whole
-    blocks (default) and without it (KVX_TMAP=0: the row mover moves all)."""
-    if tmap == "off":
-        monkeypatch.setenv("KVX_TMAP", "0")
+    blocks (KVX_TMAP=1) and without it (the default: the row mover moves all)."""
+    monkeypatch.setenv("KVX_TMAP", "1" if tmap == "on" else "0")
     for seed in range(20, 28):
         test_random_layouts_bit_exact(gpu_count, seed, uniform=pair)
