@@ -12,6 +12,9 @@
 
 #include <cudaTypedefs.h>
 
+#include <map>
+#include <mutex>
+
 using namespace kvx_host;
 
 namespace {
@@ -37,6 +40,45 @@ struct TmSide {
     int32_t num_blocks;
     uint64_t ts, hs, kv, bs;
 };
+}  // namespace
+
+namespace {
+// What kvx_begin needs to know about a device's occupancy, queried once per
+// device: a grant is on the engine's refactor path, and 20+ occupancy /
+// attribute queries per grant cost ~0.1-0.5 ms of host time.
+struct DeviceCaps {
+    int num_sms = 0;
+    int move_ctas_per_sm = 1;
+    int bulk_ctas[kNumBulkVariants] = {};
+};
+int device_caps(int device, DeviceCaps* out) {
+    static std::mutex mu;
+    static std::map<int, DeviceCaps> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(device);
+    if (it != cache.end()) {
+        *out = it->second;
+        return KVX_OK;
+    }
+    DeviceCaps c;
+    int occ = 0;
+    if (cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+        return fail(KVX_ECUDA, "query SM count");
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kvx::kvx_move_kernel, kvx::kMoveThreads, 0) != cudaSuccess)
+        return fail(KVX_ECUDA, "occupancy query");
+    c.move_ctas_per_sm = std::max(1, occ);
+    for (int v = 0; v < kNumBulkVariants; ++v) {
+        const BulkVariant& bv = kBulkVariants[v];
+        const int smem = bv.stages * (int)bv.chunk;
+        if (cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bv.fn, kvx::kBulkThreads, smem) != cudaSuccess)
+            return fail(KVX_ECUDA, "bulk kernel attributes");
+        c.bulk_ctas[v] = std::max(1, occ);
+    }
+    cache[device] = c;
+    *out = c;
+    return KVX_OK;
+}
 }  // namespace
 
 namespace kvx_host {
@@ -158,13 +200,10 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         kvx_destroy(t);
         return code;
     };
-    if (cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, d->device) != cudaSuccess)
-        return bail(fail(KVX_ECUDA, "query SM count"));
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kvx::kvx_move_kernel, kvx::kMoveThreads, 0) !=
-        cudaSuccess)
-        return bail(fail(KVX_ECUDA, "occupancy query"));
-    t->move_ctas_per_sm = std::max(1, occ);
+    DeviceCaps caps;
+    if (const int rc = device_caps(d->device, &caps)) return bail(rc);
+    t->num_sms = caps.num_sms;
+    t->move_ctas_per_sm = caps.move_ctas_per_sm;
     {
         // Ring per wave kind (kvx_wave): slab waves (mostly full blocks) and
         // token-granular waves.  KVX_BULK_CFG pins one variant for both,
@@ -176,14 +215,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         };
         t->bulk_variant_slab = pick("KVX_BULK_CFG_SLAB", pick("KVX_BULK_CFG", kSlabVariant));
         t->bulk_variant_tok = pick("KVX_BULK_CFG_TOK", pick("KVX_BULK_CFG", kTokVariant));
-        for (int v = 0; v < kNumBulkVariants; ++v) {
-            const BulkVariant& bv = kBulkVariants[v];
-            const int smem = bv.stages * (int)bv.chunk;
-            if (cudaFuncSetAttribute(bv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bv.fn, kvx::kBulkThreads, smem) != cudaSuccess)
-                return bail(fail(KVX_ECUDA, "bulk kernel attributes"));
-            t->bulk_ctas[v] = std::max(1, occ);
-        }
+        for (int v = 0; v < kNumBulkVariants; ++v) t->bulk_ctas[v] = caps.bulk_ctas[v];
         // Bulk (TMA engine) mover by default, for local and peer (NVLink)
         // destinations alike; KVX_PEER_BULK=0 keeps the LSU mover for peer
         // pushes, KVX_MOVE_IMPL=lsu everywhere.
