@@ -340,6 +340,11 @@ struct kvx_transition {
     cudaEvent_t ev_commit = nullptr;
     int32_t pend_n_live = 0;
     int64_t pend_nb_live = 0, pend_nb_free = 0;
+    // the handle's most recent work on its (possibly shared) stream: kvx_destroy
+    // waits for this event, not for the whole stream, so a caller that reuses
+    // one stream for consecutive transitions never drains it at a destroy
+    cudaEvent_t ev_ready = nullptr;  // recorded at the end of kvx_begin
+    cudaEvent_t last_ev = nullptr;
     // timing
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     bool timing_open = false;

@@ -115,6 +115,8 @@ int kvx_handoff(kvx_transition* t, uint64_t epoch, uint64_t row_bytes, int32_t n
     kvx::kvx_copy_list_kernel<kStages, kChunk><<<grid, kvx::kBulkThreads, kStages * kChunk, t->stream>>>(
         t->d_pieces, (int64_t)pieces.size());
     KVX_LAUNCHED();
+    KVX_CUDA(cudaEventRecord(t->ev_end, t->stream));  // the handoff lands inside the wave window
+    t->last_ev = t->ev_end;
     return KVX_OK;
 }
 

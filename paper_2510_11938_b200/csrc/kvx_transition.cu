@@ -397,6 +397,9 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
     // No host sync: the uploads above were staged from pageable memory
     // (copied out before cudaMemcpyAsync returned) and are stream-ordered
     // before every wave.
+    if (A.event(&t->ev_ready, false) != cudaSuccess || cudaEventRecord(t->ev_ready, t->stream) != cudaSuccess)
+        return bail(fail(KVX_ECUDA, "ready event"));
+    t->last_ev = t->ev_ready;
     *out = t;
     return KVX_OK;
 }
@@ -608,6 +611,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
         if (rec.b) KVX_CUDA(cudaEventRecord(rec.b, t->stream));
     }
     KVX_CUDA(cudaEventRecord(t->ev_end, t->stream));
+    t->last_ev = t->ev_end;
     // Commit the mirror only once every launch was accepted.
     for (int32_t i = 0; i < n; ++i)
         if (hi[i] > t->synced_hi[(size_t)req[i]]) t->synced_hi[(size_t)req[i]] = hi[i];
@@ -655,6 +659,7 @@ int kvx_src_rows(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* re
         t->h_rows, t->h_rows + n, n, t->max_blocks, t->d_src_bt);
     KVX_LAUNCHED();
     KVX_CUDA(cudaEventRecord(t->rows_free, t->stream));
+    t->last_ev = t->rows_free;
     if (!t->src_bt.empty())
         for (int32_t i = 0; i < n; ++i)
             std::memcpy(t->src_bt.data() + (size_t)req[i] * mb, rows + (size_t)i * mb, sizeof(int32_t) * mb);
@@ -754,6 +759,7 @@ int kvx_commit_async(kvx_transition* t, uint64_t epoch, int32_t n_live, const in
         t->bm->top += (int32_t)nb_free;
     }
     KVX_CUDA(cudaEventRecord(t->ev_commit, t->stream));
+    t->last_ev = t->ev_commit;
     t->pend_n_live = n_live;
     t->pend_nb_live = nb_live;
     t->pend_nb_free = nb_free;
@@ -839,7 +845,10 @@ int kvx_abort(kvx_transition* t) {
 int kvx_destroy(kvx_transition* t) {
     if (!t) return KVX_OK;
     DeviceGuard dg(t->device);
-    if (t->stream) cudaStreamSynchronize(t->stream);
+    if (t->last_ev)
+        cudaEventSynchronize(t->last_ev);  // this handle's work only; later work on a shared stream runs on
+    else if (t->stream)
+        cudaStreamSynchronize(t->stream);  // (a handle that failed inside kvx_begin)
     kvx::Arena& A = kvx::Arena::of(t->device);
     A.dev_free(t->d_src_bt, t->bt_bytes);
     A.dev_free(t->d_dst_bt, t->bt_bytes);
@@ -858,6 +867,7 @@ int kvx_destroy(kvx_transition* t) {
         A.host_free(t->h_wave[s], t->wave_bytes);
         A.event_free(t->h_wave_free[s], false);
     }
+    A.event_free(t->ev_ready, false);
     A.event_free(t->ev_begin, true);
     A.event_free(t->ev_end, true);
     A.dev_free(t->d_pieces, sizeof(kvx::Piece) * (size_t)t->piece_cap);
