@@ -5,11 +5,9 @@
 #include "pipesim/kvx_plane.hpp"
 
 #include <algorithm>
-#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
-#include <cstring>
 #include <fstream>
 #include <mutex>
 #include <string>
