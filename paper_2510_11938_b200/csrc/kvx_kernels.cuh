@@ -380,6 +380,23 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
 // threads; rows are ordered tokens-inner when the source is head-major (its
 // contiguous direction), heads-inner otherwise.  4 independent 16-byte loads
 // in flight per thread.
+// Unsigned 32-bit division by a divisor fixed for many dividends: one
+// __umulhi + add + shifts (round-up magic, exact for every 32-bit n).
+struct FastDiv {
+    uint32_t d, m, l;
+    __device__ __forceinline__ void init(uint32_t dv) {
+        d = dv;
+        l = 0;
+        while (l < 32 && (1ull << l) < (uint64_t)dv) ++l;  // ceil(log2 d)
+        m = (uint32_t)(((1ull << 32) * ((1ull << l) - dv)) / dv + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        if (d == 1) return n;
+        const uint32_t t = __umulhi(m, n);
+        return (t + ((n - t) >> 1)) >> (l - 1);
+    }
+};
+
 static __global__ void __launch_bounds__(kMoveThreads)
 kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
                     int32_t nlayers, int32_t heads, uint32_t head_bytes, int32_t block_tokens,
@@ -389,6 +406,12 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
     const int64_t units = (int64_t)nseg * nlayers;
     const uint32_t vph = head_bytes >> 4;  // 16-byte vectors per row
     const uint32_t H = (uint32_t)heads;
+    // the per-vector index math is the kernel's cost (a plain division ran it
+    // ALU-bound at 0.93 of the copy peak): divisors fixed per kernel / per unit
+    FastDiv fv, fh, ft;
+    fv.init(vph);
+    fh.init(H);
+    uint32_t ft_n = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         const int32_t layer = (int32_t)(u / nseg);
         const Seg sg = segs[u - (int64_t)layer * nseg];
@@ -403,6 +426,10 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
         const uint32_t per_kv = ntok * H * vph;
         const bool tok_inner = lp.src_ts < lp.src_hs;  // head-major source (order barely matters:
                                                         // profiles/r01_row_sweep.jsonl)
+        if (tok_inner && ntok != ft_n) {
+            ft.init(ntok);
+            ft_n = ntok;
+        }
         const uint32_t total = 2 * per_kv;
         for (uint32_t base = threadIdx.x; base < total; base += kMoveThreads * kU) {
             uint4 v[kU];
@@ -412,12 +439,17 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
                 const uint32_t i = base + (uint32_t)k * kMoveThreads;
                 dp[k] = nullptr;
                 if (i < total) {
-                    // plain division: a multiply-shift variant measured slower on the
-                    // same box (its per-unit set-up dominates short tails)
-                    const uint32_t kv = i / per_kv, r = i - kv * per_kv;
-                    const uint32_t w = r % vph, row = r / vph;
-                    const uint32_t h = tok_inner ? row / ntok : row % H;
-                    const uint32_t t = (uint32_t)sg.t0 + (tok_inner ? row % ntok : row / H);
+                    const uint32_t kv = i >= per_kv ? 1u : 0u, r = i - kv * per_kv;
+                    const uint32_t row = fv.div(r), w = r - row * vph;
+                    uint32_t h, t;
+                    if (tok_inner) {
+                        h = ft.div(row);
+                        t = (uint32_t)sg.t0 + row - h * ntok;
+                    } else {
+                        const uint32_t tt = fh.div(row);
+                        h = row - tt * H;
+                        t = (uint32_t)sg.t0 + tt;
+                    }
                     v[k] = ld_stream(reinterpret_cast<const uint4*>(sb + kv * lp.src_kv + t * lp.src_ts +
                                                                     h * lp.src_hs) + w);
                     dp[k] = reinterpret_cast<uint4*>(db + kv * lp.dst_kv + t * lp.dst_ts + h * lp.dst_hs) + w;
