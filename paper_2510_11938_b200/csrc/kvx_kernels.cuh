@@ -380,6 +380,11 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
 // threads; rows are ordered tokens-inner when the source is head-major (its
 // contiguous direction), heads-inner otherwise.  4 independent 16-byte loads
 // in flight per thread.
+#ifndef KVX_ROW_FASTDIV
+#define KVX_ROW_FASTDIV 1
+#endif
+constexpr bool kFastDivRows = KVX_ROW_FASTDIV;  // build-time A/B of the row mover's index math
+
 // Unsigned 32-bit division by a divisor fixed for many dividends: one
 // __umulhi + add + shifts (round-up magic, exact for every 32-bit n).
 struct FastDiv {
@@ -440,15 +445,23 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
                 dp[k] = nullptr;
                 if (i < total) {
                     const uint32_t kv = i >= per_kv ? 1u : 0u, r = i - kv * per_kv;
-                    const uint32_t row = fv.div(r), w = r - row * vph;
-                    uint32_t h, t;
-                    if (tok_inner) {
-                        h = ft.div(row);
-                        t = (uint32_t)sg.t0 + row - h * ntok;
+                    uint32_t row, w, h, t;
+                    if (kFastDivRows) {
+                        row = fv.div(r);
+                        w = r - row * vph;
+                        if (tok_inner) {
+                            h = ft.div(row);
+                            t = (uint32_t)sg.t0 + row - h * ntok;
+                        } else {
+                            const uint32_t tt = fh.div(row);
+                            h = row - tt * H;
+                            t = (uint32_t)sg.t0 + tt;
+                        }
                     } else {
-                        const uint32_t tt = fh.div(row);
-                        h = row - tt * H;
-                        t = (uint32_t)sg.t0 + tt;
+                        w = r % vph;
+                        row = r / vph;
+                        h = tok_inner ? row / ntok : row % H;
+                        t = (uint32_t)sg.t0 + (tok_inner ? row % ntok : row / H);
                     }
                     v[k] = ld_stream(reinterpret_cast<const uint4*>(sb + kv * lp.src_kv + t * lp.src_ts +
                                                                     h * lp.src_hs) + w);
