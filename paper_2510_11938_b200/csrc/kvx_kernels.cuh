@@ -380,11 +380,6 @@ kvx_move_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
 // threads; rows are ordered tokens-inner when the source is head-major (its
 // contiguous direction), heads-inner otherwise.  4 independent 16-byte loads
 // in flight per thread.
-#ifndef KVX_ROW_FASTDIV
-#define KVX_ROW_FASTDIV 1
-#endif
-constexpr bool kFastDivRows = KVX_ROW_FASTDIV;  // build-time A/B of the row mover's index math
-
 // Unsigned 32-bit division by a divisor fixed for many dividends: one
 // __umulhi + add + shifts (round-up magic, exact for every 32-bit n).
 struct FastDiv {
@@ -411,8 +406,9 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
     const int64_t units = (int64_t)nseg * nlayers;
     const uint32_t vph = head_bytes >> 4;  // 16-byte vectors per row
     const uint32_t H = (uint32_t)heads;
-    // the per-vector index math is the kernel's cost (a plain division ran it
-    // ALU-bound at 0.93 of the copy peak): divisors fixed per kernel / per unit
+    // the per-vector index math is the kernel's cost: with plain divisions it ran
+    // ALU-bound (same box: 0.777 -> 0.884 of the copy peak for blocks -> heads,
+    // profiles/r02ac_ab_row_fastdiv.jsonl); divisors fixed per kernel / per unit
     FastDiv fv, fh, ft;
     fv.init(vph);
     fh.init(H);
@@ -445,23 +441,15 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
                 dp[k] = nullptr;
                 if (i < total) {
                     const uint32_t kv = i >= per_kv ? 1u : 0u, r = i - kv * per_kv;
-                    uint32_t row, w, h, t;
-                    if (kFastDivRows) {
-                        row = fv.div(r);
-                        w = r - row * vph;
-                        if (tok_inner) {
-                            h = ft.div(row);
-                            t = (uint32_t)sg.t0 + row - h * ntok;
-                        } else {
-                            const uint32_t tt = fh.div(row);
-                            h = row - tt * H;
-                            t = (uint32_t)sg.t0 + tt;
-                        }
+                    const uint32_t row = fv.div(r), w = r - row * vph;
+                    uint32_t h, t;
+                    if (tok_inner) {
+                        h = ft.div(row);
+                        t = (uint32_t)sg.t0 + row - h * ntok;
                     } else {
-                        w = r % vph;
-                        row = r / vph;
-                        h = tok_inner ? row / ntok : row % H;
-                        t = (uint32_t)sg.t0 + (tok_inner ? row % ntok : row / H);
+                        const uint32_t tt = fh.div(row);
+                        h = row - tt * H;
+                        t = (uint32_t)sg.t0 + tt;
                     }
                     v[k] = ld_stream(reinterpret_cast<const uint4*>(sb + kv * lp.src_kv + t * lp.src_ts +
                                                                     h * lp.src_hs) + w);
