@@ -406,9 +406,9 @@ kvx_move_any_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* 
     const int64_t units = (int64_t)nseg * nlayers;
     const uint32_t vph = head_bytes >> 4;  // 16-byte vectors per row
     const uint32_t H = (uint32_t)heads;
-    // the per-vector index math is the kernel's cost: with plain divisions it ran
-    // ALU-bound (same box: 0.777 -> 0.884 of the copy peak for blocks -> heads,
-    // profiles/r02ac_ab_row_fastdiv.jsonl); divisors fixed per kernel / per unit
+    // divisors fixed per kernel / per unit (FastDiv): token-granular transposing
+    // waves 100 -> 87 us on C3's final wave; whole blocks go to kvx_tmap_kernel
+    // (same box, profiles/r02af_ab_transposers_same_box.jsonl)
     FastDiv fv, fh, ft;
     fv.init(vph);
     fh.init(H);

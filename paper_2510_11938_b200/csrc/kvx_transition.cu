@@ -343,14 +343,14 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
         tm_dir = dpeer;
         tm_dir.insert(tm_dir.end(), dlocal.begin(), dlocal.end());
     }
-    // Whole blocks of a transposing transition on the TMA transposer (opt-in): every
+    // Whole blocks of a transposing transition on the TMA transposer: every
     // local layer pairs the two families in the same direction, the geometry
     // fits one box (D <= 256 elements, a head plane <= one ring slot) and the
     // driver encodes the maps; else everything stays on the row mover.
-    // Opt-in (KVX_TMAP=1): on two of three boxes it beat the row mover by ~1%, on
-    // the third it lost 5% (profiles/r02l_ab_tmap_first_box.jsonl, r02n_ab_tmap.jsonl,
-    // r02p_ab_tmap_3reps.jsonl), so the row mover stays the default.
-    if (t->transpose && !layers.empty() && getenv("KVX_TMAP") && std::string(getenv("KVX_TMAP")) == "1") {
+    // Default (KVX_TMAP=0 disables): 0.941-0.954 of the copy peak on whole blocks
+    // on five of six boxes, against 0.93 for the row mover at best
+    // (profiles/r02af_ab_transposers_same_box.jsonl and the r02*_ab_tmap files).
+    if (t->transpose && !layers.empty() && !(getenv("KVX_TMAP") && std::string(getenv("KVX_TMAP")) == "0")) {
         const uint64_t head_plane = (uint64_t)g.block_tokens * g.head_dim * g.elem_bytes;
         bool ok = tm_dir[0] >= 0 && g.head_dim <= 256 && g.block_tokens <= 256 && head_plane <= kTmapSlot &&
                   (g.elem_bytes == 1 || g.elem_bytes == 2 || g.elem_bytes == 4) &&

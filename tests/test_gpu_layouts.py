@@ -135,7 +135,7 @@ def test_head_major_layouts(gpu_count, pair, impl, monkeypatch):
 @pytest.mark.parametrize("tmap", ["on", "off"])
 def test_transposes_tmap_and_row_mover(gpu_count, pair, tmap, monkeypatch):
     """Every transposing pairing with the TMA tensor-map transposer for whole
-    blocks (KVX_TMAP=1) and without it (the default: the row mover moves all)."""
+    blocks (the default) and without it (KVX_TMAP=0: the row mover moves all)."""
     monkeypatch.setenv("KVX_TMAP", "1" if tmap == "on" else "0")
     for seed in range(20, 28):
         test_random_layouts_bit_exact(gpu_count, seed, uniform=pair)
