@@ -39,6 +39,7 @@ struct TmSide {
     char* base;
     int32_t num_blocks;
     uint64_t ts, hs, kv, bs;
+    bool local;  // the pool is this device's own (tensor maps only over local memory)
 };
 }  // namespace
 
@@ -320,7 +321,7 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
             const kvx_pool* tmp = src->head_major() ? dst : src;  // token-major side
             const size_t ll = (size_t)(l - (tmp == src ? stage_begin(ob, so) : stage_begin(nb, sn)));
             tm_side.push_back({tmp->layer_base[ll], tmp->num_blocks, tmp->tok_stride(), tmp->head_stride(),
-                               tmp->kv_stride(), tmp->blk_stride()});
+                               tmp->kv_stride(), tmp->blk_stride(), !remote(tmp)});
             tm_dir.push_back(src->head_major() == dst->head_major() ? -1 : (dst->head_major() ? 1 : 0));
         }
         if (remote(dst)) t->has_peer_dst = true;
@@ -356,6 +357,9 @@ int kvx_begin(const kvx_transition_desc* d, kvx_transition** out) {
                   (g.elem_bytes == 1 || g.elem_bytes == 2 || g.elem_bytes == 4) &&
                   ((uint64_t)g.head_dim * g.elem_bytes) % 16 == 0 && tmap_encode() != nullptr;
         for (int dir : tm_dir) ok = ok && dir == tm_dir[0];
+        // tensor maps only over this device's own pools: a pulled token-major source
+        // or a pushed token-major destination behind NVLink stays on the row mover
+        for (const TmSide& s : tm_side) ok = ok && s.local;
         std::vector<CUtensorMap> maps(layers.size());
         const int hc = (int)std::min<uint64_t>((uint64_t)g.num_kv_heads, kTmapSlot / std::max<uint64_t>(1, head_plane));
         for (size_t i = 0; ok && i < layers.size(); ++i) {
