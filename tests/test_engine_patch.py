@@ -116,3 +116,17 @@ def test_measured_time_mode_c3_real_geometry(gpu_count):
     assert w0["scheduled_ms"] == w0["measured_ms"] < w0["modelled_ms"]
     first_sync = r["kv_sync_complete_ms"][0][1][0]
     assert first_sync == w0["issued_ms"] + w0["measured_ms"]
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_in_measured_time_mode(gpu_count, tmp_path):
+    """The reference's acceptance criteria with the engine on B200 time: every
+    KvSyncComplete / RefactorCommit at the measured device completion."""
+    rep = str(tmp_path / "acc_measured.jsonl")
+    out = _run("acceptance_kvx", {"PIPESIM_KVX": "measured", "PIPESIM_KVX_REPORT": rep}, timeout=3000)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    assert "ALL CRITERIA PASS" in out.stdout
+    r = _report(rep)
+    assert r["mode"] == "measured" and r["commits"] >= 2 and r["mismatched_words"] == 0
+    assert r["violation_mismatches"] == 0
+    assert all(w["scheduled_ms"] == w["measured_ms"] for w in r["wave_log"])
