@@ -157,7 +157,7 @@ int ensure_loaded(int device);
 // or V row per run) kTokVariant; KVX_BULK_CFG pins one variant for both,
 // KVX_BULK_CFG_SLAB / KVX_BULK_CFG_TOK one kind.
 using BulkFn = void (*)(const kvx::Seg*, int32_t, const kvx::LayerPtr*, int32_t, uint64_t, uint64_t, int32_t,
-                        int32_t, int32_t, unsigned long long*, unsigned long long*, int32_t);
+                        int32_t, int32_t, unsigned long long*, unsigned long long*);
 struct BulkVariant {
     int stages;
     uint32_t chunk;

@@ -507,29 +507,6 @@ __device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t 
                  "r"(smem_u32(smem)), "r"(bytes)
                  : "memory");
 }
-// The same copies with an L2 cache-policy hint (createpolicy): streaming
-// KV is read once and written once, so neither side needs to stay in L2.
-__device__ __forceinline__ uint64_t l2_policy(int hint) {
-    uint64_t p = 0;
-    if (hint == 1)
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    else if (hint == 2)
-        asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void bulk_g2s_hint(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar,
-                                              uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(smem)),
-        "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_s2g_hint(void* gmem, const void* smem, uint32_t bytes, uint64_t pol) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem),
-                 "r"(smem_u32(smem)), "r"(bytes), "l"(pol)
-                 : "memory");
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -657,8 +634,7 @@ struct UnitIter {
 //          kLag store groups drain while kStages - kLag slots load.
 // kPack = 1, kLag = 2 is the slab configuration (one 64 KiB chunk per slot).
 template <int kStages, uint32_t kChunk, int kLag = 2, int kPack = 1, class Iter>
-__device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint64_t* bars, int l2_hint = 0) {
-    const uint64_t pol = l2_policy(l2_hint);
+__device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint64_t* bars) {
     static_assert(kLag >= 1 && kLag < kStages, "lag");
     static_assert(kPack >= 1, "pack");
     for (int i = 0; i < kStages; ++i) mbar_init(&bars[i], 1);
@@ -687,10 +663,7 @@ __device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint6
         mbar_expect_tx(&bars[st], used);
         uint32_t off = 0;
         for (uint32_t q = 0; q < k; ++q) {
-            if (l2_hint)
-                bulk_g2s_hint(smem + (size_t)st * kChunk + off, src[q], pend_n[st][q], &bars[st], pol);
-            else
-                bulk_g2s(smem + (size_t)st * kChunk + off, src[q], pend_n[st][q], &bars[st]);
+            bulk_g2s(smem + (size_t)st * kChunk + off, src[q], pend_n[st][q], &bars[st]);
             off += pend_n[st][q];
         }
         return true;
@@ -706,10 +679,7 @@ __device__ __forceinline__ void bulk_stream(Iter& it, unsigned char* smem, uint6
         mbar_wait(&bars[st], parity);
         uint32_t off = 0;
         for (int q = 0; q < pend_k[st]; ++q) {
-            if (l2_hint)
-                bulk_s2g_hint(pend_dst[st][q], smem + (size_t)st * kChunk + off, pend_n[st][q], pol);
-            else
-                bulk_s2g(pend_dst[st][q], smem + (size_t)st * kChunk + off, pend_n[st][q]);
+            bulk_s2g(pend_dst[st][q], smem + (size_t)st * kChunk + off, pend_n[st][q]);
             off += pend_n[st][q];
         }
         bulk_commit();
@@ -741,8 +711,7 @@ template <int kStages, uint32_t kChunk, int kLag = 2, int kPack = 1>
 __global__ void __launch_bounds__(kBulkThreads)
 kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __restrict__ layers,
                 int32_t nlayers, uint64_t block_bytes, uint64_t token_bytes, int32_t block_tokens,
-                int32_t n_peer, int32_t peer_ctas, unsigned long long* t_start, unsigned long long* t_end,
-                int32_t l2_hint) {
+                int32_t n_peer, int32_t peer_ctas, unsigned long long* t_start, unsigned long long* t_end) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[kStages];
     __shared__ UnitDesc desc[2][kDescBatch];
@@ -785,7 +754,7 @@ kvx_bulk_kernel(const Seg* __restrict__ segs, int32_t nseg, const LayerPtr* __re
     it.my_units = my_units;
     it.nbatch = nbatch;
     it.chunk = kChunk;
-    if (it.load_unit()) bulk_stream<kStages, kChunk, kLag, kPack>(it, smem, bars, l2_hint);
+    if (it.load_unit()) bulk_stream<kStages, kChunk, kLag, kPack>(it, smem, bars);
     if (t_end) atomicMax(t_end, global_ns());  // after bulk_wait_all: this CTA's stores landed
 }
 

@@ -539,7 +539,6 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                 (uint32_t)(t->g.head_dim * t->g.elem_bytes), t->g.block_tokens, 0, t->has_peer_dst ? 1 : 0);
         } else if (t->use_bulk && (!t->has_peer_dst || t->peer_bulk)) {
             const int vi = slab ? t->bulk_variant_slab : t->bulk_variant_tok;
-            static const int l2_hint = getenv("KVX_L2_HINT") ? atoi(getenv("KVX_L2_HINT")) : 0;  // experiment
             const BulkVariant& bv = kBulkVariants[vi];
             // Grid: measured on B200 across boxes (profiles/grid_cross_box/): 96
             // one-CTA-per-SM streams are the best HBM-bound grid on every chip tried
@@ -582,8 +581,7 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
                                         block_bytes(t->g), token_bytes(t->g), t->g.block_tokens,
                                         t->n_peer_layers, peer_ctas,
                                         rec.timer >= 0 ? t->d_timer + rec.timer : nullptr,
-                                        rec.timer >= 0 ? t->d_timer + kvx_transition::kTimerSlots + rec.timer : nullptr,
-                                        l2_hint));
+                                        rec.timer >= 0 ? t->d_timer + kvx_transition::kTimerSlots + rec.timer : nullptr));
             if (t->head_tails && t->max_ctas > 0) {
                 // capped wave (HBM shared with serving): the tail mover runs after the
                 // bulk mover on the same stream, so the wave never holds more than
