@@ -1119,7 +1119,9 @@ def main():
 
     # ---- NVLink under the reference's disjoint grant (N > 1)
     nvl = None
-    if world > 1 and not fold and not args.no_nvlink_probe:
+    # (folded ranks share GPUs, so the probe is no measurement there; KVX_BENCH_FOLD_PROBE=1
+    # runs it anyway as a functional check of the N=8 path on a 4-GPU box)
+    if world > 1 and (not fold or os.environ.get("KVX_BENCH_FOLD_PROBE") == "1") and not args.no_nvlink_probe:
         nvl = nvlink_probe(kvx, torch, dist, plan, g, rank, world, dev, gather)
 
     # ---- NCCL baseline of the cross-GPU path (N > 1, when bytes cross GPUs)
