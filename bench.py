@@ -358,6 +358,52 @@ def host_observed_stall(make, t, reps: int = 8):
     return statistics.median(out), min(out), max(out)
 
 
+def serving_stall(make, t, old_pools, old_ranges, src_bt, stream, dev, reps: int = 8, read_bytes: int = 1 << 30):
+    """The device stall with a decode iteration between the last pre-barrier
+    wave and the barrier, as in the reference's timeline: the final wave moves
+    the tokens decode appended after the last snapshot (engine.cpp:491-507,
+    676-687), so at least one decode step runs between wave 0 and the
+    barrier.  The timed loop's step issues the final wave right behind wave
+    0's 17 GB mover instead, and the final wave then pays the write-back of
+    wave 0's dirty L2 lines (`scripts/final_wave_l2.py`: 74 vs 63 us).
+    Stand-in for the decode step, per rep: the append of exactly the rows the
+    final wave moves (kvx_pool_append_pattern: same payload, dirty in L2),
+    then `read_bytes` of reads (the step's attention reads of the KV cache,
+    which leave L2 holding clean lines).  Returns the median barrier ->
+    commit-result device time and the final-wave mover time (ms)."""
+    import torch
+    fin = next((w for w in reversed(t.waves) if w.final), None)
+    if fin is None:
+        return None
+    flush = torch.ones(read_bytes // 4, dtype=torch.float32, device=dev)
+    sp = stream.cuda_stream
+    st, fw = [], []
+    for rep in range(reps + 1):
+        tr = make()
+        w0 = t.events[0]
+        tr.begin_refactor((w0.req, w0.hi))
+        ev = run_events(tr, t.events[1:], stop_at_barrier=True)
+        for k, (b, _e) in enumerate(old_ranges):
+            if old_pools[k] is not None:
+                old_pools[k].append_pattern(SEED, b, fin.req, fin.lo, fin.hi, src_bt, stream=sp)
+        with torch.cuda.stream(stream):
+            flush.sum()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        run_events(tr, ev, lambda: a0.record(stream))
+        tr.on_refactor_commit((t.live_req, t.live_kv), wait=False)
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        res = tr.collect_commit()
+        assert res.violations == t.violations, res.violations
+        if rep:
+            st.append(a0.elapsed_time(a1))
+            mv = tr.move_timings()
+            fw.append(mv[-1][0] if mv else float("nan"))
+        tr.close()
+    del flush
+    return statistics.median(st), statistics.median(fw), min(st)
+
+
 def reference_condition_stall(make, t, plan, shape, stream, dev, reps: int = 4):
     """The stall under the reference's own conditions (engine.cpp:614-687):
     the new stages' weights are migrated WHILE wave 0 runs (same HBM; the
@@ -1083,6 +1129,13 @@ def main():
         th = torch.tensor([h_med, h_hi], dtype=torch.float64, device=dev)
         dist.all_reduce(th, op=dist.ReduceOp.MAX)
         h_med, h_hi = [float(x) for x in th.tolist()]
+    # ---- the device stall with a decode step between wave 0 and the barrier
+    #      (the reference's timeline; see serving_stall)
+    sv = serving_stall(make, t, old_pools, W.stage_ranges(L, t.old_boundaries), plan.src_bt, stream, dev)
+    if sv is not None and world > 1:
+        ts = torch.tensor(list(sv), dtype=torch.float64, device=dev)
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        sv = tuple(float(x) for x in ts.tolist())
     ref_cond = None
     if world == 1 and not args.no_weights:
         ref_cond = reference_condition_stall(make, t, plan, CONFIGS[args.config][1], stream, dev)
@@ -1222,7 +1275,14 @@ def main():
                   "host_observed_ms": round(h_med, 4), "host_observed_range_ms": [round(h_lo, 4), round(h_hi, 4)],
                   "host_note": "wall clock from the barrier handler call (after the host saw the earlier waves "
                                "complete) to the commit result on the host (engine.cpp:676-713)",
-                  "reference_condition": ref_cond},
+                  "reference_condition": ref_cond,
+                  "device_after_decode_ms": None if sv is None else round(sv[0], 4),
+                  "final_wave_after_decode_ms": None if sv is None else round(sv[1], 4),
+                  "after_decode_note": "as device_ms, with a decode step between the last pre-barrier wave and "
+                                       "the barrier, as in the reference's timeline (the final wave moves what "
+                                       "decode appended): the append of the final wave's rows, then 1 GiB of "
+                                       "KV-cache reads. device_ms issues the final wave right behind wave 0's "
+                                       "17 GB mover and so also pays the write-back of wave 0's dirty L2 lines"},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                 "ms_per_step": round(e2e_s * 1e3 / e2e_steps, 4)},
