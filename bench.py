@@ -384,7 +384,7 @@ def serving_stall(make, t, old_pools, old_ranges, src_bt, stream, dev, reps: int
         tr.begin_refactor((w0.req, w0.hi))
         ev = run_events(tr, t.events[1:], stop_at_barrier=True)
         for k, (b, _e) in enumerate(old_ranges):
-            if old_pools[k] is not None:
+            if old_pools[k] is not None and not old_pools[k].imported:  # this rank's own old stages
                 old_pools[k].append_pattern(SEED, b, fin.req, fin.lo, fin.hi, src_bt, stream=sp)
         with torch.cuda.stream(stream):
             flush.sum()
