@@ -109,7 +109,7 @@ def _ncu_dram(path: str):
     return (total or None), dur
 
 
-def ncu_traffic(cfg: str, timeout_s: float = 240.0):
+def ncu_traffic(cfg: str, timeout_s: float = 240.0, world: int = 1, placement: str = "affinity"):
     """DRAM traffic of the dominant launch (the wave-0 TMA bulk mover), taken
     IN THIS RUN: ncu (one pass, two dram counters, --clock-control none) over
     a child `bench.py --traffic-probe` that builds the same pools and issues
@@ -124,7 +124,8 @@ def ncu_traffic(cfg: str, timeout_s: float = 240.0):
     log = os.path.join("/tmp", f"kvx_traffic_{os.getpid()}.csv")
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
            "--clock-control", "none", "-k", "regex:kvx_bulk_kernel", "-c", "1", "--csv", "--log-file", log,
-           sys.executable, os.path.abspath(__file__), "--traffic-probe", "--config", cfg]
+           sys.executable, os.path.abspath(__file__), "--traffic-probe", "--config", cfg,
+           "--probe-world", str(world), "--placement", placement]
     try:
         out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s)
         if out.returncode != 0:
@@ -140,16 +141,21 @@ def ncu_traffic(cfg: str, timeout_s: float = 240.0):
 
 def traffic_probe(args):
     """Child of ncu_traffic (runs under ncu): the bench's pools for the config
-    and its wave 0, once; the first kvx_bulk_kernel launch is wave 0's mover."""
+    and its wave 0, once; the first kvx_bulk_kernel launch is wave 0's mover.
+    --probe-world N: rank 0's share of the N-GPU placement (its own pools
+    only; used when rank 0 moves no layer over NVLink)."""
     import torch
     from paper_2510_11938_b200 import kvx
     torch.cuda.set_device(0)
     plan = Plan(args.config)
     t = plan.t
     g = kvx.geometry(plan.L, plan.H, plan.D)
-    old_dev, new_dev = S.placement(plan.L, t.old_boundaries, t.new_boundaries, 1, "affinity")
+    old_dev, new_dev = S.placement(plan.L, t.old_boundaries, t.new_boundaries, args.probe_world, args.placement)
     old_pools, new_pools = S.setup_rank_pools(kvx, g, t.old_boundaries, t.new_boundaries, old_dev, new_dev, 0, 0,
                                               plan.old_blocks, plan.dst_blocks, all_gather=None, fill=None)
+    for j, (b, e) in enumerate(W.stage_ranges(plan.L, t.new_boundaries)):
+        if new_pools[j] is None:  # another rank's new stage: kvx_begin wants every pool; none of
+            new_pools[j] = kvx.Pool(0, g, e - b, plan.dst_blocks)  # rank 0's layers go there
     tr = kvx.Transition(g, t.old_boundaries, old_pools, t.new_boundaries, new_pools, 0, plan.N, plan.max_blocks,
                         plan.dst_blocks, plan.src_bt, epoch=t.epoch, max_sync_rounds=plan.scn.max_sync_rounds,
                         kv_bytes_per_token=plan.kv_bytes_per_token)
@@ -161,7 +167,8 @@ def traffic_probe(args):
         tr.wait()
     tr.close()
     for p in old_pools + new_pools:
-        p.close()
+        if p is not None:
+            p.close()
     return 0
 
 
@@ -877,6 +884,7 @@ def main():
     ap.add_argument("--no-nvlink-probe", action="store_true", help="N>1: skip the disjoint-grant NVLink wave")
     ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--probe-all-waves", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--probe-world", type=int, default=1, help=argparse.SUPPRESS)
     ap.add_argument("--layouts", default="blocks,blocks",
                     help="old,new pool layouts: blocks (FlashInfer NHD [blocks][2][B][H][D]), planes "
                          "(FlashAttention [2][blocks][B][H][D]) or heads (FlashInfer HND [blocks][2][H][B][D], "
@@ -1231,8 +1239,9 @@ def main():
                 "traffic": None, "kernel": "kvx_bulk_kernel (wave 0, slowest rank)",
                 "algorithmic_bytes_per_gpu": {"hbm_rw": [int(x) for x in hbm], "nvlink_out": [int(x) for x in out],
                                               "nvlink_in": [int(x) for x in inn]},
-                "traffic_note": "N>1: DRAM / NVLink bytes of the movers come from ncu on rank 0 "
-                                "(scripts/nvlink_r02.sh, profiles/), not from this run",
+                "traffic_note": "N>1: rank 0's wave-0 mover under ncu in this run when rank 0 moves no layer "
+                                "over NVLink (vs its own hbm_rw); NVLink bytes from ncu: scripts/nvlink_ncu.sh, "
+                                "profiles/r02j/",
                 "t_roof_ms": round(t_roof * 1e3, 4), "launch_ms": round(w0_avg, 4),
                 "peak_source": f"hbm {peak_kind}; nvlink 770 GB/s measured peer copy"}
 
@@ -1259,6 +1268,12 @@ def main():
         roof["traffic"], roof["traffic_source"] = ncu_traffic(args.config)
         if roof["traffic"]:
             roof["traffic_over_algorithmic"] = round(roof["traffic"] / w0_bytes, 4)
+    elif not args.no_ncu and not fold and out[0] == 0 and inn[0] == 0 and dev == 0:
+        # rank 0's share is local: the same wave-0 mover over its own layers
+        roof["traffic"], roof["traffic_source"] = ncu_traffic(args.config, world=n_gpus, placement=args.placement)
+        if roof["traffic"]:
+            roof["traffic_rank"] = 0
+            roof["traffic_over_algorithmic"] = round(roof["traffic"] / hbm[0], 4)
 
     value = plan.step_bytes * K / (dev_ms * 1e-3) / 1e9
     e2e_value = plan.step_bytes * e2e_steps / e2e_s / 1e9
