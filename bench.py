@@ -405,7 +405,7 @@ def serving_stall(make, t, old_pools, old_ranges, src_bt, stream, dev, reps: int
         if rep:
             st.append(a0.elapsed_time(a1))
             mv = tr.move_timings()
-            fw.append(mv[-1][0] if mv else float("nan"))
+            fw.append(mv[-1][0] if mv else 0.0)  # 0: no mover of this rank's own (max over ranks)
         tr.close()
     del flush
     return statistics.median(st), statistics.median(fw), min(st)
@@ -1020,15 +1020,18 @@ def main():
     n_waves = max((len(m) for m in mv), default=0)
     wave_ms = [round(statistics.median(m[i][0] for m in mv if len(m) > i), 4) for i in range(n_waves)]
 
-    tm = torch.tensor([dev_ms, stall_med, float(launches), w0_avg, float(w0_bytes)], dtype=torch.float64,
+    # a rank that launches no mover of its own (N=8 C3: the old-stage GPUs whose
+    # layers their receivers pull) reports 0 here and null in rank_wave0_move_ms
+    w0_red = w0_avg if w0_ms else 0.0
+    tm = torch.tensor([dev_ms, stall_med, float(launches), w0_red, float(w0_bytes)], dtype=torch.float64,
                       device=dev)
     rank_ms = [round(dev_ms / K, 4)]
-    rank_w0 = [round(w0_avg, 4)]
+    rank_w0 = [round(w0_avg, 4) if w0_ms else None]
     if world > 1:
         allv = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(world)]
-        dist.all_gather(allv, torch.tensor([dev_ms / K, w0_avg], dtype=torch.float64, device=dev))
+        dist.all_gather(allv, torch.tensor([dev_ms / K, w0_red], dtype=torch.float64, device=dev))
         rank_ms = [round(float(v[0]), 4) for v in allv]
-        rank_w0 = [round(float(v[1]), 4) for v in allv]
+        rank_w0 = [round(float(v[1]), 4) if float(v[1]) > 0 else None for v in allv]
         mx = tm.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = tm.clone()
