@@ -7,10 +7,14 @@ One process drives two GPUs; each sends 8.4 GB to the other at the same time.
             20 pushed layers (height, pitch = layer stride)
   ce2d_hbm  ce2d with a local 8.4 GB r+w copy on the same GPU beside it (the
             gather into the staging buffer)
+  ce1d_runs one 1-D copy per (layer, run): 5,120 cudaMemcpyAsync per GPU
+            (host issue time reported: the two GPUs are issued one after the other)
 Per-direction GB/s = bytes / max over the two GPUs of the CUDA-event time.
 Usage (gpurun --gpus 2): python scripts/ce_probe.py
 """
 import json
+import sys
+import time
 
 import torch
 from cuda.bindings import runtime as rt
@@ -47,6 +51,12 @@ def main():
             for l in range(L):
                 ck(rt.cudaMemcpyAsync(dst + l * P, src + l * P, P, kind, s))
             return L * P
+        if mode.startswith("ce1d_runs"):  # one 1-D copy per (layer, run): 5,120 calls per GPU
+            for l in range(L):
+                for r in range(runs):
+                    o = l * P + r * width
+                    ck(rt.cudaMemcpyAsync(dst + o, src + o, width, kind, s))
+            return runs * width * L
         for r in range(runs):
             ck(rt.cudaMemcpy2DAsync(dst + r * width, P, src + r * width, P, width, L, kind, s))
         if mode == "ce2d_hbm":
@@ -56,8 +66,9 @@ def main():
         return runs * width * L
 
     out = []
-    for mode in ("ce1d", "ce2d", "ce2d_hbm", "ce1d", "ce2d", "ce2d_hbm"):
-        times = []
+    modes = sys.argv[1].split(",") if len(sys.argv) > 1 else ["ce1d", "ce2d", "ce2d_hbm", "ce1d", "ce2d", "ce2d_hbm"]
+    for mode in modes:
+        times, hosts = [], []
         for rep in range(4):
             for d in devs:
                 torch.cuda.synchronize(d)
@@ -66,9 +77,11 @@ def main():
                 ev[d][0].record(st[d])
                 hs[d].wait_stream(st[d])
             nb = 0
+            h0 = time.perf_counter()
             for d in devs:
                 torch.cuda.set_device(d)
                 nb = issue(mode, d)
+            host_ms = (time.perf_counter() - h0) * 1e3
             for d in devs:
                 st[d].wait_stream(hs[d])
                 ev[d][1].record(st[d])
@@ -77,9 +90,11 @@ def main():
             t = max(ev[d][0].elapsed_time(ev[d][1]) for d in devs)
             if rep:
                 times.append(t)
+                hosts.append(host_ms)
         t = sorted(times)[len(times) // 2]
         line = {"mode": mode, "bytes_per_direction": nb, "ms": round(t, 3),
-                "GBps_per_direction": round(nb / (t * 1e-3) / 1e9, 1), "frac_770": round(nb / (t * 1e-3) / 770e9, 4)}
+                "GBps_per_direction": round(nb / (t * 1e-3) / 1e9, 1), "frac_770": round(nb / (t * 1e-3) / 770e9, 4),
+                "host_issue_ms_both_gpus": round(sorted(hosts)[len(hosts) // 2], 3)}
         print(json.dumps(line), flush=True)
         out.append(line)
 
