@@ -514,7 +514,9 @@ int kvx_wave(kvx_transition* t, uint64_t epoch, int32_t n, const int32_t* req, c
             // whole blocks: the TMA transposer; partial blocks: the row mover beside it
             // on the side stream (joined before the wave's end event)
             const uint32_t head_plane = (uint32_t)(t->g.block_tokens * t->g.head_dim * t->g.elem_bytes);
-            int64_t tgrid = std::min<int64_t>(units, 96);
+            // 128 CTAs: 0.957-0.969 of the copy peak against 0.946-0.954 on 96 (112 and
+            // 136 slower still) on two boxes (profiles/r02am_tmap_grid_sweep*.jsonl)
+            int64_t tgrid = std::min<int64_t>(units, 128);
             if (const char* tg = getenv("KVX_TMAP_GRID")) tgrid = std::max<int64_t>(1, atoll(tg));
             if (t->max_ctas > 0) tgrid = std::min<int64_t>(tgrid, t->max_ctas);
             kvx::kvx_tmap_kernel<kTmapStages, kTmapLag><<<(unsigned)std::max<int64_t>(1, tgrid), 32,
